@@ -1,0 +1,261 @@
+/*
+ * fsb200.h — C ABI of the B200-native dense-mapping hot path of arXiv 1909.07545
+ * (non-rectified variational fisheye stereo, anisotropic TGV-L1 along epipolar
+ * trajectory fields).
+ *
+ * The reference package (`fisheyestereo`, pure Python/NumPy) has no FFI layer:
+ * its boundary for this path is the Python function
+ *     fisheyestereo.solve_pyramid(i0, i1, rig, params, collect_diagnostics=False,
+ *                                 traj_override=None) -> StereoResult
+ * (reference pkg/src/fisheyestereo/solver.py:401-452) plus the per-stage functions
+ * its tests call directly. Every entry point below replaces one of those
+ * functions; the replaced reference interface is cited on each declaration.
+ * The Python host mirror (paper_1909_07545_b200/) binds these through ctypes.
+ *
+ * Conventions (all entry points):
+ *   - every array argument is a DEVICE pointer owned by the caller; nothing is
+ *     allocated inside (scratch is caller-provided, sized by *_bytes helpers);
+ *   - images / scalar fields are row-major float32 (H, W); vector fields are
+ *     interleaved float32 (H, W, 2) with channel order (x, y); masks are uint8
+ *     0/1 (H, W) — the layout of reference rasters.py:1-11;
+ *   - work is enqueued asynchronously on `stream` (a cudaStream_t, may be 0);
+ *   - the return value is 0 on success, a cudaError_t (> 0) if a launch failed,
+ *     or FSB_EINVAL (-1) / FSB_ENOSPC (-2) / FSB_EDOMAIN (-3) for argument errors
+ *     (the reference's ValueError cases);
+ *   - entry points are stateless and re-entrant; one stream per concurrent solve.
+ */
+#ifndef FSB200_H_
+#define FSB200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSB_OK 0
+#define FSB_EINVAL (-1)   /* bad shape / null pointer / bad parameter (ValueError) */
+#define FSB_ENOSPC (-2)   /* caller-provided scratch/workspace too small          */
+#define FSB_EDOMAIN (-3)  /* trajectory field on a rotated or zero-baseline rig   */
+
+#define FSB_CAM_PINHOLE 0     /* reference camera.py:87-106  */
+#define FSB_CAM_UNIFIED 1     /* reference camera.py:109-136 */
+#define FSB_CAM_POLYNOMIAL 2  /* reference camera.py:139-190 */
+
+/* Lens + image grid; mirrors CameraBase and its subclasses (camera.py:47-190).
+ * Distances in pixels, fov = full field-of-view angle in radians. */
+typedef struct fsb_camera {
+  int32_t model;
+  int32_t width;
+  int32_t height;
+  int32_t reserved;
+  double fx, fy, cx, cy, fov;
+  double xi;    /* unified model only */
+  double k[4];  /* polynomial model only: r/f = k1 t + k2 t^3 + k3 t^5 + k4 t^7 */
+} fsb_camera;
+
+/* StereoRig(cam0, cam1, RelativePose(R, t)) with X1 = R X0 + t (camera.py:245-287). */
+typedef struct fsb_rig {
+  fsb_camera cam0;
+  fsb_camera cam1;
+  double rotation[9];  /* row-major */
+  double translation[3];
+} fsb_rig;
+
+/* SolverParams (solver.py:36-69). */
+typedef struct fsb_params {
+  double lam, alpha0, alpha1, beta, eta;
+  int32_t warp_iters, pd_iters;
+  double du_max;
+  int32_t pyramid_levels;
+  int32_t min_width;
+  double pyramid_scale;
+  double epsilon_scale;
+  double tensor_sigma;
+  double theta;
+} fsb_params;
+
+/* Per-iteration invariants (Diagnostics, solver.py:104-119). Device arrays the
+ * caller sizes with fsb_diag_counts(); any pointer may be NULL. */
+typedef struct fsb_diag {
+  float* max_p_norm;    /* one per primal-dual iteration, all levels  */
+  float* max_q_norm;    /* one per primal-dual iteration, all levels  */
+  float* max_du;        /* one per warp iteration, all levels         */
+  double* mean_abs_du;  /* one per warp iteration, all levels         */
+} fsb_diag;
+
+/* ---------------------------------------------------------------- geometry */
+
+/* CameraBase.fov_mask (camera.py:79-84). mask: (cam.height, cam.width) uint8. */
+int fsb_fov_mask(const fsb_camera* cam, uint8_t* mask, void* scratch, size_t scratch_bytes,
+                 void* stream);
+size_t fsb_fov_mask_scratch_bytes(const fsb_camera* cam);
+
+/* camera.unproject / camera.project on n points (camera.py:101,115,126,155,171).
+ * pix: (n,2) f64, rays/points: (n,3) f64, valid: (n) u8. Invalid outputs are NaN.
+ * The polynomial model iterates Newton until every point of the call converged
+ * (camera.py:177-185); scratch holds that convergence count. */
+int fsb_unproject(const fsb_camera* cam, const double* pix, int64_t n, double* rays,
+                  uint8_t* valid, void* scratch, size_t scratch_bytes, void* stream);
+int fsb_project(const fsb_camera* cam, const double* pts, int64_t n, double* pix,
+                uint8_t* valid, void* stream);
+size_t fsb_unproject_scratch_bytes(void);
+
+/* generate_calibration_field (fields.py:34-45). field: (H,W,2) f64, ok: (H,W) u8. */
+int fsb_calibration_field(const fsb_rig* rig, double* field, uint8_t* ok, void* scratch,
+                          size_t scratch_bytes, void* stream);
+
+/* calibrate_second_image (solver.py:389-398): i1c = masked bicubic of i1 at
+ * x + calibration(x), mask1 = cam1 FOV mask (computed inside when mask1 == NULL).
+ * i1: (cam1.height, cam1.width) f32; i1c, ok: cam0 grid. */
+int fsb_calibrate_second_image(const fsb_rig* rig, const float* i1, const uint8_t* mask1,
+                               float* i1c, uint8_t* ok, void* scratch, size_t scratch_bytes,
+                               void* stream);
+size_t fsb_calibrate_scratch_bytes(const fsb_rig* rig);
+
+/* generate_trajectory_field (fields.py:48-108) for the translation-only rig
+ * (cam, cam, (I, t)); fp64 throughout, dirs stored f32 (H,W,2), ok u8 (H,W).
+ * Returns FSB_EDOMAIN for a zero baseline (fields.py:63-66). */
+int fsb_trajectory_field(const fsb_camera* cam, const double t[3], double epsilon_scale,
+                         double depth, float* dirs, uint8_t* ok, void* scratch,
+                         size_t scratch_bytes, void* stream);
+size_t fsb_trajectory_scratch_bytes(const fsb_camera* cam);
+
+/* ---------------------------------------------------------------- rasters */
+
+/* sample_bicubic (rasters.py:57-141) with its mask-aware fallback chain.
+ * field: (h,w,c) f32 interleaved, c in {1,2}; pos: (n,2) f64 (x,y);
+ * out: (n,c) f32 (NaN where invalid); valid: (n) u8. Accumulates in f64 when
+ * acc64 != 0, else in f32 (the per-warp hot-path precision). */
+int fsb_sample_bicubic(const float* field, int32_t h, int32_t w, int32_t c,
+                       const uint8_t* mask, const double* pos, int64_t n, float* out,
+                       uint8_t* valid, int32_t acc64, void* stream);
+
+/* gradient / divergence (rasters.py:144-172). u: (h,w); g, p: (h,w,2). */
+int fsb_gradient(const float* u, const uint8_t* mask, int32_t h, int32_t w, float* g,
+                 void* stream);
+int fsb_divergence(const float* p, const uint8_t* mask, int32_t h, int32_t w, float* div,
+                   void* stream);
+
+/* smooth_masked (rasters.py:185-191), Gaussian with SciPy's reflect/truncate=4. */
+int fsb_smooth_masked(const float* f, const uint8_t* mask, int32_t h, int32_t w,
+                      double sigma, float* out, void* scratch, size_t scratch_bytes,
+                      void* stream);
+size_t fsb_smooth_scratch_bytes(int32_t h, int32_t w);
+
+/* pyramid_shapes (rasters.py:207-221): writes up to max_levels (h,w) pairs,
+ * finest first; returns the level count or FSB_EINVAL. Host-only. */
+int fsb_pyramid_shapes(int32_t h, int32_t w, int32_t levels, double scale, int32_t min_width,
+                       int32_t* shapes, int32_t max_levels);
+
+/* downsample_area (rasters.py:228-260). */
+int fsb_downsample_area(const float* src, const uint8_t* mask, int32_t fh, int32_t fw,
+                        float* dst, uint8_t* dmask, int32_t ch, int32_t cw, void* stream);
+
+/* upsample_state (rasters.py:276-297). */
+int fsb_upsample_state(const float* u, const float* wv, const uint8_t* mask, int32_t sh,
+                       int32_t sw, const uint8_t* dmask, int32_t dh, int32_t dw,
+                       float* u_out, float* w_out, void* stream);
+
+/* ---------------------------------------------------------------- solver */
+
+/* Device view of one pyramid level's solver buffers (all (h,w) f32 planes
+ * unless noted; pitch == w). Filled by the caller (or fsb_level_bind). */
+typedef struct fsb_level {
+  int32_t h, w;
+  const float* i0;       /* level image 0                                 */
+  const float* i1;       /* level (calibrated) image 1                    */
+  const uint8_t* mask;   /* level solve mask                              */
+  const float* traj;     /* (h,w,2) trajectory directions                 */
+  const uint8_t* traj_ok;
+  float* tensor;         /* 3 planes a,b,c    (compute_tensor)            */
+  float* steps;          /* 3 planes sigma_p, tau_u, tau_v                */
+  float* u;  float* u_bar;
+  float* v;  float* v_bar;  /* 2 planes each                              */
+  float* p;              /* 2 planes                                       */
+  float* q;              /* 4 planes                                       */
+  float* wv;             /* (h,w,2) accumulated warp                       */
+  float* u_omega;
+  float* iu;  float* rho0;
+  float* i1w;            /* warped image                                   */
+  uint8_t* i1w_ok;       /* warp_ok & mask                                 */
+  float* dirs;           /* (h,w,2) sampled unit directions                */
+  uint8_t* dir_ok;
+  double* partials;      /* reduction scratch (fsb_level_partials(h,w))    */
+} fsb_level;
+
+size_t fsb_level_partials(int32_t h, int32_t w);
+
+/* compute_tensor(smooth_masked(i0)) + precondition_steps (solver.py:319-321,
+ * 122-161, 246-276). scratch >= fsb_smooth_scratch_bytes(h,w). */
+int fsb_level_setup(const fsb_level* lv, const fsb_params* prm, void* scratch,
+                    size_t scratch_bytes, void* stream);
+
+/* compute_tensor (solver.py:122-141) on an already-smoothed image; tensor
+ * out: 3 planes a,b,c. */
+int fsb_compute_tensor(const float* smoothed, const uint8_t* mask, int32_t h, int32_t w,
+                       double beta, double eta, float* tensor, void* scratch,
+                       size_t scratch_bytes, void* stream);
+
+/* precondition_steps (solver.py:246-276) from tensor planes; steps out: 3 planes
+ * sigma_p, tau_u, tau_v (sigma_q = 1 / (2 alpha0) is a scalar). */
+int fsb_precondition_steps(const float* tensor, const uint8_t* mask, int32_t h, int32_t w,
+                           const fsb_params* prm, float* steps, void* scratch,
+                           size_t scratch_bytes, void* stream);
+
+/* Warp-loop prologue (solver.py:332-346 with image_derivative_along 192-202):
+ * i1w, dirs, I_u, rho0, and the u_omega / u_bar / v_bar resets. */
+int fsb_warp_linearize(const fsb_level* lv, void* stream);
+
+/* `iters` calls of primal_dual_iterate (solver.py:279-303). diag_p/diag_q, if
+ * non-NULL, receive one max-norm per iteration (solver.py:350-354). */
+int fsb_pd_iterate(const fsb_level* lv, const fsb_params* prm, int32_t iters, float* diag_p,
+                   float* diag_q, void* stream);
+
+/* thresholding_step (solver.py:205-218), elementwise on n f64 values (the same
+ * device function runs fused, in f32, inside the primal kernel). */
+int fsb_thresholding_step(const double* u_hat, const double* rho_hat, const double* iu,
+                          const double* tau_u, double lam, int64_t n, double* out, void* stream);
+
+/* Warp-loop epilogue (solver.py:356-365): clip, accumulate u and w. */
+int fsb_warp_finish(const fsb_level* lv, const fsb_params* prm, float* diag_max_du,
+                    double* diag_mean_du, void* stream);
+
+/* solve_level (solver.py:306-367): setup + N warps of (linearize, K PD, finish).
+ * u and wv hold the initial WarpState on entry and the result on exit; v, p, q,
+ * u_bar, v_bar are (re)initialised inside as the reference does. */
+int fsb_solve_level(const fsb_level* lv, const fsb_params* prm, const fsb_diag* diag,
+                    int64_t diag_pd_offset, int64_t diag_warp_offset, void* scratch,
+                    size_t scratch_bytes, void* stream);
+
+/* ---------------------------------------------------------------- pyramid */
+
+/* Number of levels / diagnostic slots for a frame of the given size. */
+int fsb_diag_counts(int32_t h, int32_t w, const fsb_params* prm, int64_t* n_pd,
+                    int64_t* n_warp);
+
+/* Workspace for fsb_solve_pyramid. */
+size_t fsb_solve_pyramid_workspace_bytes(const fsb_rig* rig, const fsb_params* prm);
+
+/* solve_pyramid (solver.py:401-452), whole frame on device.
+ * i0: cam0 grid f32; i1: cam1 grid f32. Outputs on the cam0 grid:
+ * u (H,W), w (H,W,2), v (H,W,2), mask (H,W) u8, i1c (H,W).
+ * traj_dirs / traj_ok: optional per-level override arrays (coarsest first,
+ * level sizes from fsb_pyramid_shapes), i.e. the reference's traj_override
+ * (solver.py:437-438); pass NULL to generate trajectory fields on device.
+ * diag may be NULL. */
+int fsb_solve_pyramid(const fsb_rig* rig, const fsb_params* prm, const float* i0,
+                      const float* i1, const float* const* traj_dirs,
+                      const uint8_t* const* traj_ok, void* workspace, size_t workspace_bytes,
+                      float* u, float* w, float* v, uint8_t* mask, float* i1c,
+                      const fsb_diag* diag, void* stream);
+
+/* Library build identification, e.g. "fsb200 sm_100a". */
+const char* fsb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSB200_H_ */

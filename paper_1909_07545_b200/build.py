@@ -1,0 +1,86 @@
+"""Build libfsb200.so (the C-ABI of include/fsb200.h) in-tree with nvcc for sm_100a.
+
+    python -m paper_1909_07545_b200.build [--force] [--verbose]
+
+Translation units with fp64 geometry/setup math are compiled with -fmad=false so
+their rounding sequence follows NumPy's (no FMA contraction); the fp32 hot-path
+units keep contraction on.
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+BUILD = PKG / "_build"
+LIB = PKG / "libfsb200.so"
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+          "-I", str(ROOT / "include")]
+# (source, extra flags)
+UNITS = [
+    ("fields.cu", ["-fmad=false"]),
+    ("rasters.cu", ["-fmad=false"]),
+    ("setup.cu", ["-fmad=false"]),
+    ("pd.cu", []),
+    ("solver.cu", []),
+]
+HEADERS = [CSRC / "fsb_common.cuh", ROOT / "include" / "fsb200.h"]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.sep not in cand or Path(cand).exists()):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _stale(target: Path, deps: list[Path]) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    objs = []
+    for src, extra in UNITS:
+        s = CSRC / src
+        o = BUILD / (s.stem + ".o")
+        objs.append(o)
+        if force or _stale(o, [s, *HEADERS, Path(__file__)]):
+            cmd = [nvcc(), *ARCH, *COMMON, *extra, "-c", str(s), "-o", str(o)]
+            if ptxas_verbose:
+                cmd += ["-Xptxas", "-v"]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.run(cmd, check=True)
+    if force or _stale(LIB, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    return LIB
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--ptxas", action="store_true", help="print ptxas register/smem usage")
+    a = ap.parse_args(argv)
+    out = build(force=a.force, verbose=a.verbose, ptxas_verbose=a.ptxas)
+    print(out)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

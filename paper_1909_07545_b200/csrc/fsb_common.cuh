@@ -1,0 +1,298 @@
+// Shared device code: launch helpers, fp64 lens models, mask-aware bicubic.
+//
+// Everything here is a from-scratch B200 restatement of the reference's
+// per-pixel math; the reference file:line each function follows is cited.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/fsb200.h"
+
+#define FSB_INLINE __device__ __forceinline__
+
+namespace fsb {
+
+constexpr double kPi = 3.14159265358979311599796346854;  // np.pi
+constexpr int kPolyMaxIter = 50;                          // camera.py:31
+constexpr double kPolyTol = 1e-10;                        // camera.py:30
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? FSB_OK : static_cast<int>(e);
+}
+
+inline dim3 grid2d(int w, int h, dim3 blk) {
+  return dim3((unsigned)((w + blk.x - 1) / blk.x), (unsigned)((h + blk.y - 1) / blk.y), 1);
+}
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------- lens models
+// All fp64 (the trajectory field needs fp64 finite differences).
+// Translation units that include these are compiled with -fmad=false so the
+// rounding sequence follows NumPy's (no contraction), see build.py.
+
+struct Cam {
+  int model, width, height;
+  double fx, fy, cx, cy, fov, xi, k0, k1, k2, k3;
+};
+
+inline Cam make_cam(const fsb_camera& c) {
+  Cam d;
+  d.model = c.model; d.width = c.width; d.height = c.height;
+  d.fx = c.fx; d.fy = c.fy; d.cx = c.cx; d.cy = c.cy; d.fov = c.fov; d.xi = c.xi;
+  d.k0 = c.k[0]; d.k1 = c.k[1]; d.k2 = c.k[2]; d.k3 = c.k[3];
+  return d;
+}
+
+// _ray_angles (camera.py:41-44)
+FSB_INLINE double ray_angle(double x, double y, double z) { return atan2(hypot(x, y), z); }
+
+// np.linalg.norm over a trailing axis of 3: sqrt((x*x + y*y) + z*z)
+FSB_INLINE double norm3(double x, double y, double z) {
+  return sqrt(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+}
+
+// PolynomialFisheyeCamera._radial / _radial_deriv (camera.py:145-153)
+FSB_INLINE double poly_radial(const Cam& c, double t) {
+  double t2 = t * t;
+  return t * (c.k0 + t2 * (c.k1 + t2 * (c.k2 + t2 * c.k3)));
+}
+FSB_INLINE double poly_radial_deriv(const Cam& c, double t) {
+  double t2 = t * t;
+  return c.k0 + t2 * (3.0 * c.k1 + t2 * (5.0 * c.k2 + t2 * 7.0 * c.k3));
+}
+
+// One damped Newton update (camera.py:178-183); returns |step| < tol.
+FSB_INLINE bool poly_newton_step(const Cam& c, double rd, double& theta) {
+  double f = poly_radial(c, theta) - rd;
+  double df = poly_radial_deriv(c, theta);
+  double step = f / (fabs(df) > 1e-12 ? df : 1e-12);
+  step = fmin(fmax(step, -0.5), 0.5);
+  theta = fmin(fmax(theta - step, 0.0), kPi);
+  return fabs(step) < kPolyTol;
+}
+
+FSB_INLINE void poly_start(const Cam& c, double px, double py, double& rd, double& phi,
+                           double& theta) {
+  double mx = (px - c.cx) / c.fx, my = (py - c.cy) / c.fy;
+  rd = hypot(mx, my);
+  phi = atan2(my, mx);
+  theta = rd / fmax(fabs(c.k0), 1e-6);
+}
+
+// Number of Newton iterations this pixel needs before |step| < tol, capped at
+// kPolyMaxIter. The reference loops until ALL pixels of the call converged
+// (camera.py:177-185), so every pixel runs max-over-pixels of this count.
+FSB_INLINE int poly_conv_iters(const Cam& c, double px, double py) {
+  double rd, phi, theta;
+  poly_start(c, px, py, rd, phi, theta);
+  for (int it = 1; it <= kPolyMaxIter; ++it)
+    if (poly_newton_step(c, rd, theta)) return it;
+  return kPolyMaxIter;
+}
+
+// camera.unproject for one pixel (camera.py:101-106, 126-136, 171-190).
+// `poly_iters` is the call-wide Newton iteration count (ignored otherwise).
+// Returns validity; ray is the unit ray (left unspecified when invalid).
+FSB_INLINE bool cam_unproject(const Cam& c, double px, double py, int poly_iters, double& rx,
+                              double& ry, double& rz) {
+  const double half_fov = 0.5 * c.fov + 1e-12;
+  if (c.model == FSB_CAM_POLYNOMIAL) {
+    double rd, phi, theta;
+    poly_start(c, px, py, rd, phi, theta);
+    bool conv = false;
+    for (int it = 0; it < poly_iters; ++it) conv = poly_newton_step(c, rd, theta);
+    double st = sin(theta);
+    rx = st * cos(phi);
+    ry = st * sin(phi);
+    rz = cos(theta);
+    return conv && theta <= half_fov;
+  }
+  double mx = (px - c.cx) / c.fx, my = (py - c.cy) / c.fy;
+  if (c.model == FSB_CAM_PINHOLE) {
+    double n = norm3(mx, my, 1.0);
+    rx = mx / n; ry = my / n; rz = 1.0 / n;
+    return ray_angle(rx, ry, rz) <= half_fov;
+  }
+  // unified
+  double r2 = __dadd_rn(__dmul_rn(mx, mx), __dmul_rn(my, my));
+  double disc = 1.0 + (1.0 - c.xi * c.xi) * r2;
+  bool valid = disc >= 0.0;
+  double eta = (c.xi + sqrt(fmax(disc, 0.0))) / (1.0 + r2);
+  double x = eta * mx, y = eta * my, z = eta - c.xi;
+  double n = fmax(norm3(x, y, z), 1e-300);
+  rx = x / n; ry = y / n; rz = z / n;
+  return valid && ray_angle(rx, ry, rz) <= half_fov;
+}
+
+// camera.project for one point (camera.py:91-99, 115-124, 155-169).
+FSB_INLINE bool cam_project(const Cam& c, double X, double Y, double Z, double& px, double& py) {
+  const double half_fov = 0.5 * c.fov + 1e-12;
+  if (c.model == FSB_CAM_PINHOLE) {
+    bool valid = Z > 1e-12;
+    double zs = valid ? Z : 1.0;
+    px = (c.fx * X) / zs + c.cx;
+    py = (c.fy * Y) / zs + c.cy;
+    return valid && ray_angle(X, Y, Z) <= half_fov;
+  }
+  if (c.model == FSB_CAM_UNIFIED) {
+    double rho = norm3(X, Y, Z);
+    double denom = Z + c.xi * rho;
+    bool valid = (denom > 1e-12) && (rho > 0.0);
+    double d = valid ? denom : 1.0;
+    px = (c.fx * X) / d + c.cx;
+    py = (c.fy * Y) / d + c.cy;
+    return valid && ray_angle(X, Y, Z) <= half_fov;
+  }
+  double theta = ray_angle(X, Y, Z);
+  double rxy = hypot(X, Y);
+  double safe = fmax(rxy, 1e-300);
+  double d = poly_radial(c, theta);
+  px = ((c.fx * d) * X) / safe + c.cx;
+  py = ((c.fy * d) * Y) / safe + c.cy;
+  if (rxy == 0.0) { px = c.cx; py = c.cy; }
+  return theta <= half_fov && norm3(X, Y, Z) > 0.0;
+}
+
+// ---------------------------------------------------------------- bicubic
+// sample_bicubic (rasters.py:45-141): Catmull-Rom on the 4x4 stencil when all
+// 16 taps are in bounds and in mask; else bilinear renormalised over the valid
+// inner 2x2 (weight sum > 1e-12); else the nearest valid tap (strict '<' in
+// scan order dy outer, dx inner); else invalid. Acc = float on the per-warp hot
+// path, double for the once-per-frame/level gathers.
+
+template <typename Acc>
+FSB_INLINE void cubic_weights(Acc f, Acc w[4]) {  // rasters.py:45-54
+  Acc f2 = f * f, f3 = f2 * f;
+  w[0] = (Acc(-0.5) * f + f2) - Acc(0.5) * f3;
+  w[1] = (Acc(1.0) - Acc(2.5) * f2) + Acc(1.5) * f3;
+  w[2] = (Acc(0.5) * f + Acc(2.0) * f2) - Acc(1.5) * f3;
+  w[3] = Acc(-0.5) * f2 + Acc(0.5) * f3;
+}
+
+// Split a continuous position into the stencil base and fraction. Returns false
+// for non-finite positions or when no tap of the stencil can be in bounds
+// (the reference's any_valid & finite is then False).
+template <typename Acc>
+FSB_INLINE bool split_pos(double x, double y, int h, int w, int& ix, int& iy, Acc& fx, Acc& fy) {
+  if (!isfinite(x) || !isfinite(y)) return false;
+  double flx = floor(x), fly = floor(y);
+  if (flx < -2.0 || flx > (double)w || fly < -2.0 || fly > (double)h) return false;
+  ix = (int)flx; iy = (int)fly;
+  fx = (Acc)(x - flx);
+  fy = (Acc)(y - fly);
+  return true;
+}
+
+template <int C>
+FSB_INLINE void load_tap(const float* __restrict__ f, int idx, float v[C]) {
+  if constexpr (C == 1) {
+    v[0] = __ldg(f + idx);
+  } else {
+    float2 t = __ldg(reinterpret_cast<const float2*>(f) + idx);
+    v[0] = t.x; v[1] = t.y;
+  }
+}
+
+template <int C, typename Acc>
+FSB_INLINE bool bicubic_at(const float* __restrict__ field, const uint8_t* __restrict__ mask, int h,
+                           int w, int ix, int iy, Acc fx, Acc fy, Acc out[C]) {
+  Acc wx[4], wy[4];
+  cubic_weights(fx, wx);
+  cubic_weights(fy, wy);
+  Acc cub[C], bil[C], near[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) { cub[k] = Acc(0); bil[k] = Acc(0); near[k] = Acc(0); }
+  Acc bws = Acc(0);
+  Acc nd2 = Acc(INFINITY);
+  bool all_ok = true, any_ok = false;
+  const Acc bx[2] = {Acc(1) - fx, fx};
+  const Acc by[2] = {Acc(1) - fy, fy};
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int r = iy + a - 1;
+    const bool rin = (unsigned)r < (unsigned)h;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int c = ix + b - 1;
+      const bool ok = rin && (unsigned)c < (unsigned)w && __ldg(mask + (size_t)r * w + c);
+      float vf[C];
+#pragma unroll
+      for (int k = 0; k < C; ++k) vf[k] = 0.f;
+      if (ok) load_tap<C>(field, r * w + c, vf);
+      all_ok &= ok;
+      any_ok |= ok;
+      const Acc wt = wy[a] * wx[b];
+#pragma unroll
+      for (int k = 0; k < C; ++k) cub[k] += wt * (Acc)vf[k];
+      if (a >= 1 && a <= 2 && b >= 1 && b <= 2) {
+        const Acc bw = ok ? by[a - 1] * bx[b - 1] : Acc(0);
+#pragma unroll
+        for (int k = 0; k < C; ++k) bil[k] += bw * (Acc)vf[k];
+        bws += bw;
+      }
+      const Acc ddx = Acc(b - 1) - fx, ddy = Acc(a - 1) - fy;
+      const Acc d2 = ddx * ddx + ddy * ddy;
+      if (ok && d2 < nd2) {
+        nd2 = d2;
+#pragma unroll
+        for (int k = 0; k < C; ++k) near[k] = (Acc)vf[k];
+      }
+    }
+  }
+  if (all_ok) {
+#pragma unroll
+    for (int k = 0; k < C; ++k) out[k] = cub[k];
+  } else if (bws > Acc(1e-12)) {
+#pragma unroll
+    for (int k = 0; k < C; ++k) out[k] = bil[k] / bws;
+  } else {
+#pragma unroll
+    for (int k = 0; k < C; ++k) out[k] = near[k];
+  }
+  return any_ok;
+}
+
+// Full sample at a continuous position: returns validity, out untouched when
+// invalid.
+template <int C, typename Acc>
+FSB_INLINE bool bicubic_sample(const float* __restrict__ field, const uint8_t* __restrict__ mask,
+                               int h, int w, double x, double y, Acc out[C]) {
+  int ix, iy;
+  Acc fx, fy;
+  if (!split_pos<Acc>(x, y, h, w, ix, iy, fx, fy)) return false;
+  return bicubic_at<C, Acc>(field, mask, h, w, ix, iy, fx, fy, out);
+}
+
+// ---------------------------------------------------------------- reductions
+// Max of non-negative floats/doubles via integer atomicMax on the bit pattern
+// (order-independent, hence deterministic).
+FSB_INLINE float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+FSB_INLINE double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+FSB_INLINE double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+FSB_INLINE void atomic_max_nonneg(float* addr, float v) {
+  atomicMax(reinterpret_cast<int*>(addr), __float_as_int(v));
+}
+FSB_INLINE void atomic_max_nonneg(double* addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(addr),
+            (unsigned long long)__double_as_longlong(v));
+}
+
+}  // namespace fsb

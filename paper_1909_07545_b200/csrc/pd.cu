@@ -1,0 +1,303 @@
+// K5 / K6 / K8: per-warp linearisation, the primal-dual iteration, and the
+// warp epilogue. fp32 compute and storage.
+//
+// Reference: solver.py:279-303 (primal_dual_iterate), solver.py:331-365 (warp
+// loop body), solver.py:192-218 (image_derivative_along, thresholding_step),
+// rasters.py:144-182 (gradient, divergence, edge indicators).
+//
+// Layout: every per-pixel quantity is a row-major fp32 plane of h*w (pitch w);
+// multi-channel state (v, v_bar, p, q, tensor, steps) is stored as consecutive
+// planes so every load of a warp is a coalesced 128-byte line.
+
+#include "fsb_common.cuh"
+
+namespace fsb {
+
+constexpr int kBX = 32, kBY = 8;
+
+struct PD {
+  int h, w;
+  size_t n;
+  const uint8_t* __restrict__ m;
+  const float* __restrict__ T;   // a,b,c planes
+  const float* __restrict__ S;   // sigma_p, tau_u, tau_v planes
+  const float* __restrict__ iu;
+  const float* __restrict__ rho0;
+  const float* __restrict__ u_omega;
+  float* u; float* u_bar; float* v; float* v_bar; float* p; float* q;
+  float lam, alpha0, alpha1, theta, sigma_q;
+};
+
+__device__ __forceinline__ bool ex_at(const uint8_t* __restrict__ m, int w, int x, size_t i) {
+  return x + 1 < w && m[i] && m[i + 1];
+}
+__device__ __forceinline__ bool ey_at(const uint8_t* __restrict__ m, int h, int w, int y, size_t i) {
+  return y + 1 < h && m[i] && m[i + w];
+}
+
+// thresholding_step (solver.py:205-218): the closed-form prox of
+// lam*|rho_hat + (u - u_hat) iu| + (u - u_hat)^2 / (2 tau_u); iu == 0 passes through.
+template <typename T>
+__device__ __forceinline__ T shrink_step(T u_hat, T rho_hat, T g, T tau_u, T lam) {
+  const T tl = tau_u * lam;
+  const T th = (tl * g) * g;
+  T step;
+  if (rho_hat < -th) step = tl * g;
+  else if (rho_hat > th) step = -(tl * g);
+  else step = g != T(0) ? -(rho_hat / g) : T(0);
+  return g != T(0) ? u_hat + step : u_hat;
+}
+
+__global__ void k_threshold(const double* __restrict__ u_hat, const double* __restrict__ rho_hat,
+                            const double* __restrict__ iu, const double* __restrict__ tau_u,
+                            double lam, int64_t n, double* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = shrink_step<double>(u_hat[i], rho_hat[i], iu[i], tau_u[i], lam);
+}
+
+// Dual ascent with unit-ball projection (solver.py:290-293).
+template <bool kDiag>
+__global__ void __launch_bounds__(256) k_pd_dual(PD s, float* __restrict__ dp, float* __restrict__ dq) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
+  int y = blockIdx.y * blockDim.y + threadIdx.y;
+  float pn = 0.f, qn = 0.f;
+  if (x < s.w && y < s.h) {
+    const size_t i = (size_t)y * s.w + x, n = s.n;
+    const bool ex = ex_at(s.m, s.w, x, i), ey = ey_at(s.m, s.h, s.w, y, i);
+    const float ub = s.u_bar[i];
+    const float vb0 = s.v_bar[i], vb1 = s.v_bar[n + i];
+    float gx = 0.f, gy = 0.f, g00 = 0.f, g01 = 0.f, g10 = 0.f, g11 = 0.f;
+    if (ex) { gx = s.u_bar[i + 1] - ub; g00 = s.v_bar[i + 1] - vb0; g10 = s.v_bar[n + i + 1] - vb1; }
+    if (ey) { gy = s.u_bar[i + s.w] - ub; g01 = s.v_bar[i + s.w] - vb0; g11 = s.v_bar[n + i + s.w] - vb1; }
+    const float a = s.T[i], b = s.T[n + i], c = s.T[2 * n + i];
+    const float sp = s.S[i] * s.alpha1;
+    float p0 = s.p[i] + sp * ((a * gx + b * gy) - vb0);
+    float p1 = s.p[n + i] + sp * ((b * gx + c * gy) - vb1);
+    float pnorm = sqrtf(p0 * p0 + p1 * p1);
+    float pd = fmaxf(1.f, pnorm);
+    p0 = p0 / pd; p1 = p1 / pd;
+    const float sq = s.sigma_q * s.alpha0;
+    float q0 = s.q[i] + sq * g00, q1 = s.q[n + i] + sq * g01;
+    float q2 = s.q[2 * n + i] + sq * g10, q3 = s.q[3 * n + i] + sq * g11;
+    float qnorm = sqrtf((q0 * q0 + q1 * q1) + (q2 * q2 + q3 * q3));
+    float qd = fmaxf(1.f, qnorm);
+    q0 = q0 / qd; q1 = q1 / qd; q2 = q2 / qd; q3 = q3 / qd;
+    s.p[i] = p0; s.p[n + i] = p1;
+    s.q[i] = q0; s.q[n + i] = q1; s.q[2 * n + i] = q2; s.q[3 * n + i] = q3;
+    if (kDiag) {
+      pn = sqrtf(p0 * p0 + p1 * p1);
+      qn = sqrtf((q0 * q0 + q1 * q1) + (q2 * q2 + q3 * q3));
+    }
+  }
+  if (kDiag) {
+    pn = warp_max(pn); qn = warp_max(qn);
+    if ((threadIdx.x & 31) == 0) { atomic_max_nonneg(dp, pn); atomic_max_nonneg(dq, qn); }
+  }
+}
+
+// Primal descent, data-term shrinkage and over-relaxation (solver.py:295-303).
+__global__ void __launch_bounds__(256) k_pd_primal(PD s) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
+  int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= s.w || y >= s.h) return;
+  const size_t i = (size_t)y * s.w + x, n = s.n;
+  const int w = s.w;
+  const bool ex = ex_at(s.m, w, x, i), ey = ey_at(s.m, s.h, w, y, i);
+  const bool exl = x > 0 && ex_at(s.m, w, x - 1, i - 1);
+  const bool eyu = y > 0 && ey_at(s.m, s.h, w, y - 1, i - w);
+  const float p0 = s.p[i], p1 = s.p[n + i];
+  // divergence(T p) with Dirichlet edges (rasters.py:158-172)
+  float dv = ex ? s.T[i] * p0 + s.T[n + i] * p1 : 0.f;
+  if (exl) dv -= s.T[i - 1] * s.p[i - 1] + s.T[n + i - 1] * s.p[n + i - 1];
+  if (ey) dv += s.T[n + i] * p0 + s.T[2 * n + i] * p1;
+  if (eyu) dv -= s.T[n + i - w] * s.p[i - w] + s.T[2 * n + i - w] * s.p[n + i - w];
+  // divergence of q[0:2] and q[2:4]
+  float d0 = ex ? s.q[i] : 0.f, d1 = ex ? s.q[2 * n + i] : 0.f;
+  if (exl) { d0 -= s.q[i - 1]; d1 -= s.q[2 * n + i - 1]; }
+  if (ey) { d0 += s.q[n + i]; d1 += s.q[3 * n + i]; }
+  if (eyu) { d0 -= s.q[n + i - w]; d1 -= s.q[3 * n + i - w]; }
+
+  const float tau_u = s.S[n + i], tau_v = s.S[2 * n + i];
+  const float u = s.u[i];
+  const float u_hat = u + (tau_u * s.alpha1) * dv;
+  const float g = s.iu[i];
+  const float rho_hat = s.rho0[i] + (u_hat - s.u_omega[i]) * g;
+  const float u_new = shrink_step<float>(u_hat, rho_hat, g, tau_u, s.lam);
+  const float v0 = s.v[i], v1 = s.v[n + i];
+  const float v0n = v0 + tau_v * (s.alpha0 * d0 + s.alpha1 * p0);
+  const float v1n = v1 + tau_v * (s.alpha0 * d1 + s.alpha1 * p1);
+  s.u[i] = u_new;
+  s.v[i] = v0n; s.v[n + i] = v1n;
+  s.u_bar[i] = u_new + s.theta * (u_new - u);
+  s.v_bar[i] = v0n + s.theta * (v0n - v0);
+  s.v_bar[n + i] = v1n + s.theta * (v1n - v1);
+}
+
+// Warp prologue part 1 (solver.py:332-337): i1w at x+w, trajectory direction
+// at x+w (renormalised, valid if norm > 0.5 and in mask).
+__global__ void __launch_bounds__(256) k_warp_sample(fsb_level L) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
+  int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= L.w || y >= L.h) return;
+  const size_t i = (size_t)y * L.w + x;
+  const float2 wv = reinterpret_cast<const float2*>(L.wv)[i];
+  const double px = (double)x + (double)wv.x, py = (double)y + (double)wv.y;
+  float iv[1];
+  bool wok = bicubic_sample<1, float>(L.i1, L.mask, L.h, L.w, px, py, iv);
+  float dr[2];
+  bool dok = bicubic_sample<2, float>(L.traj, L.traj_ok, L.h, L.w, px, py, dr);
+  const bool mk = L.mask[i] != 0;
+  float d0 = 0.f, d1 = 0.f;
+  if (dok) {
+    float nrm = sqrtf(dr[0] * dr[0] + dr[1] * dr[1]);
+    if (nrm > 0.5f && mk) { d0 = dr[0] / nrm; d1 = dr[1] / nrm; } else dok = false;
+  }
+  L.i1w[i] = wok ? iv[0] : 0.f;
+  L.i1w_ok[i] = wok && mk;
+  reinterpret_cast<float2*>(L.dirs)[i] = make_float2(d0, d1);
+  L.dir_ok[i] = dok;
+}
+
+// Warp prologue part 2 (solver.py:339-346 with image_derivative_along 192-202):
+// I_u = i1w(x+dir) - i1w(x) on taps valid in mask & warp_ok; rho0; resets.
+__global__ void __launch_bounds__(256) k_warp_linearize(fsb_level L) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
+  int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= L.w || y >= L.h) return;
+  const size_t i = (size_t)y * L.w + x, n = (size_t)L.h * L.w;
+  const float2 d = reinterpret_cast<const float2*>(L.dirs)[i];
+  float ahead[1];
+  bool ok = bicubic_sample<1, float>(L.i1w, L.i1w_ok, L.h, L.w, (double)x + (double)d.x,
+                                     (double)y + (double)d.y, ahead);
+  const float i1w = L.i1w[i];
+  const bool data_ok = ok && L.i1w_ok[i] && L.dir_ok[i];
+  L.iu[i] = data_ok ? ahead[0] - i1w : 0.f;
+  L.rho0[i] = data_ok ? i1w - L.i0[i] : 0.f;
+  const float u = L.u[i];
+  L.u_omega[i] = u;
+  L.u_bar[i] = u;
+  L.v_bar[i] = L.v[i];
+  L.v_bar[n + i] = L.v[n + i];
+}
+
+// Warp epilogue (solver.py:356-360): clip the increment, accumulate u and w.
+template <bool kDiag>
+__global__ void __launch_bounds__(256) k_warp_finish(fsb_level L, float du_max, float* dmax,
+                                                     double* partials) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
+  int y = blockIdx.y * blockDim.y + threadIdx.y;
+  float adu = 0.f;
+  if (x < L.w && y < L.h) {
+    const size_t i = (size_t)y * L.w + x;
+    const float uo = L.u_omega[i];
+    float du = fminf(fmaxf(L.u[i] - uo, -du_max), du_max);
+    if (!L.mask[i]) du = 0.f;
+    const float u = uo + du;
+    L.u[i] = u;
+    L.u_bar[i] = u;
+    const float2 d = reinterpret_cast<const float2*>(L.dirs)[i];
+    float2 wv = reinterpret_cast<float2*>(L.wv)[i];
+    wv.x = wv.x + du * d.x;
+    wv.y = wv.y + du * d.y;
+    reinterpret_cast<float2*>(L.wv)[i] = wv;
+    adu = fabsf(du);
+  }
+  if (kDiag) {
+    // max is order-free; the sum goes to fixed per-block slots (deterministic)
+    __shared__ double ssum[8];
+    __shared__ float smax[8];
+    float mx = warp_max(adu);
+    double sm = warp_sum((double)adu);
+    int lane = threadIdx.x & 31, wid = (threadIdx.y * blockDim.x + threadIdx.x) >> 5;
+    if (lane == 0) { ssum[wid] = sm; smax[wid] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+      double t = 0.0; float mm = 0.f;
+      int nw = (blockDim.x * blockDim.y) >> 5;
+      for (int k = 0; k < nw; ++k) { t += ssum[k]; mm = fmaxf(mm, smax[k]); }
+      partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+      atomic_max_nonneg(dmax, mm);
+    }
+  }
+}
+
+// mean |du| over the mask: ordered sum of the block partials / mask count.
+__global__ void k_mean_finish(const double* __restrict__ partials, int nparts,
+                              const uint8_t* __restrict__ m, size_t n, double* out) {
+  __shared__ double sh[256];
+  __shared__ unsigned long long cnt[256];
+  double t = 0.0;
+  unsigned long long c = 0;
+  for (int k = threadIdx.x; k < nparts; k += blockDim.x) t += partials[k];
+  for (size_t k = threadIdx.x; k < n; k += blockDim.x) c += m[k] ? 1 : 0;
+  sh[threadIdx.x] = t; cnt[threadIdx.x] = c;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) { sh[threadIdx.x] += sh[threadIdx.x + s]; cnt[threadIdx.x] += cnt[threadIdx.x + s]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = cnt[0] ? sh[0] / (double)cnt[0] : 0.0;
+}
+
+PD make_pd(const fsb_level* L, const fsb_params* prm) {
+  PD s;
+  s.h = L->h; s.w = L->w; s.n = (size_t)L->h * L->w;
+  s.m = L->mask; s.T = L->tensor; s.S = L->steps; s.iu = L->iu; s.rho0 = L->rho0;
+  s.u_omega = L->u_omega; s.u = L->u; s.u_bar = L->u_bar; s.v = L->v; s.v_bar = L->v_bar;
+  s.p = L->p; s.q = L->q;
+  s.lam = (float)prm->lam; s.alpha0 = (float)prm->alpha0; s.alpha1 = (float)prm->alpha1;
+  s.theta = (float)prm->theta;
+  s.sigma_q = (float)(1.0 / (2.0 * prm->alpha0));  // solver.py:265
+  return s;
+}
+
+int pd_iterate_internal(const fsb_level* L, const fsb_params* prm, int iters, float* diag_p,
+                        float* diag_q, cudaStream_t st) {
+  PD s = make_pd(L, prm);
+  dim3 blk(kBX, kBY), grd = grid2d(L->w, L->h, blk);
+  for (int k = 0; k < iters; ++k) {
+    if (diag_p && diag_q)
+      k_pd_dual<true><<<grd, blk, 0, st>>>(s, diag_p + k, diag_q + k);
+    else
+      k_pd_dual<false><<<grd, blk, 0, st>>>(s, nullptr, nullptr);
+    k_pd_primal<<<grd, blk, 0, st>>>(s);
+  }
+  return launch_status();
+}
+
+int warp_linearize_internal(const fsb_level* L, cudaStream_t st) {
+  dim3 blk(kBX, kBY), grd = grid2d(L->w, L->h, blk);
+  k_warp_sample<<<grd, blk, 0, st>>>(*L);
+  k_warp_linearize<<<grd, blk, 0, st>>>(*L);
+  return launch_status();
+}
+
+size_t level_partials_internal(int h, int w) {
+  dim3 blk(kBX, kBY), grd = grid2d(w, h, blk);
+  return (size_t)grd.x * grd.y;
+}
+
+int warp_finish_internal(const fsb_level* L, const fsb_params* prm, float* dmax, double* dmean,
+                         cudaStream_t st) {
+  dim3 blk(kBX, kBY), grd = grid2d(L->w, L->h, blk);
+  if (dmax && dmean && L->partials) {
+    k_warp_finish<true><<<grd, blk, 0, st>>>(*L, (float)prm->du_max, dmax, L->partials);
+    k_mean_finish<<<1, 256, 0, st>>>(L->partials, (int)(grd.x * grd.y), L->mask,
+                                     (size_t)L->h * L->w, dmean);
+  } else {
+    k_warp_finish<false><<<grd, blk, 0, st>>>(*L, (float)prm->du_max, nullptr, nullptr);
+  }
+  return launch_status();
+}
+
+}  // namespace fsb
+
+extern "C" int fsb_thresholding_step(const double* u_hat, const double* rho_hat, const double* iu,
+                                     const double* tau_u, double lam, int64_t n, double* out,
+                                     void* stream) {
+  if (n < 0 || (n > 0 && (!u_hat || !rho_hat || !iu || !tau_u || !out))) return FSB_EINVAL;
+  if (n == 0) return FSB_OK;
+  fsb::k_threshold<<<(unsigned)((n + 255) / 256), 256, 0, fsb::as_stream(stream)>>>(
+      u_hat, rho_hat, iu, tau_u, lam, n, out);
+  return fsb::launch_status();
+}

@@ -1,0 +1,386 @@
+// Native host driver: solve_level and solve_pyramid enqueue the whole frame on
+// one stream (no host sync, no allocation), so a frame can be captured into a
+// CUDA graph once and replayed. Workspace is caller-owned and carved here.
+//
+// Reference: solver.py:306-367 (solve_level), solver.py:401-452 (solve_pyramid),
+// fields.py:159-167 (translation_only_rig), camera.py:66-77 (scaled_to).
+
+#include <math.h>
+#include <string.h>
+
+#include <vector>
+
+#include "fsb_common.cuh"
+
+namespace fsb {
+
+// defined in the other translation units
+int trajectory_field_internal(const fsb_camera* cam, const double t[3], double eps_scale,
+                              double depth, float* dirs, uint8_t* ok, void* scratch,
+                              size_t scratch_bytes, cudaStream_t st);
+size_t traj_scratch_bytes_internal(int w, int h);
+int fov_mask_internal(const fsb_camera* cam, uint8_t* mask, int* iters, cudaStream_t st);
+int calibrate_internal(const fsb_rig* rig, const float* i1, const uint8_t* mask1, float* i1c,
+                       uint8_t* ok, int* iters0, cudaStream_t st);
+int pyramid_shapes_internal(int h, int w, int levels, double scale, int min_width, int* shapes,
+                            int max_levels);
+int downsample_internal(const float* src, const uint8_t* mask, int fh, int fw, float* dst,
+                        uint8_t* dmask, int ch, int cw, cudaStream_t st);
+int upsample_internal(const float* u, const float* wv, const uint8_t* mask, int sh, int sw,
+                      const uint8_t* dmask, int dh, int dw, float* uo, float* wo, cudaStream_t st);
+size_t level_setup_scratch_internal(int h, int w);
+int level_setup_internal(const fsb_level* lv, const fsb_params* prm, void* scratch,
+                         size_t scratch_bytes, cudaStream_t st);
+int pd_iterate_internal(const fsb_level* L, const fsb_params* prm, int iters, float* diag_p,
+                        float* diag_q, cudaStream_t st);
+int warp_linearize_internal(const fsb_level* L, cudaStream_t st);
+int warp_finish_internal(const fsb_level* L, const fsb_params* prm, float* dmax, double* dmean,
+                         cudaStream_t st);
+size_t level_partials_internal(int h, int w);
+
+namespace {
+
+constexpr int kMaxLevels = 32;
+
+bool params_ok(const fsb_params* p) {
+  // SolverParams.__post_init__ (solver.py:63-69) plus the pyramid checks of
+  // pyramid_shapes (rasters.py:210-213).
+  if (!p) return false;
+  if (!(p->lam > 0 && p->alpha0 > 0 && p->alpha1 > 0 && p->beta > 0 && p->eta > 0)) return false;
+  if (!(p->du_max > 0)) return false;
+  if (p->warp_iters < 1 || p->pd_iters < 1) return false;
+  if (p->pyramid_levels < 1 || !(p->pyramid_scale > 1.0)) return false;
+  return true;
+}
+
+bool cam_valid(const fsb_camera& c) {
+  return c.width > 0 && c.height > 0 && c.model >= FSB_CAM_PINHOLE &&
+         c.model <= FSB_CAM_POLYNOMIAL;
+}
+
+fsb_camera scaled_to(const fsb_camera& c, int h, int w) {  // camera.py:66-77
+  fsb_camera o = c;
+  double sx = (double)w / (double)c.width, sy = (double)h / (double)c.height;
+  o.width = w; o.height = h;
+  o.fx = c.fx * sx; o.fy = c.fy * sy;
+  o.cx = (c.cx + 0.5) * sx - 0.5;
+  o.cy = (c.cy + 0.5) * sy - 0.5;
+  return o;
+}
+
+// translation_only_rig (fields.py:159-167): t_res = R^T t
+void residual_translation(const fsb_rig& r, double t[3]) {
+  for (int i = 0; i < 3; ++i)
+    t[i] = (r.rotation[0 * 3 + i] * r.translation[0] + r.rotation[1 * 3 + i] * r.translation[1]) +
+           r.rotation[2 * 3 + i] * r.translation[2];
+}
+
+// Bump allocator over the caller's workspace (sizing pass when base == nullptr).
+struct Carve {
+  char* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    size_t bytes = align_up(count * sizeof(T));
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += bytes;
+    return p;
+  }
+};
+
+struct LevelState {  // state buffers sized for the finest level, reused per level
+  float *u[2], *wv[2];
+  float *u_bar, *v, *v_bar, *p, *q, *T, *S, *u_omega, *iu, *rho0, *i1w, *dirs;
+  uint8_t *i1w_ok, *dir_ok;
+  double* partials;
+};
+
+struct Plan {
+  int nlev;
+  int shapes[2 * kMaxLevels];  // finest first
+  size_t n0;                   // finest pixel count
+  // frame buffers
+  uint8_t *mask0, *mask1, *i1c_ok, *solve_mask;
+  int* iters;  // 4 ints of Newton-count scratch
+  float *lvl_i0[kMaxLevels], *lvl_i1[kMaxLevels];
+  uint8_t* lvl_mask[kMaxLevels];
+  float* traj[kMaxLevels];
+  uint8_t* traj_ok[kMaxLevels];
+  void* traj_scratch;
+  size_t traj_scratch_bytes;
+  void* setup_scratch;
+  size_t setup_scratch_bytes;
+  LevelState st;
+  size_t bytes;
+};
+
+int make_plan(const fsb_rig* rig, const fsb_params* prm, void* base, Plan& P) {
+  const int H = rig->cam0.height, W = rig->cam0.width;
+  int n = pyramid_shapes_internal(H, W, prm->pyramid_levels, prm->pyramid_scale, prm->min_width,
+                                  P.shapes, kMaxLevels);
+  if (n < 1) return FSB_EINVAL;
+  if (n > kMaxLevels) return FSB_EINVAL;
+  P.nlev = n;
+  P.n0 = (size_t)H * W;
+  const size_t n0 = P.n0, n1 = (size_t)rig->cam1.height * rig->cam1.width;
+  Carve c{static_cast<char*>(base)};
+  P.mask0 = c.take<uint8_t>(n0);
+  P.mask1 = c.take<uint8_t>(n1);
+  P.i1c_ok = c.take<uint8_t>(n0);
+  P.solve_mask = c.take<uint8_t>(n0);
+  P.iters = c.take<int>(64);
+  for (int l = 0; l < n; ++l) {
+    size_t np = (size_t)P.shapes[2 * l] * P.shapes[2 * l + 1];
+    P.lvl_i0[l] = l == 0 ? nullptr : c.take<float>(np);
+    P.lvl_i1[l] = l == 0 ? nullptr : c.take<float>(np);
+    P.lvl_mask[l] = l == 0 ? nullptr : c.take<uint8_t>(np);
+    P.traj[l] = c.take<float>(2 * np);
+    P.traj_ok[l] = c.take<uint8_t>(np);
+  }
+  P.traj_scratch_bytes = traj_scratch_bytes_internal(W, H);
+  P.traj_scratch = c.take<char>(P.traj_scratch_bytes);
+  P.setup_scratch_bytes = level_setup_scratch_internal(H, W);
+  P.setup_scratch = c.take<char>(P.setup_scratch_bytes);
+  LevelState& s = P.st;
+  for (int k = 0; k < 2; ++k) { s.u[k] = c.take<float>(n0); s.wv[k] = c.take<float>(2 * n0); }
+  s.u_bar = c.take<float>(n0);
+  s.v = c.take<float>(2 * n0);
+  s.v_bar = c.take<float>(2 * n0);
+  s.p = c.take<float>(2 * n0);
+  s.q = c.take<float>(4 * n0);
+  s.T = c.take<float>(3 * n0);
+  s.S = c.take<float>(3 * n0);
+  s.u_omega = c.take<float>(n0);
+  s.iu = c.take<float>(n0);
+  s.rho0 = c.take<float>(n0);
+  s.i1w = c.take<float>(n0);
+  s.dirs = c.take<float>(2 * n0);
+  s.i1w_ok = c.take<uint8_t>(n0);
+  s.dir_ok = c.take<uint8_t>(n0);
+  s.partials = c.take<double>(level_partials_internal(H, W) + 64);
+  P.bytes = c.off;
+  return FSB_OK;
+}
+
+__global__ void k_and_mask(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b, size_t n,
+                           uint8_t* __restrict__ o) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) o[i] = a[i] && b[i];
+}
+
+}  // namespace
+
+size_t level_partials_count(int h, int w) { return level_partials_internal(h, w) + 64; }
+
+int solve_level_internal(const fsb_level* L, const fsb_params* prm, const fsb_diag* diag,
+                         int64_t pd_off, int64_t warp_off, void* scratch, size_t scratch_bytes,
+                         cudaStream_t st) {
+  const size_t n = (size_t)L->h * L->w;
+  int rc = level_setup_internal(L, prm, scratch, scratch_bytes, st);
+  if (rc) return rc;
+  // solver.py:323-327: v, p, q, v_bar start at zero, u_bar = u
+  cudaMemsetAsync(L->v, 0, 2 * n * sizeof(float), st);
+  cudaMemsetAsync(L->v_bar, 0, 2 * n * sizeof(float), st);
+  cudaMemsetAsync(L->p, 0, 2 * n * sizeof(float), st);
+  cudaMemsetAsync(L->q, 0, 4 * n * sizeof(float), st);
+  cudaMemcpyAsync(L->u_bar, L->u, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  const int N = prm->warp_iters, K = prm->pd_iters;
+  for (int wi = 0; wi < N; ++wi) {
+    rc = warp_linearize_internal(L, st);
+    if (rc) return rc;
+    float* dp = (diag && diag->max_p_norm) ? diag->max_p_norm + pd_off + (int64_t)wi * K : nullptr;
+    float* dq = (diag && diag->max_q_norm) ? diag->max_q_norm + pd_off + (int64_t)wi * K : nullptr;
+    rc = pd_iterate_internal(L, prm, K, dp && dq ? dp : nullptr, dp && dq ? dq : nullptr, st);
+    if (rc) return rc;
+    float* dm = (diag && diag->max_du) ? diag->max_du + warp_off + wi : nullptr;
+    double* dmean = (diag && diag->mean_abs_du) ? diag->mean_abs_du + warp_off + wi : nullptr;
+    rc = warp_finish_internal(L, prm, dm && dmean ? dm : nullptr, dm && dmean ? dmean : nullptr,
+                              st);
+    if (rc) return rc;
+  }
+  return FSB_OK;
+}
+
+int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const float* i0,
+                           const float* i1, const float* const* traj_dirs,
+                           const uint8_t* const* traj_okv, void* ws, size_t ws_bytes, float* u_out,
+                           float* w_out, float* v_out, uint8_t* mask_out, float* i1c,
+                           const fsb_diag* diag, cudaStream_t st) {
+  if (!rig || !params_ok(prm) || !cam_valid(rig->cam0) || !cam_valid(rig->cam1)) return FSB_EINVAL;
+  if (!i0 || !i1 || !ws || !u_out || !w_out || !v_out || !mask_out || !i1c) return FSB_EINVAL;
+  if ((traj_dirs == nullptr) != (traj_okv == nullptr)) return FSB_EINVAL;
+  Plan P;
+  int rc = make_plan(rig, prm, nullptr, P);
+  if (rc) return rc;
+  if (ws_bytes < P.bytes) return FSB_ENOSPC;
+  make_plan(rig, prm, ws, P);
+  double t_res[3];
+  residual_translation(*rig, t_res);
+  if (!traj_dirs && t_res[0] == 0.0 && t_res[1] == 0.0 && t_res[2] == 0.0)
+    return FSB_EDOMAIN;  // fields.py:63-66, raised before any work
+
+  const int H = rig->cam0.height, W = rig->cam0.width;
+  const size_t n0 = P.n0;
+  const int N = prm->warp_iters, K = prm->pd_iters;
+
+  if (diag) {  // max slots start at 0 (atomicMax on non-negative bit patterns)
+    int64_t npd = (int64_t)P.nlev * N * K, nw = (int64_t)P.nlev * N;
+    if (diag->max_p_norm) cudaMemsetAsync(diag->max_p_norm, 0, npd * sizeof(float), st);
+    if (diag->max_q_norm) cudaMemsetAsync(diag->max_q_norm, 0, npd * sizeof(float), st);
+    if (diag->max_du) cudaMemsetAsync(diag->max_du, 0, nw * sizeof(float), st);
+    if (diag->mean_abs_du) cudaMemsetAsync(diag->mean_abs_du, 0, nw * sizeof(double), st);
+  }
+
+  // masks + calibration (solver.py:418-420)
+  rc = fov_mask_internal(&rig->cam0, P.mask0, P.iters + 0, st);
+  if (rc) return rc;
+  rc = fov_mask_internal(&rig->cam1, P.mask1, P.iters + 1, st);
+  if (rc) return rc;
+  rc = calibrate_internal(rig, i1, P.mask1, i1c, P.i1c_ok, P.iters + 2, st);
+  if (rc) return rc;
+  k_and_mask<<<(unsigned)((n0 + 255) / 256), 256, 0, st>>>(P.mask0, P.i1c_ok, n0, P.solve_mask);
+
+  // pyramids (solver.py:423-426), finest first in P.shapes
+  P.lvl_i0[0] = const_cast<float*>(i0);
+  P.lvl_i1[0] = i1c;
+  P.lvl_mask[0] = P.solve_mask;
+  for (int l = 1; l < P.nlev; ++l) {
+    int fh = P.shapes[2 * (l - 1)], fw = P.shapes[2 * (l - 1) + 1];
+    int ch = P.shapes[2 * l], cw = P.shapes[2 * l + 1];
+    rc = downsample_internal(P.lvl_i0[l - 1], P.lvl_mask[l - 1], fh, fw, P.lvl_i0[l],
+                             P.lvl_mask[l], ch, cw, st);
+    if (rc) return rc;
+    rc = downsample_internal(P.lvl_i1[l - 1], P.lvl_mask[l - 1], fh, fw, P.lvl_i1[l],
+                             P.lvl_mask[l], ch, cw, st);
+    if (rc) return rc;
+  }
+
+  int64_t pd_off = 0, warp_off = 0;
+  int cur = 0;
+  int prev_h = 0, prev_w = 0;
+  const uint8_t* prev_mask = nullptr;
+  for (int k = 0; k < P.nlev; ++k) {
+    const int l = P.nlev - 1 - k;  // coarse -> fine
+    const int h = P.shapes[2 * l], w = P.shapes[2 * l + 1];
+    const size_t np = (size_t)h * w;
+    const float* traj;
+    const uint8_t* tok;
+    if (traj_dirs) {
+      traj = traj_dirs[k];
+      tok = traj_okv[k];
+    } else {
+      fsb_camera cl = scaled_to(rig->cam0, h, w);
+      rc = trajectory_field_internal(&cl, t_res, prm->epsilon_scale, 1.0, P.traj[l], P.traj_ok[l],
+                                     P.traj_scratch, P.traj_scratch_bytes, st);
+      if (rc) return rc;
+      traj = P.traj[l];
+      tok = P.traj_ok[l];
+    }
+    LevelState& S = P.st;
+    float* u = S.u[cur];
+    float* wv = S.wv[cur];
+    if (k == 0) {
+      cudaMemsetAsync(u, 0, np * sizeof(float), st);
+      cudaMemsetAsync(wv, 0, 2 * np * sizeof(float), st);
+    } else {
+      rc = upsample_internal(S.u[cur ^ 1], S.wv[cur ^ 1], prev_mask, prev_h, prev_w, P.lvl_mask[l],
+                             h, w, u, wv, st);
+      if (rc) return rc;
+    }
+    fsb_level L;
+    memset(&L, 0, sizeof(L));
+    L.h = h; L.w = w;
+    L.i0 = P.lvl_i0[l]; L.i1 = P.lvl_i1[l]; L.mask = P.lvl_mask[l];
+    L.traj = traj; L.traj_ok = tok;
+    L.tensor = S.T; L.steps = S.S;
+    L.u = u; L.u_bar = S.u_bar; L.v = S.v; L.v_bar = S.v_bar; L.p = S.p; L.q = S.q;
+    L.wv = wv; L.u_omega = S.u_omega; L.iu = S.iu; L.rho0 = S.rho0; L.i1w = S.i1w;
+    L.i1w_ok = S.i1w_ok; L.dirs = S.dirs; L.dir_ok = S.dir_ok; L.partials = S.partials;
+    rc = solve_level_internal(&L, prm, diag, pd_off, warp_off, P.setup_scratch,
+                              P.setup_scratch_bytes, st);
+    if (rc) return rc;
+    pd_off += (int64_t)N * K;
+    warp_off += N;
+    prev_h = h; prev_w = w; prev_mask = P.lvl_mask[l];
+    if (l == 0) {
+      cudaMemcpyAsync(u_out, u, n0 * sizeof(float), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(w_out, wv, 2 * n0 * sizeof(float), cudaMemcpyDeviceToDevice, st);
+      // v planes -> interleaved (H,W,2) output
+      cudaMemcpy2DAsync(v_out, 2 * sizeof(float), S.v, sizeof(float), sizeof(float), n0,
+                        cudaMemcpyDeviceToDevice, st);
+      cudaMemcpy2DAsync(v_out + 1, 2 * sizeof(float), S.v + n0, sizeof(float), sizeof(float), n0,
+                        cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(mask_out, P.solve_mask, n0, cudaMemcpyDeviceToDevice, st);
+    }
+    cur ^= 1;
+  }
+  (void)H; (void)W;
+  return launch_status();
+}
+
+size_t solve_pyramid_bytes(const fsb_rig* rig, const fsb_params* prm) {
+  if (!rig || !params_ok(prm) || !cam_valid(rig->cam0) || !cam_valid(rig->cam1)) return 0;
+  Plan P;
+  if (make_plan(rig, prm, nullptr, P)) return 0;
+  return P.bytes;
+}
+
+}  // namespace fsb
+
+using namespace fsb;
+
+extern "C" {
+
+size_t fsb_level_partials(int32_t h, int32_t w) { return level_partials_count(h, w); }
+
+int fsb_warp_linearize(const fsb_level* lv, void* stream) {
+  if (!lv || lv->h < 1 || lv->w < 1) return FSB_EINVAL;
+  return warp_linearize_internal(lv, as_stream(stream));
+}
+
+int fsb_pd_iterate(const fsb_level* lv, const fsb_params* prm, int32_t iters, float* diag_p,
+                   float* diag_q, void* stream) {
+  if (!lv || !prm || iters < 0 || lv->h < 1 || lv->w < 1) return FSB_EINVAL;
+  return pd_iterate_internal(lv, prm, iters, diag_p, diag_q, as_stream(stream));
+}
+
+int fsb_warp_finish(const fsb_level* lv, const fsb_params* prm, float* diag_max_du,
+                    double* diag_mean_du, void* stream) {
+  if (!lv || !prm || lv->h < 1 || lv->w < 1) return FSB_EINVAL;
+  return warp_finish_internal(lv, prm, diag_max_du, diag_mean_du, as_stream(stream));
+}
+
+int fsb_solve_level(const fsb_level* lv, const fsb_params* prm, const fsb_diag* diag,
+                    int64_t diag_pd_offset, int64_t diag_warp_offset, void* scratch,
+                    size_t scratch_bytes, void* stream) {
+  if (!lv || !params_ok(prm) || lv->h < 1 || lv->w < 1) return FSB_EINVAL;
+  return solve_level_internal(lv, prm, diag, diag_pd_offset, diag_warp_offset, scratch,
+                              scratch_bytes, as_stream(stream));
+}
+
+int fsb_diag_counts(int32_t h, int32_t w, const fsb_params* prm, int64_t* n_pd, int64_t* n_warp) {
+  if (!params_ok(prm) || h < 1 || w < 1) return FSB_EINVAL;
+  int shapes[2 * 32];
+  int n = pyramid_shapes_internal(h, w, prm->pyramid_levels, prm->pyramid_scale, prm->min_width,
+                                  shapes, 32);
+  if (n < 1) return FSB_EINVAL;
+  if (n_pd) *n_pd = (int64_t)n * prm->warp_iters * prm->pd_iters;
+  if (n_warp) *n_warp = (int64_t)n * prm->warp_iters;
+  return n;
+}
+
+size_t fsb_solve_pyramid_workspace_bytes(const fsb_rig* rig, const fsb_params* prm) {
+  return solve_pyramid_bytes(rig, prm);
+}
+
+int fsb_solve_pyramid(const fsb_rig* rig, const fsb_params* prm, const float* i0, const float* i1,
+                      const float* const* traj_dirs, const uint8_t* const* traj_ok,
+                      void* workspace, size_t workspace_bytes, float* u, float* w, float* v,
+                      uint8_t* mask, float* i1c, const fsb_diag* diag, void* stream) {
+  return solve_pyramid_internal(rig, prm, i0, i1, traj_dirs, traj_ok, workspace, workspace_bytes,
+                                u, w, v, mask, i1c, diag, as_stream(stream));
+}
+
+const char* fsb_version(void) { return "fsb200 0.1 sm_100a"; }
+
+}  // extern "C"

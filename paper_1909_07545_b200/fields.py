@@ -1,0 +1,85 @@
+"""Calibration and trajectory fields on the GPU (reference fields.py:34-182).
+
+Both fields are computed in fp64 by libfsb200 (K1/K2); the trajectory
+directions are stored as fp32 on the device and returned here as float64.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _dev, _ext
+from .camera import RelativePose, StereoRig
+
+
+def translation_only_rig(rig) -> StereoRig:
+    """Residual rig after the calibration warp: (cam0, cam0, (I, R^T t)) (fields.py:159-167)."""
+    t_res = rig.pose.rotation.T @ rig.pose.translation
+    return StereoRig(rig.cam0, rig.cam0, RelativePose(np.eye(3), t_res))
+
+
+def generate_calibration_field(rig):
+    """Rotation + intrinsics flow x1 = x + field[x] and its validity (fields.py:34-45)."""
+    L = _ext.lib()
+    rs = _ext.rig_struct(rig)
+    h, w = rs.cam0.height, rs.cam0.width
+    field = _dev.empty((h, w, 2), torch.float64)
+    ok = _dev.empty((h, w), torch.uint8)
+    s = _dev.scratch(256)
+    _ext.check(L.fsb_calibration_field(C.byref(rs), _dev.ptr(field), _dev.ptr(ok), _dev.ptr(s),
+                                       s.numel(), _dev.stream_ptr()), "calibration_field")
+    return _dev.download(field), _dev.download(ok, bool)
+
+
+def trajectory_field_device(cam, t, epsilon_scale: float = 0.1, depth: float = 1.0):
+    """Device tensors (dirs (H,W,2) f32, ok (H,W) u8) for the rig (cam, cam, (I, t))."""
+    L = _ext.lib()
+    cs = _ext.camera_struct(cam)
+    tt = (C.c_double * 3)(*[float(v) for v in np.asarray(t, dtype=np.float64).reshape(3)])
+    dirs = _dev.empty((cs.height, cs.width, 2))
+    ok = _dev.empty((cs.height, cs.width), torch.uint8)
+    s = _dev.scratch(L.fsb_trajectory_scratch_bytes(C.byref(cs)))
+    _ext.check(L.fsb_trajectory_field(C.byref(cs), tt, float(epsilon_scale), float(depth),
+                                      _dev.ptr(dirs), _dev.ptr(ok), _dev.ptr(s), s.numel(),
+                                      _dev.stream_ptr()), "generate_trajectory_field")
+    return dirs, ok
+
+
+def generate_trajectory_field(rig, epsilon_scale: float = 0.1, depth: float = 1.0):
+    """Unit epipolar-curve tangents per pixel (fields.py:48-108).
+
+    Requires a translation-only rig; raises ValueError for a rotated rig or a
+    zero baseline like the reference.
+    """
+    R = np.asarray(rig.pose.rotation, dtype=np.float64)
+    if np.max(np.abs(R - np.eye(3))) > 1e-9:
+        raise ValueError("trajectory field needs a rotation-free rig; "
+                         "apply the calibration field first")
+    dirs, ok = trajectory_field_device(rig.cam0, rig.pose.translation, epsilon_scale, depth)
+    return _dev.download(dirs), _dev.download(ok, bool)
+
+
+def calibrate_second_image(i1, rig, mask1=None):
+    """Warp image 1 by the calibration field once (solver.py:389-398).
+
+    Returns (i1c, ok, cal, cal_ok) like the reference.
+    """
+    L = _ext.lib()
+    rs = _ext.rig_struct(rig)
+    i1a = np.asarray(i1, dtype=np.float64)
+    if i1a.shape != (rs.cam1.height, rs.cam1.width):
+        raise ValueError("image 1 does not match camera 1 dimensions")
+    d1 = _dev.upload(i1a)
+    dm1 = _dev.upload(np.asarray(mask1, dtype=bool), torch.uint8) if mask1 is not None else None
+    h, w = rs.cam0.height, rs.cam0.width
+    i1c = _dev.empty((h, w))
+    ok = _dev.empty((h, w), torch.uint8)
+    s = _dev.scratch(L.fsb_calibrate_scratch_bytes(C.byref(rs)))
+    _ext.check(L.fsb_calibrate_second_image(C.byref(rs), _dev.ptr(d1), _dev.ptr(dm1),
+                                            _dev.ptr(i1c), _dev.ptr(ok), _dev.ptr(s), s.numel(),
+                                            _dev.stream_ptr()), "calibrate_second_image")
+    cal, cal_ok = generate_calibration_field(rig)
+    return _dev.download(i1c), _dev.download(ok, bool), cal, cal_ok

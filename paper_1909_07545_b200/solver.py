@@ -1,0 +1,474 @@
+"""Anisotropic TGV-L1 primal-dual disparity solver on B200 — the drop-in boundary.
+
+Same public surface as the reference's `fisheyestereo.solver` for the dense
+mapping path (solver.py:36-452): `SolverParams`, `StereoResult`, `WarpState`,
+`SolverState`, `Diagnostics`, `solve_pyramid`, `solve_level`,
+`primal_dual_iterate`, `compute_tensor`, `precondition_steps`,
+`image_derivative_along`, `warp_image`, `thresholding_step`,
+`calibrate_second_image`. Host arrays in (float64, any layout the reference
+accepts), host arrays out (float64 / bool) — every pixel of work runs in
+libfsb200's sm_100a kernels.
+
+`Solver` is the device-resident engine underneath `solve_pyramid`: it owns the
+workspace for one (rig, params) pair, can capture the whole frame into a CUDA
+graph, and exposes device-tensor entry points for throughput measurement.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from collections import OrderedDict
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+import torch
+
+from . import _dev, _ext
+from .fields import calibrate_second_image  # noqa: F401  (re-export, solver.py:389)
+from .rasters import pixel_grid, pyramid_shapes, sample_bicubic
+
+
+@dataclass
+class SolverParams:
+    """Optimisation weights and schedule (solver.py:36-80), same defaults."""
+
+    lam: float = 5.0
+    alpha0: float = 17.0
+    alpha1: float = 1.2
+    beta: float = 9.0
+    eta: float = 0.85
+    warp_iters: int = 50
+    pd_iters: int = 10
+    du_max: float = 0.2
+    pyramid_levels: int = 5
+    pyramid_scale: float = 2.0
+    min_width: int = 50
+    epsilon_scale: float = 0.1
+    tensor_sigma: float = 1.0
+    theta: float = 1.0
+
+    def __post_init__(self):
+        if min(self.lam, self.alpha0, self.alpha1, self.beta, self.eta) <= 0:
+            raise ValueError("all weights must be positive")
+        if self.du_max <= 0:
+            raise ValueError("du_max must be positive")
+        if self.warp_iters < 1 or self.pd_iters < 1:
+            raise ValueError("iteration counts must be >= 1")
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+    @staticmethod
+    def from_dict(d: dict) -> "SolverParams":
+        unknown = set(d) - set(SolverParams.__dataclass_fields__)
+        if unknown:
+            raise ValueError(f"unknown solver parameters: {sorted(unknown)}")
+        return SolverParams(**d)
+
+
+@dataclass
+class WarpState:
+    u: np.ndarray
+    w: np.ndarray
+    omega: int = 0
+
+
+@dataclass
+class SolverState:
+    u: np.ndarray
+    v: np.ndarray
+    p: np.ndarray
+    q: np.ndarray
+    u_bar: np.ndarray
+    v_bar: np.ndarray
+
+
+@dataclass
+class Diagnostics:
+    max_p_norm: list = field(default_factory=list)
+    max_q_norm: list = field(default_factory=list)
+    max_du: list = field(default_factory=list)
+    mean_abs_du: list = field(default_factory=list)
+    du_max_limit: float = 0.0
+    record_increments: bool = False
+    increments: list = field(default_factory=list)
+
+
+@dataclass
+class StereoResult:
+    u: np.ndarray
+    w: np.ndarray
+    v: np.ndarray
+    mask: np.ndarray
+    i1_calibrated: np.ndarray
+    diagnostics: Diagnostics | None = None
+
+
+# ---------------------------------------------------------------- level buffers
+
+def _planes(a, c: int) -> torch.Tensor:
+    """(H, W, C) host array -> (C, H, W) contiguous device planes."""
+    arr = np.asarray(a, dtype=np.float64)
+    return _dev.upload(np.moveaxis(arr, -1, 0))
+
+
+def _from_planes(t: torch.Tensor) -> np.ndarray:
+    return np.moveaxis(_dev.download(t), 0, -1)
+
+
+class _Level:
+    """Device buffers of one pyramid level, viewable as the C `fsb_level`."""
+
+    def __init__(self, h: int, w: int):
+        self.h, self.w = h, w
+        E = _dev.empty
+        U8 = torch.uint8
+        self.i0 = E((h, w)); self.i1 = E((h, w)); self.mask = E((h, w), U8)
+        self.traj = E((h, w, 2)); self.traj_ok = E((h, w), U8)
+        self.tensor = E((3, h, w)); self.steps = E((3, h, w))
+        self.u = E((h, w)); self.u_bar = E((h, w))
+        self.v = E((2, h, w)); self.v_bar = E((2, h, w))
+        self.p = E((2, h, w)); self.q = E((4, h, w))
+        self.wv = E((h, w, 2)); self.u_omega = E((h, w))
+        self.iu = E((h, w)); self.rho0 = E((h, w)); self.i1w = E((h, w))
+        self.i1w_ok = E((h, w), U8); self.dirs = E((h, w, 2)); self.dir_ok = E((h, w), U8)
+        self.partials = E((int(_ext.lib().fsb_level_partials(h, w)),), torch.float64)
+
+    def struct(self) -> _ext.FsbLevel:
+        s = _ext.FsbLevel()
+        s.h, s.w = self.h, self.w
+        for name, _ in _ext.FsbLevel._fields_[2:]:
+            setattr(s, name, _dev.ptr(getattr(self, name)))
+        return s
+
+
+def _setup_level(lv: _Level, i0, mask, prm: _ext.FsbParams) -> None:
+    L = _ext.lib()
+    lv.i0.copy_(_dev.upload(i0))
+    lv.mask.copy_(_dev.upload(np.asarray(mask, dtype=bool), torch.uint8))
+    s = _dev.scratch(L.fsb_smooth_scratch_bytes(lv.h, lv.w))
+    st = lv.struct()
+    _ext.check(L.fsb_level_setup(C.byref(st), C.byref(prm), _dev.ptr(s), s.numel(),
+                                 _dev.stream_ptr()), "level_setup")
+
+
+# ---------------------------------------------------------------- per-stage API
+
+@dataclass
+class _StepSizes:
+    sigma_p: np.ndarray
+    sigma_q: float
+    tau_u: np.ndarray
+    tau_v: np.ndarray
+
+
+def compute_tensor(i0, beta: float, eta: float, mask) -> np.ndarray:
+    """Edge tensor (a, b, c) per pixel from an already-smoothed image (solver.py:122-141)."""
+    L = _ext.lib()
+    f = np.asarray(i0, dtype=np.float64)
+    h, w = f.shape
+    df = _dev.upload(f)
+    dm = _dev.upload(np.asarray(mask, dtype=bool), torch.uint8)
+    t = _dev.empty((3, h, w))
+    s = _dev.scratch(L.fsb_smooth_scratch_bytes(h, w))
+    _ext.check(L.fsb_compute_tensor(_dev.ptr(df), _dev.ptr(dm), h, w, float(beta), float(eta),
+                                    _dev.ptr(t), _dev.ptr(s), s.numel(), _dev.stream_ptr()),
+               "compute_tensor")
+    return _from_planes(t)
+
+
+def precondition_steps(t, mask, params: SolverParams) -> _StepSizes:
+    """Diagonal preconditioner step sizes (solver.py:246-276)."""
+    L = _ext.lib()
+    tt = np.asarray(t, dtype=np.float64)
+    h, w, _ = tt.shape
+    dt = _planes(tt, 3)
+    dm = _dev.upload(np.asarray(mask, dtype=bool), torch.uint8)
+    steps = _dev.empty((3, h, w))
+    s = _dev.scratch(h * w * 24 + 256)
+    prm = _ext.params_struct(params)
+    _ext.check(L.fsb_precondition_steps(_dev.ptr(dt), _dev.ptr(dm), h, w, C.byref(prm),
+                                        _dev.ptr(steps), _dev.ptr(s), s.numel(),
+                                        _dev.stream_ptr()), "precondition_steps")
+    st = _dev.download(steps)
+    return _StepSizes(sigma_p=st[0], sigma_q=1.0 / (2.0 * params.alpha0), tau_u=st[1],
+                      tau_v=st[2])
+
+
+def thresholding_step(u_hat, rho_hat, iu, tau_u, lam: float):
+    """Closed-form prox of the linearised L1 data term (solver.py:205-218).
+
+    Evaluated by the same device function the primal kernel inlines (here in
+    f64, elementwise over broadcast host arrays).
+    """
+    L = _ext.lib()
+    arrs = np.broadcast_arrays(*(np.asarray(a, dtype=np.float64)
+                                 for a in (u_hat, rho_hat, iu, tau_u)))
+    shape = arrs[0].shape
+    n = int(np.prod(shape))
+    dev = [_dev.upload(a.reshape(-1), torch.float64) for a in arrs]
+    out = _dev.empty((max(n, 1),), torch.float64)
+    _ext.check(L.fsb_thresholding_step(*[_dev.ptr(d) for d in dev], float(lam), n,
+                                       _dev.ptr(out), _dev.stream_ptr()), "thresholding_step")
+    return _dev.download(out)[:n].reshape(shape)
+
+
+def primal_dual_iterate(state: SolverState, t, iu, rho0, u_omega, params: SolverParams, mask,
+                        steps: _StepSizes | None = None) -> SolverState:
+    """One primal-dual cycle on the GPU (solver.py:279-303)."""
+    L = _ext.lib()
+    u = np.asarray(state.u, dtype=np.float64)
+    h, w = u.shape
+    lv = _Level(h, w)
+    lv.mask.copy_(_dev.upload(np.asarray(mask, dtype=bool), torch.uint8))
+    lv.tensor.copy_(_planes(t, 3))
+    if steps is None:
+        steps = precondition_steps(t, mask, params)
+    lv.steps.copy_(_dev.upload(np.stack([steps.sigma_p, steps.tau_u, steps.tau_v])))
+    lv.u.copy_(_dev.upload(u)); lv.u_bar.copy_(_dev.upload(state.u_bar))
+    lv.v.copy_(_planes(state.v, 2)); lv.v_bar.copy_(_planes(state.v_bar, 2))
+    lv.p.copy_(_planes(state.p, 2)); lv.q.copy_(_planes(state.q, 4))
+    lv.iu.copy_(_dev.upload(iu)); lv.rho0.copy_(_dev.upload(rho0))
+    lv.u_omega.copy_(_dev.upload(u_omega))
+    prm = _ext.params_struct(params)
+    st = lv.struct()
+    _ext.check(L.fsb_pd_iterate(C.byref(st), C.byref(prm), 1, None, None, _dev.stream_ptr()),
+               "primal_dual_iterate")
+    return SolverState(u=_dev.download(lv.u), v=_from_planes(lv.v), p=_from_planes(lv.p),
+                       q=_from_planes(lv.q), u_bar=_dev.download(lv.u_bar),
+                       v_bar=_from_planes(lv.v_bar))
+
+
+def warp_image(image, w, mask):
+    """Masked bicubic resample of `image` at x + w(x), zero where invalid (solver.py:181-189)."""
+    img = np.asarray(image, dtype=np.float64)
+    vals, ok = sample_bicubic(img, pixel_grid(*img.shape) + np.asarray(w), mask, acc64=False)
+    return np.where(ok, vals, 0.0), ok
+
+
+def image_derivative_along(dirs, i1w, i1w_valid, mask):
+    """I_u = i1w(x + dir) - i1w(x) on valid taps (solver.py:192-202)."""
+    a = np.asarray(i1w, dtype=np.float64)
+    valid = np.asarray(i1w_valid, dtype=bool)
+    ahead, ok = sample_bicubic(a, pixel_grid(*a.shape) + np.asarray(dirs),
+                               np.asarray(mask, dtype=bool) & valid, acc64=False)
+    iu = np.where(ok & valid, ahead - a, 0.0)
+    return iu, ok & valid
+
+
+def solve_level(i0, i1, traj_dirs, traj_valid, params: SolverParams, mask, init: WarpState,
+                diagnostics: Diagnostics | None = None) -> tuple[WarpState, SolverState]:
+    """Warping loop on one pyramid level, all on the GPU (solver.py:306-367)."""
+    L = _ext.lib()
+    m = np.asarray(mask, dtype=bool)
+    h, w = m.shape
+    lv = _Level(h, w)
+    lv.i1.copy_(_dev.upload(i1))
+    lv.traj.copy_(_dev.upload(traj_dirs))
+    lv.traj_ok.copy_(_dev.upload(np.asarray(traj_valid, dtype=bool), torch.uint8))
+    lv.u.copy_(_dev.upload(init.u))
+    lv.wv.copy_(_dev.upload(init.w))
+    prm = _ext.params_struct(params)
+    N, K = params.warp_iters, params.pd_iters
+    if diagnostics is not None:
+        diagnostics.du_max_limit = params.du_max
+    record = diagnostics is not None and diagnostics.record_increments
+    dp = _dev.zeros((N * K,)); dq = _dev.zeros((N * K,))
+    dmx = _dev.zeros((N,)); dmean = _dev.zeros((N,), torch.float64)
+    if not record:
+        s = _dev.scratch(L.fsb_smooth_scratch_bytes(h, w))
+        lv.i0.copy_(_dev.upload(i0))
+        lv.mask.copy_(_dev.upload(m, torch.uint8))
+        st = lv.struct()
+        diag = _ext.FsbDiag(_dev.ptr(dp), _dev.ptr(dq), _dev.ptr(dmx), _dev.ptr(dmean))
+        _ext.check(L.fsb_solve_level(C.byref(st), C.byref(prm),
+                                     C.byref(diag) if diagnostics is not None else None, 0, 0,
+                                     _dev.ptr(s), s.numel(), _dev.stream_ptr()), "solve_level")
+    else:
+        # Per-warp enqueue so each (du, dirs) increment can be recorded (solver.py:364-365).
+        _setup_level(lv, i0, m, prm)
+        for t in (lv.v, lv.v_bar, lv.p, lv.q):
+            t.zero_()
+        lv.u_bar.copy_(lv.u)
+        st = lv.struct()
+        for wi in range(N):
+            _ext.check(L.fsb_warp_linearize(C.byref(st), _dev.stream_ptr()), "warp_linearize")
+            _ext.check(L.fsb_pd_iterate(C.byref(st), C.byref(prm), K,
+                                        _dev.ptr(dp[wi * K:]), _dev.ptr(dq[wi * K:]),
+                                        _dev.stream_ptr()), "pd_iterate")
+            _ext.check(L.fsb_warp_finish(C.byref(st), C.byref(prm), _dev.ptr(dmx[wi:]),
+                                         _dev.ptr(dmean[wi:]), _dev.stream_ptr()), "warp_finish")
+            du = _dev.download(lv.u) - _dev.download(lv.u_omega)
+            diagnostics.increments.append((du, _dev.download(lv.dirs)))
+    if diagnostics is not None:
+        diagnostics.max_p_norm.extend(float(x) for x in _dev.download(dp))
+        diagnostics.max_q_norm.extend(float(x) for x in _dev.download(dq))
+        diagnostics.max_du.extend(float(x) for x in _dev.download(dmx))
+        diagnostics.mean_abs_du.extend(float(x) for x in _dev.download(dmean))
+    ws = WarpState(u=_dev.download(lv.u), w=_dev.download(lv.wv), omega=init.omega + N)
+    ss = SolverState(u=ws.u, v=_from_planes(lv.v), p=_from_planes(lv.p), q=_from_planes(lv.q),
+                     u_bar=_dev.download(lv.u_bar), v_bar=_from_planes(lv.v_bar))
+    return ws, ss
+
+
+# ---------------------------------------------------------------- pyramid engine
+
+class Solver:
+    """Device-resident solve_pyramid engine for one (rig, params) pair.
+
+    Owns the workspace, fixed input/output buffers (so the frame can be
+    captured into a CUDA graph) and optional diagnostics slots.
+    """
+
+    def __init__(self, rig, params: SolverParams, collect_diagnostics: bool = False):
+        L = _ext.lib()
+        self.rig = rig
+        self.params = params
+        self.rs = _ext.rig_struct(rig)
+        self.ps = _ext.params_struct(params)
+        self.H, self.W = self.rs.cam0.height, self.rs.cam0.width
+        self.H1, self.W1 = self.rs.cam1.height, self.rs.cam1.width
+        nbytes = L.fsb_solve_pyramid_workspace_bytes(C.byref(self.rs), C.byref(self.ps))
+        if nbytes == 0:
+            raise ValueError("invalid rig or solver parameters")
+        self.shapes = pyramid_shapes(self.H, self.W, params.pyramid_levels,
+                                     params.pyramid_scale, params.min_width)
+        self.workspace = _dev.scratch(nbytes)
+        E = _dev.empty
+        self.i0 = E((self.H, self.W)); self.i1 = E((self.H1, self.W1))
+        self.u = E((self.H, self.W)); self.w = E((self.H, self.W, 2))
+        self.v = E((self.H, self.W, 2)); self.mask = E((self.H, self.W), torch.uint8)
+        self.i1c = E((self.H, self.W))
+        self.diag = None
+        if collect_diagnostics:
+            npd, nw = C.c_int64(), C.c_int64()
+            L.fsb_diag_counts(self.H, self.W, C.byref(self.ps), C.byref(npd), C.byref(nw))
+            self.d_p = E((npd.value,)); self.d_q = E((npd.value,))
+            self.d_du = E((nw.value,)); self.d_mean = E((nw.value,), torch.float64)
+            self.diag = _ext.FsbDiag(_dev.ptr(self.d_p), _dev.ptr(self.d_q),
+                                     _dev.ptr(self.d_du), _dev.ptr(self.d_mean))
+        self._traj = None
+        self.graph = None
+
+    # -- trajectory override (solver.py:437-438)
+    def set_traj_override(self, traj_override) -> None:
+        from .camera import StereoRig
+        from .fields import translation_only_rig
+        if traj_override is None:
+            self._traj = None
+            return
+        rig_t = translation_only_rig(self.rig)
+        dirs_t, ok_t = [], []
+        for (h, w) in self.shapes[::-1]:
+            cam_l = self.rig.cam0.scaled_to((h, w))
+            d, ok = traj_override(StereoRig(cam_l, cam_l, rig_t.pose))
+            dirs_t.append(_dev.upload(np.asarray(d, dtype=np.float64)))
+            ok_t.append(_dev.upload(np.asarray(ok, dtype=bool), torch.uint8))
+        n = len(dirs_t)
+        self._traj = (dirs_t, ok_t, (C.c_void_p * n)(*[_dev.ptr(t) for t in dirs_t]),
+                      (C.c_void_p * n)(*[_dev.ptr(t) for t in ok_t]))
+        self.graph = None
+
+    def run(self, i0: torch.Tensor | None = None, i1: torch.Tensor | None = None) -> None:
+        """Enqueue one frame on the current stream (device inputs, device outputs)."""
+        L = _ext.lib()
+        i0 = self.i0 if i0 is None else i0
+        i1 = self.i1 if i1 is None else i1
+        td, tk = (self._traj[2], self._traj[3]) if self._traj else (None, None)
+        rc = L.fsb_solve_pyramid(C.byref(self.rs), C.byref(self.ps), _dev.ptr(i0), _dev.ptr(i1),
+                                 C.cast(td, C.c_void_p) if td else None,
+                                 C.cast(tk, C.c_void_p) if tk else None,
+                                 _dev.ptr(self.workspace), self.workspace.numel(),
+                                 _dev.ptr(self.u), _dev.ptr(self.w), _dev.ptr(self.v),
+                                 _dev.ptr(self.mask), _dev.ptr(self.i1c),
+                                 C.byref(self.diag) if self.diag is not None else None,
+                                 _dev.stream_ptr())
+        _ext.check(rc, "solve_pyramid")
+
+    def capture(self) -> None:
+        """Capture one frame (on the fixed input buffers) into a CUDA graph."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            self.run()  # warm-up outside capture (module load, lazy init)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.run()
+        self.graph = g
+
+    def replay(self) -> None:
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+    def solve(self, i0, i1) -> StereoResult:
+        """Host images in, StereoResult (float64 host arrays) out."""
+        i0a = np.asarray(i0)
+        i1a = np.asarray(i1)
+        if i0a.shape != (self.H, self.W):
+            raise ValueError("image 0 does not match camera 0 dimensions")
+        if i1a.shape != (self.H1, self.W1):
+            raise ValueError("image 1 does not match camera 1 dimensions")
+        self.i0.copy_(torch.from_numpy(np.ascontiguousarray(i0a, dtype=np.float32)),
+                      non_blocking=False)
+        self.i1.copy_(torch.from_numpy(np.ascontiguousarray(i1a, dtype=np.float32)),
+                      non_blocking=False)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self.run()
+        diag = None
+        if self.diag is not None:
+            diag = Diagnostics(du_max_limit=self.params.du_max)
+            diag.max_p_norm = [float(x) for x in _dev.download(self.d_p)]
+            diag.max_q_norm = [float(x) for x in _dev.download(self.d_q)]
+            diag.max_du = [float(x) for x in _dev.download(self.d_du)]
+            diag.mean_abs_du = [float(x) for x in _dev.download(self.d_mean)]
+        return StereoResult(u=_dev.download(self.u), w=_dev.download(self.w),
+                            v=_dev.download(self.v), mask=_dev.download(self.mask, bool),
+                            i1_calibrated=_dev.download(self.i1c), diagnostics=diag)
+
+
+_CACHE: "OrderedDict[tuple, Solver]" = OrderedDict()
+_CACHE_SIZE = 4
+
+
+def _rig_key(rig) -> tuple:
+    def cam(c):
+        return (c.model, c.width, c.height, c.fx, c.fy, c.cx, c.cy, c.fov,
+                getattr(c, "xi", None), tuple(getattr(c, "k", ())))
+    return (cam(rig.cam0), cam(rig.cam1),
+            tuple(np.asarray(rig.pose.rotation, dtype=np.float64).ravel()),
+            tuple(np.asarray(rig.pose.translation, dtype=np.float64).ravel()))
+
+
+def solve_pyramid(i0, i1, rig, params: SolverParams, collect_diagnostics: bool = False,
+                  traj_override=None) -> StereoResult:
+    """Full coarse-to-fine solve of a calibrated stereo pair (solver.py:401-452).
+
+    Drop-in for `fisheyestereo.solve_pyramid`: same arguments, same
+    `StereoResult` fields, ValueError on shape mismatch / invalid params /
+    zero baseline. Engines are cached per (rig, params) so repeated frames
+    reuse the workspace and CUDA graph.
+    """
+    i0a, i1a = np.asarray(i0), np.asarray(i1)
+    if i0a.shape != (rig.cam0.height, rig.cam0.width):
+        raise ValueError("image 0 does not match camera 0 dimensions")
+    if i1a.shape != (rig.cam1.height, rig.cam1.width):
+        raise ValueError("image 1 does not match camera 1 dimensions")
+    if traj_override is None and not np.any(rig.pose.rotation.T @ rig.pose.translation):
+        raise ValueError("trajectory field undefined for zero baseline")
+    key = (_rig_key(rig), tuple(asdict(params).items()), bool(collect_diagnostics))
+    eng = None if traj_override is not None else _CACHE.get(key)
+    if eng is None:
+        eng = Solver(rig, params, collect_diagnostics)
+        if traj_override is not None:
+            eng.set_traj_override(traj_override)
+        else:
+            _CACHE[key] = eng
+            while len(_CACHE) > _CACHE_SIZE:
+                _CACHE.popitem(last=False)
+    else:
+        _CACHE.move_to_end(key)
+    return eng.solve(i0a, i1a)

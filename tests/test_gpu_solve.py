@@ -1,0 +1,154 @@
+"""End-to-end parity of the GPU solve (fp32) against the pinned fp64 oracle.
+
+North-star gate (BASELINE.json): final disparity within 1e-3 px median and
+1e-2 px 99th-percentile absolute error over the solve mask. Solver invariants
+from the reference tests (dual feasibility, du clip, accumulation identity,
+determinism) are checked at fp32 tolerances stated inline.
+"""
+
+import json
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+from conftest import camera_from_record, load_golden
+from oracle import fs_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+MEDIAN_TOL = 1e-3
+P99_TOL = 1e-2
+
+
+def err_stats(a, b, sel):
+    e = np.abs(np.asarray(a) - np.asarray(b))[sel]
+    if e.size == 0:
+        return 0.0, 0.0, 0.0
+    return float(np.median(e)), float(np.percentile(e, 99)), float(e.max())
+
+
+def _rig(g):
+    from paper_1909_07545_b200.camera import RelativePose, StereoRig
+    return StereoRig(camera_from_record(g["cam0"]), camera_from_record(g["cam1"]),
+                     RelativePose(g["R"], g["t"]))
+
+
+def _params(g):
+    from paper_1909_07545_b200.solver import SolverParams
+    return SolverParams.from_dict(json.loads(str(g["params"])))
+
+
+def test_level_solve_parity():
+    from paper_1909_07545_b200.solver import Diagnostics, WarpState, solve_level
+    g = load_golden("level_solve")
+    prm = _params(g)
+    f = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
+    i0, i1, dirs, u0, w0 = f(g["i0"]), f(g["i1"]), f(g["dirs"]), f(g["u0"]), f(g["w0"])
+    d = Diagnostics()
+    ws, ss = solve_level(i0, i1, dirs, g["tok"], prm, g["mask"], WarpState(u=u0, w=w0), d)
+    tr = O.Trace()
+    ou, ow, os_ = O.level_solve(i0, i1, dirs, g["tok"], prm, g["mask"], u0, w0, tr)
+    med, p99, mx = err_stats(ws.u, ou, g["mask"])
+    assert med <= MEDIAN_TOL and p99 <= P99_TOL, (med, p99, mx)
+    med, p99, mx = err_stats(ws.w, ow, g["mask"][..., None] & np.ones(2, bool))
+    assert med <= MEDIAN_TOL and p99 <= P99_TOL, (med, p99, mx)
+    assert len(d.max_p_norm) == prm.warp_iters * prm.pd_iters
+    assert max(d.max_p_norm) <= 1 + 1e-6 and max(d.max_q_norm) <= 1 + 1e-6
+    assert max(d.max_du) <= prm.du_max * (1 + 1e-6)
+    np.testing.assert_allclose(d.max_du, tr.max_du, atol=1e-4)
+    np.testing.assert_allclose(d.mean_abs_du, tr.mean_abs_du, atol=1e-4)
+
+
+def test_pyramid_solve_parity_small_rendered_pair():
+    from paper_1909_07545_b200.solver import solve_pyramid
+    g = load_golden("pyramid_solve")
+    rig, prm = _rig(g), _params(g)
+    res = solve_pyramid(g["i0"], g["i1"], rig, prm, collect_diagnostics=True)
+    sol = O.pyramid_solve(g["i0"], g["i1"], rig, prm, trace=True)
+    np.testing.assert_array_equal(res.mask, sol.mask)
+    np.testing.assert_allclose(res.i1_calibrated, sol.i1c, atol=2e-7)
+    med, p99, mx = err_stats(res.u, sol.u, sol.mask)
+    print(f"u error median {med:.2e} p99 {p99:.2e} max {mx:.2e}")
+    assert med <= MEDIAN_TOL and p99 <= P99_TOL
+    d = res.diagnostics
+    assert len(d.max_p_norm) == len(sol.trace.max_p_norm)
+    assert max(d.max_p_norm) <= 1 + 1e-6 and max(d.max_q_norm) <= 1 + 1e-6
+    assert max(d.max_du) <= prm.du_max * (1 + 1e-6)
+
+
+def test_accumulation_identity():
+    """test_solver.py:307-321: u and w equal the running sums of increments."""
+    from paper_1909_07545_b200.solver import Diagnostics, WarpState, solve_level
+    g = load_golden("level_solve")
+    prm = _params(g)
+    h, w = g["mask"].shape
+    d = Diagnostics(record_increments=True)
+    ws, _ = solve_level(g["i0"], g["i1"], g["dirs"], g["tok"], prm, g["mask"],
+                        WarpState(u=np.zeros((h, w)), w=np.zeros((h, w, 2))), d)
+    u_sum = sum(du for du, _ in d.increments)
+    w_sum = sum(du[..., None] * dd for du, dd in d.increments)
+    assert np.max(np.abs(ws.u - u_sum)) < 1e-5
+    assert np.max(np.abs(ws.w - w_sum)) < 1e-5
+    assert all(m <= prm.du_max * (1 + 1e-6) for m in d.max_du)
+
+
+def test_determinism_and_graph_replay():
+    """Outputs are bit-identical run to run and through a CUDA graph (SPEC: deterministic)."""
+    import torch
+    from paper_1909_07545_b200.solver import Solver
+    g = load_golden("pyramid_solve")
+    eng = Solver(_rig(g), _params(g))
+    r1 = eng.solve(g["i0"], g["i1"])
+    r2 = eng.solve(g["i0"], g["i1"])
+    eng.capture()
+    r3 = eng.solve(g["i0"], g["i1"])
+    torch.cuda.synchronize()
+    for a, b in ((r1, r2), (r1, r3)):
+        assert np.array_equal(a.u, b.u) and np.array_equal(a.w, b.w)
+        assert np.array_equal(a.v, b.v) and np.array_equal(a.mask, b.mask)
+
+
+def test_api_errors():
+    from paper_1909_07545_b200.camera import RelativePose, StereoRig
+    from paper_1909_07545_b200.solver import SolverParams, solve_pyramid
+    g = load_golden("pyramid_solve")
+    rig = _rig(g)
+    with pytest.raises(ValueError):
+        solve_pyramid(np.zeros((10, 10)), g["i1"], rig, SolverParams())
+    with pytest.raises(ValueError):
+        solve_pyramid(g["i0"], np.zeros((3, 3)), rig, SolverParams())
+    zero = StereoRig(rig.cam0, rig.cam1, RelativePose(rig.pose.rotation, np.zeros(3)))
+    with pytest.raises(ValueError):
+        solve_pyramid(g["i0"], g["i1"], zero, SolverParams(pyramid_levels=1))
+
+
+def test_traj_override_matches_generated():
+    """Override path (solver.py:437-438) fed with the generated field gives the same answer."""
+    from paper_1909_07545_b200 import fields as F
+    from paper_1909_07545_b200.solver import solve_pyramid
+    g = load_golden("pyramid_solve")
+    rig, prm = _rig(g), _params(g)
+    a = solve_pyramid(g["i0"], g["i1"], rig, prm)
+
+    def override(rig_lvl):
+        return F.generate_trajectory_field(rig_lvl, prm.epsilon_scale)
+
+    b = solve_pyramid(g["i0"], g["i1"], rig, prm, traj_override=override)
+    assert np.array_equal(a.u, b.u) and np.array_equal(a.w, b.w)
+
+
+def test_empty_mask_frame():
+    """A rig whose FOV masks leave nothing to solve returns zeros, not NaNs."""
+    from paper_1909_07545_b200.camera import PinholeCamera, RelativePose, StereoRig
+    from paper_1909_07545_b200.solver import SolverParams, solve_pyramid
+    cam = PinholeCamera(width=24, height=20, fx=10.0, fy=10.0, cx=11.5, cy=9.5, fov=1e-6)
+    rig = StereoRig(cam, cam, RelativePose.from_displacement((0.1, 0.0, 0.0)))
+    res = solve_pyramid(np.zeros((20, 24)), np.zeros((20, 24)), rig,
+                        SolverParams(warp_iters=2, pd_iters=2, pyramid_levels=2, min_width=4))
+    sol = O.pyramid_solve(np.zeros((20, 24)), np.zeros((20, 24)), rig,
+                          SimpleNamespace(**SolverParams(warp_iters=2, pd_iters=2,
+                                                         pyramid_levels=2, min_width=4).to_dict()))
+    np.testing.assert_array_equal(res.mask, sol.mask)
+    assert not res.mask.any()
+    assert np.all(res.u == 0) and np.all(res.w == 0) and np.isfinite(res.v).all()
