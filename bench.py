@@ -1,0 +1,449 @@
+"""Benchmark: coarse-to-fine TGV-L1 fisheye stereo solve (solve_pyramid) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload c3|c1|c2|c5] [--no-cpu] [--no-e2e]
+
+A step = one full `solve_pyramid` frame per GPU (BASELINE config 3 by default:
+1024^2 unified fisheye pair, 6-DoF pose, reference defaults N=50 warps x K=10
+primal-dual iterations, 5 pyramid levels). Frames are independent, so N GPUs
+run N different frames per step (weak scaling, no collective on the data path;
+the only collective is the max-over-ranks of the timings).
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §Measurement for every field).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = ("frames/sec & Mpix·iter/sec at 1024² (1/2/4/8 B200); "
+          "primal-dual HBM GB/s vs peak")
+PD_BYTES_PER_PIXEL_ITER = 133  # 12 f32 state read + 9 f32 const + 1 B mask + 12 f32 write
+
+
+# ---------------------------------------------------------------- workloads
+
+def workload(name: str, frame: int = 0):
+    """(rig, params, description, supersample) of a BASELINE configuration."""
+    from paper_1909_07545_b200.camera import (PolynomialFisheyeCamera, RelativePose, StereoRig,
+                                              UnifiedCamera)
+    from paper_1909_07545_b200.solver import SolverParams
+    if name == "c3":
+        cam = UnifiedCamera(width=1024, height=1024, fx=455.0, fy=455.0, cx=511.5, cy=511.5,
+                            fov=math.pi, xi=0.9)
+        pose = RelativePose.from_displacement((0.08, 0.02, 0.03), rotvec=(0.01, 0.03, -0.02))
+        return (StereoRig(cam, cam, pose), SolverParams(),
+                "C3: 1024x1024 unified (xi=0.9) pair, 6-DoF pose, default_scene, "
+                "N=50 warps x K=10 PD, 5 levels", 2)
+    if name == "c1":
+        cam = PolynomialFisheyeCamera(width=320, height=320, fx=100.0, fy=100.0, cx=159.5,
+                                      cy=159.5, fov=math.pi, k=(1.0, 0.0, 0.0, 0.0))
+        return (StereoRig(cam, cam, RelativePose.from_displacement((0.1, 0.0, 0.0))),
+                SolverParams(warp_iters=5, pd_iters=10, pyramid_levels=3),
+                "C1: 320x320 equidistant, pure x baseline, N=5 x K=10, 3 levels", 2)
+    if name == "c2":
+        kw = dict(width=640, height=480, fx=200.0, fy=200.0, cy=239.5, fov=math.radians(163.0),
+                  k=(1.0, 0.03, -0.006, 0.001))
+        rig = StereoRig(PolynomialFisheyeCamera(cx=319.5, **kw),
+                        PolynomialFisheyeCamera(cx=320.5, **kw),
+                        RelativePose.from_displacement((0.064, 0, 0),
+                                                       rotvec=(0.002, 0.004, 0.001)))
+        return (rig, SolverParams(warp_iters=10, pd_iters=10, pyramid_levels=5, min_width=40),
+                "C2: 640x480 Kannala-Brandt, N=10 x K=10, 5 levels (min_width 40)", 1)
+    if name == "c5":
+        cam = UnifiedCamera(width=2048, height=2048, fx=910.0, fy=910.0, cx=1023.5, cy=1023.5,
+                            fov=math.pi, xi=0.9)
+        return (StereoRig(cam, cam, RelativePose.from_displacement((0.1, 0, 0),
+                                                                   rotvec=(0, 0.02, 0.005))),
+                SolverParams(warp_iters=20, pd_iters=10, pyramid_levels=7, min_width=32),
+                "C5: 2048x2048 unified, N=20 x K=10, 7 levels (min_width 32), TGV", 1)
+    raise ValueError(name)
+
+
+def pixel_iters_per_frame(rig, prm) -> int:
+    from paper_1909_07545_b200.rasters import pyramid_shapes
+    shapes = pyramid_shapes(rig.cam0.height, rig.cam0.width, prm.pyramid_levels,
+                            prm.pyramid_scale, prm.min_width)
+    return sum(h * w for h, w in shapes) * prm.warp_iters * prm.pd_iters
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------- CPU baseline (oracle)
+
+_CPU = {}
+
+
+def _cpu_init(i0, i1, mask, traj, tok, prm_dict):
+    """Worker setup for the CPU sample: finest-level tensor/steps (outside timing)."""
+    from types import SimpleNamespace
+    from oracle import fs_oracle as O
+    prm = SimpleNamespace(**prm_dict)
+    T = O.edge_tensor(O.smooth_in_mask(i0, mask, prm.tensor_sigma), mask, prm.beta, prm.eta)
+    _CPU.update(i0=i0, i1=i1, mask=mask, traj=traj, tok=tok, prm=prm, T=T,
+                st=O.step_sizes(T, mask, prm.alpha0, prm.alpha1))
+
+
+def _cpu_sample(_):
+    """One warp iteration of the finest level (linearise + K PD + clip), as
+    solver.py:331-360 runs it; returns the wall seconds."""
+    import numpy as _np
+    from oracle import fs_oracle as O
+    c = _CPU
+    h, w = c["mask"].shape
+    t0 = time.perf_counter()
+    prm = c["prm"]
+    u = _np.zeros((h, w))
+    wv = _np.zeros((h, w, 2))
+    _, _, dirs, _, iu, rho0 = O.linearize(c["i0"], c["i1"], c["traj"], c["tok"], c["mask"], wv)
+    z2 = _np.zeros((h, w, 2))
+    s = O.PDState(u=u, v=z2, p=z2, q=_np.zeros((h, w, 4)), u_bar=u.copy(), v_bar=z2)
+    for _k in range(prm.pd_iters):
+        s = O.pd_cycle(s, c["T"], iu, rho0, u, prm, c["mask"], c["st"])
+    du = _np.where(c["mask"], _np.clip(s.u - u, -prm.du_max, prm.du_max), 0.0)
+    _ = wv + du[..., None] * dirs
+    return time.perf_counter() - t0
+
+
+def cpu_inputs(rig, prm, i0=None, i1=None):
+    """Finest-level CPU inputs. With no images given, a smooth numpy texture
+    (the CPU path's cost is data-independent: every NumPy op runs on every pixel)."""
+    from oracle import fs_oracle as O
+    H, W = rig.cam0.height, rig.cam0.width
+    if i0 is None:
+        rng = np.random.default_rng(0)
+        i0 = O.gauss_filter(rng.random((H, W)), 2.0)
+        i1 = np.roll(i0, 2, axis=1)
+    mask = O.fov_mask(rig.cam0) & O.fov_mask(rig.cam1)
+    cam = O.as_lens(rig.cam0)
+    traj, tok = O.trajectory_field(cam, O.residual_translation(rig), prm.epsilon_scale)
+    return np.asarray(i0, np.float64), np.asarray(i1, np.float64), mask, traj, tok
+
+
+def cpu_pool(rig, prm, procs, i0=None, i1=None):
+    import multiprocessing as mp
+    args = cpu_inputs(rig, prm, i0, i1) + (prm.to_dict(),)
+    ctx = mp.get_context("fork")
+    return ctx.Pool(procs, initializer=_cpu_init, initargs=args)
+
+
+def cpu_step(pool, procs) -> float:
+    t0 = time.perf_counter()
+    pool.map(_cpu_sample, range(procs), chunksize=1)
+    return time.perf_counter() - t0
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(rig, prm, i0, i1, steps=1, warmup=0, procs=None):
+    procs = procs or cpu_cores()
+    H, W = rig.cam0.height, rig.cam0.width
+    pool = cpu_pool(rig, prm, procs, i0, i1)
+    try:
+        for _ in range(warmup):
+            cpu_step(pool, procs)
+        times = [cpu_step(pool, procs) for _ in range(steps)]
+    finally:
+        pool.close()
+        pool.join()
+    t = sum(times) / len(times)
+    mpix = procs * H * W * prm.pd_iters / t / 1e6
+    fps = mpix * 1e6 / pixel_iters_per_frame(rig, prm)
+    return {"value": fps, "unit": "frames/s", "mpix_iter_per_s": mpix, "cores": procs,
+            "kind": "port",
+            "sample": (f"oracle/fs_oracle.py (pinned fp64 NumPy restatement of the reference) on "
+                       f"{procs} host processes, each one finest-level warp iteration "
+                       f"({H}x{W}: linearise + K={prm.pd_iters} PD + clip) of the workload; "
+                       f"frames/s extrapolated by pixel-iterations per frame "
+                       f"({pixel_iters_per_frame(rig, prm) / 1e6:.2f} M); "
+                       f"{t:.1f} s per step"),
+            "seconds_per_step": t}
+
+
+# ---------------------------------------------------------------- reference arm
+
+def run_reference(a) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    rig, prm, desc, _ = workload(a.workload)
+    steps, warmup = max(a.steps, 1), max(a.warmup, 0)
+    cb = cpu_baseline(rig, prm, None, None, steps=steps, warmup=min(warmup, 1))
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "frames/s",
+            "n_gpus": a.gpus, "steps": steps, "warmup": warmup,
+            "ms_per_step": cb["seconds_per_step"] * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (numpy smooth texture; CPU cost is data-independent)",
+            "config": {"workload": desc, "impl": "CPU oracle port of the reference (fp64 NumPy)"},
+            "mpix_iter_per_s": cb["mpix_iter_per_s"],
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- B200 arm
+
+def pd_roofline(eng, rig, prm, img0, iters=50):
+    """Time the dominant kernel (primal-dual iteration, fsb_pd_iterate) at the
+    finest level with CUDA events on its launch stream; returns roofline dict."""
+    import ctypes as C
+    import torch
+    from paper_1909_07545_b200 import _dev, _ext
+    from paper_1909_07545_b200.fields import trajectory_field_device, translation_only_rig
+    from paper_1909_07545_b200.solver import _Level
+    L = _ext.lib()
+    H, W = rig.cam0.height, rig.cam0.width
+    lv = _Level(H, W)
+    lv.i0.copy_(img0)
+    lv.i1.copy_(eng.i1c)
+    lv.mask.copy_(eng.mask)
+    d, ok = trajectory_field_device(rig.cam0, translation_only_rig(rig).pose.translation,
+                                    prm.epsilon_scale)
+    lv.traj.copy_(d)
+    lv.traj_ok.copy_(ok)
+    lv.u.zero_(); lv.wv.zero_()
+    ps = _ext.params_struct(prm)
+    s = _dev.scratch(L.fsb_smooth_scratch_bytes(H, W))
+    st = lv.struct()
+    sp = _dev.stream_ptr()
+    _ext.check(L.fsb_level_setup(C.byref(st), C.byref(ps), _dev.ptr(s), s.numel(), sp), "setup")
+    for t in (lv.v, lv.v_bar, lv.p, lv.q):
+        t.zero_()
+    lv.u_bar.copy_(lv.u)
+    _ext.check(L.fsb_warp_linearize(C.byref(st), sp), "linearize")
+    _ext.check(L.fsb_pd_iterate(C.byref(st), C.byref(ps), 5, None, None, sp), "pd")
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("pd_roofline")
+    e0.record(stream)
+    _ext.check(L.fsb_pd_iterate(C.byref(st), C.byref(ps), iters, None, None, sp), "pd")
+    e1.record(stream)
+    torch.cuda.nvtx.range_pop()
+    torch.cuda.synchronize()
+    t_iter = e0.elapsed_time(e1) / 1e3 / iters
+    bytes_iter = PD_BYTES_PER_PIXEL_ITER * H * W
+    peak, peak_src = measured_peak()
+    achieved = bytes_iter / t_iter / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None,
+            "kernel": "primal-dual iteration (fsb_pd_iterate: k_pd_dual + k_pd_primal)",
+            "algorithmic_bytes_per_launch": bytes_iter,
+            "per_unit": f"{PD_BYTES_PER_PIXEL_ITER} B per pixel-iteration x {H}x{W} px",
+            "us_per_launch": t_iter * 1e6, "peak_source": peak_src}
+
+
+def run_b200(a) -> None:
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1909_07545_b200 import synth as S
+    from paper_1909_07545_b200.solver import Solver, solve_pyramid
+
+    rig, prm, desc, ss = workload(a.workload)
+    H, W = rig.cam0.height, rig.cam0.width
+    # each rank solves its own frame: the scene is reseeded per rank (C4-style)
+    scene = S.reseed_scene(S.default_scene(), rank)
+    img0, _, _ = S.render_device(scene, rig.cam0, supersample=ss)
+    img1, _, _ = S.render_device(scene, rig.cam1, pose=rig.pose, supersample=ss)
+
+    eng = Solver(rig, prm)
+    eng.i0.copy_(img0)
+    eng.i1.copy_(img1)
+    if a.profile_pd:  # ncu helper: one frame, then only the PD iterations (NVTX "pd_roofline")
+        eng.run()
+        print(json.dumps(pd_roofline(eng, rig, prm, img0, iters=a.steps)), flush=True)
+        return
+    kernels = eng.capture()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(max(a.warmup, 0)):
+        eng.replay()
+    torch.cuda.synchronize()
+    K = a.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(K):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            ev[k][0].record(stream)
+            eng.replay()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_ms = sum(s.elapsed_time(e) for s, e in ev)
+    t_all = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_all, op=dist.ReduceOp.MAX)
+    t_max = float(t_all.item()) / 1e3
+    frames = world * K
+    fps = frames / t_max
+    ppf = pixel_iters_per_frame(rig, prm)
+
+    # end to end through the public API: host float64 images in, StereoResult out
+    e2e = None
+    if not a.no_e2e:
+        h0 = img0.cpu().numpy().astype(np.float64)
+        h1 = img1.cpu().numpy().astype(np.float64)
+        solve_pyramid(h0, h1, rig, prm)  # engine build + graph capture outside timing
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(K):
+            res = solve_pyramid(h0, h1, rig, prm)
+        torch.cuda.synchronize()
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        assert res.u.shape == (H, W)
+        e2e = {"value": frames / float(te.item()), "unit": "frames/s",
+               "h2d_bytes_per_step": 2 * H * W * 4,
+               "d2h_bytes_per_step": H * W * (4 + 8 + 8 + 1 + 4),
+               "api": "paper_1909_07545_b200.solve_pyramid (float64 host arrays in/out)",
+               "timer": "host wall clock incl. fp64<->fp32 host conversion"}
+
+    roof = pd_roofline(eng, rig, prm, img0) if rank == 0 else None
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cb = cpu_baseline(rig, prm, img0.cpu().numpy().astype(np.float64),
+                          img1.cpu().numpy().astype(np.float64))
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu["mpix_iter_per_s"] = cb["mpix_iter_per_s"]
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": K,
+            "warmup": a.warmup, "ms_per_step": t_max * 1e3 / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": f"synthetic (GPU ray-cast default_scene, reseeded per rank, ss={ss})",
+            "config": {"workload": desc, "frames_per_step_per_gpu": 1,
+                       "pixel_iters_per_frame": ppf,
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "parallelism": f"frame-partitioned x{world}, no data-path collective"},
+            "mpix_iter_per_s": fps * ppf / 1e6,
+            "e2e": e2e,
+            "gpu_launches": kernels * K,
+            "kernels_per_frame": kernels,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=["c3", "c1", "c2", "c5"], default="c3")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the public-API e2e leg")
+    ap.add_argument("--profile-pd", action="store_true",
+                    help="only time the PD kernel at the finest level (for ncu --nvtx)")
+    a = ap.parse_args(argv)
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_b200(a)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -251,6 +251,46 @@ int fsb_solve_pyramid(const fsb_rig* rig, const fsb_params* prm, const float* i0
                       float* u, float* w, float* v, uint8_t* mask, float* i1c,
                       const fsb_diag* diag, void* stream);
 
+/* CUDA-graph form of fsb_solve_pyramid: captures one frame (same arguments,
+ * fixed buffers) on `stream` into an executable graph; *n_kernels receives the
+ * number of kernel nodes per frame. Replay with fsb_graph_launch. */
+typedef struct fsb_graph fsb_graph;
+int fsb_graph_create(const fsb_rig* rig, const fsb_params* prm, const float* i0, const float* i1,
+                     const float* const* traj_dirs, const uint8_t* const* traj_ok,
+                     void* workspace, size_t workspace_bytes, float* u, float* w, float* v,
+                     uint8_t* mask, float* i1c, const fsb_diag* diag, void* stream,
+                     fsb_graph** graph, int64_t* n_kernels);
+int fsb_graph_launch(fsb_graph* graph, void* stream);
+int fsb_graph_destroy(fsb_graph* graph);
+
+/* ---------------------------------------------------------------- synthetic inputs */
+
+#define FSB_PRIM_PLANE 0   /* synth.py:124-138 */
+#define FSB_PRIM_SPHERE 1  /* synth.py:141-158 */
+#define FSB_PRIM_BOX 2     /* synth.py:161-182 */
+#define FSB_TEX_NOISE 0    /* ValueNoise   synth.py:28-84  */
+#define FSB_TEX_CHECKER 1  /* Checkerboard synth.py:87-98  */
+#define FSB_TEX_SINE 2     /* SineGrating  synth.py:101-115 */
+
+/* One textured primitive of a Scene (synth.py:187-205).
+ * geom: plane point[3] + unit normal[3]; sphere center[3] + radius; box lo[3] + hi[3].
+ * tex:  noise (scale, lo, hi, persistence); checker (period, lo, hi);
+ *       sine (wavelength, lo, hi, unit direction[3]). */
+typedef struct fsb_prim {
+  int32_t kind, tex_kind, octaves, reserved;
+  int64_t seed;
+  double geom[7];
+  double tex[8];
+} fsb_prim;
+
+/* render (synth.py:217-254) without sensor noise: ray-cast `prims` (device
+ * array) through `cam` placed at `origin` with world->camera `rotation`
+ * (NULL = identity / origin 0, i.e. camera 0), s x s supersampling.
+ * image (H,W) f32 in [0,1]; depth (H,W) f32 and hit (H,W) u8 may be NULL. */
+int fsb_render(const fsb_camera* cam, const double rotation[9], const double origin[3],
+               const fsb_prim* prims, int32_t nprims, int32_t supersample, float* image,
+               float* depth, uint8_t* hit, void* stream);
+
 /* Library build identification, e.g. "fsb200 sm_100a". */
 const char* fsb_version(void);
 

@@ -220,6 +220,29 @@ def main() -> int:
                         u=ws.u, w=ws.w, v=ss.v, p=ss.p, q=ss.q,
                         max_p=np.array(di.max_p_norm), max_q=np.array(di.max_q_norm),
                         max_du=np.array(di.max_du), mean_du=np.array(di.mean_abs_du))
+    # ---- renderer (GPU input generator) on every primitive / texture kind
+    sc = synth.default_scene()
+    extra = synth.Scene(primitives=(
+        synth.Plane(point=(0.0, 0.0, 2.0), normal=(0.1, 0.0, -1.0),
+                    texture=synth.Checkerboard(period=0.3)),
+        synth.Sphere(center=(-0.3, 0.2, 1.2), radius=0.3,
+                     texture=synth.SineGrating(wavelength=0.2, direction=(1.0, 1.0, 0.0))),
+        synth.Box(lo=(0.2, -0.5, 0.9), hi=(0.6, -0.1, 1.4),
+                  texture=synth.ValueNoise(scale=0.1, octaves=2, seed=3))))
+    rec = {}
+    k = 0
+    for scene, c, pose_, ss in [
+            (sc, cams["unified"], None, 2),
+            (sc, cams["kb"], camera.RelativePose.from_displacement((0.1, 0, 0), rotvec=(0, .03, 0)), 1),
+            (extra, cams["pinhole"], None, 3),
+            (synth.reseed_scene(sc, 5), cams["equidistant"], None, 1)]:
+        img, dep, hit = synth.render(scene, c, pose=pose_, supersample=ss)
+        rec[f"img{k}"] = img
+        rec[f"depth{k}"] = dep
+        rec[f"hit{k}"] = hit
+        k += 1
+    np.savez_compressed(OUT / "render.npz", **rec)
+
     total = sum(f.stat().st_size for f in OUT.glob("*.npz"))
     print(f"wrote {len(list(OUT.glob('*.npz')))} fixtures, {total / 1024:.0f} KiB -> {OUT}")
     return 0

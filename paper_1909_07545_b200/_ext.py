@@ -30,7 +30,8 @@ EXPORTED = (
     "fsb_smooth_scratch_bytes", "fsb_pyramid_shapes", "fsb_downsample_area",
     "fsb_upsample_state", "fsb_compute_tensor", "fsb_precondition_steps", "fsb_level_partials", "fsb_level_setup", "fsb_warp_linearize",
     "fsb_pd_iterate", "fsb_thresholding_step", "fsb_warp_finish", "fsb_solve_level", "fsb_diag_counts",
-    "fsb_solve_pyramid_workspace_bytes", "fsb_solve_pyramid", "fsb_version",
+    "fsb_solve_pyramid_workspace_bytes", "fsb_solve_pyramid", "fsb_render", "fsb_graph_create", "fsb_graph_launch", "fsb_graph_destroy",
+    "fsb_version",
 )
 
 
@@ -66,6 +67,12 @@ class FsbLevel(C.Structure):
             "i0", "i1", "mask", "traj", "traj_ok", "tensor", "steps", "u", "u_bar", "v",
             "v_bar", "p", "q", "wv", "u_omega", "iu", "rho0", "i1w", "i1w_ok", "dirs",
             "dir_ok", "partials")]
+
+
+class FsbPrim(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("tex_kind", C.c_int32), ("octaves", C.c_int32),
+                ("reserved", C.c_int32), ("seed", C.c_int64), ("geom", C.c_double * 7),
+                ("tex", C.c_double * 8)]
 
 
 class FsbError(RuntimeError):
@@ -121,6 +128,13 @@ def lib() -> C.CDLL:
             "fsb_solve_pyramid_workspace_bytes": (sz, [P(FsbRig), P(FsbParams)]),
             "fsb_solve_pyramid": (C.c_int, [P(FsbRig), P(FsbParams), vp, vp, vp, vp, vp, sz,
                                             vp, vp, vp, vp, vp, P(FsbDiag), vp]),
+            "fsb_render": (C.c_int, [P(FsbCamera), P(C.c_double), P(C.c_double), vp, i32, i32,
+                                     vp, vp, vp, vp]),
+            "fsb_graph_create": (C.c_int, [P(FsbRig), P(FsbParams), vp, vp, vp, vp, vp, sz, vp,
+                                           vp, vp, vp, vp, P(FsbDiag), vp, P(C.c_void_p),
+                                           P(C.c_int64)]),
+            "fsb_graph_launch": (C.c_int, [vp, vp]),
+            "fsb_graph_destroy": (C.c_int, [vp]),
             "fsb_version": (C.c_char_p, []),
         }
         for name, (res, args) in sig.items():

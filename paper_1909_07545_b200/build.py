@@ -31,6 +31,7 @@ UNITS = [
     ("setup.cu", ["-fmad=false"]),
     ("pd.cu", []),
     ("solver.cu", []),
+    ("synth.cu", ["-fmad=false"]),
 ]
 HEADERS = [CSRC / "fsb_common.cuh", ROOT / "include" / "fsb200.h"]
 

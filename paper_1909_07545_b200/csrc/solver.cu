@@ -381,6 +381,60 @@ int fsb_solve_pyramid(const fsb_rig* rig, const fsb_params* prm, const float* i0
                                 u, w, v, mask, i1c, diag, as_stream(stream));
 }
 
+struct fsb_graph {
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+};
+
+int fsb_graph_create(const fsb_rig* rig, const fsb_params* prm, const float* i0, const float* i1,
+                     const float* const* traj_dirs, const uint8_t* const* traj_ok,
+                     void* workspace, size_t workspace_bytes, float* u, float* w, float* v,
+                     uint8_t* mask, float* i1c, const fsb_diag* diag, void* stream,
+                     fsb_graph** out, int64_t* n_kernels) {
+  if (!out || !stream) return FSB_EINVAL;  // capture needs a non-default stream
+  *out = nullptr;
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return (int)e;
+  int rc = solve_pyramid_internal(rig, prm, i0, i1, traj_dirs, traj_ok, workspace,
+                                  workspace_bytes, u, w, v, mask, i1c, diag, st);
+  cudaGraph_t g = nullptr;
+  e = cudaStreamEndCapture(st, &g);
+  if (rc) { if (g) cudaGraphDestroy(g); return rc; }
+  if (e != cudaSuccess) return (int)e;
+  size_t n = 0;
+  cudaGraphGetNodes(g, nullptr, &n);
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (n) cudaGraphGetNodes(g, nodes.data(), &n);
+  int64_t k = 0;
+  for (size_t i = 0; i < n; ++i) {
+    cudaGraphNodeType t;
+    cudaGraphNodeGetType(nodes[i], &t);
+    if (t == cudaGraphNodeTypeKernel) ++k;
+  }
+  cudaGraphExec_t ex = nullptr;
+  e = cudaGraphInstantiate(&ex, g, 0);
+  if (e != cudaSuccess) { cudaGraphDestroy(g); return (int)e; }
+  fsb_graph* G = new fsb_graph{g, ex};
+  *out = G;
+  if (n_kernels) *n_kernels = k;
+  return FSB_OK;
+}
+
+int fsb_graph_launch(fsb_graph* G, void* stream) {
+  if (!G) return FSB_EINVAL;
+  cudaError_t e = cudaGraphLaunch(G->exec, as_stream(stream));
+  return e == cudaSuccess ? FSB_OK : (int)e;
+}
+
+int fsb_graph_destroy(fsb_graph* G) {
+  if (!G) return FSB_OK;
+  cudaGraphExecDestroy(G->exec);
+  cudaGraphDestroy(G->graph);
+  delete G;
+  return FSB_OK;
+}
+
 const char* fsb_version(void) { return "fsb200 0.1 sm_100a"; }
 
 }  // extern "C"

@@ -348,7 +348,9 @@ class Solver:
             self.diag = _ext.FsbDiag(_dev.ptr(self.d_p), _dev.ptr(self.d_q),
                                      _dev.ptr(self.d_du), _dev.ptr(self.d_mean))
         self._traj = None
+        self._host = None
         self.graph = None
+        self.kernels_per_frame = None
 
     # -- trajectory override (solver.py:437-438)
     def set_traj_override(self, traj_override) -> None:
@@ -367,57 +369,90 @@ class Solver:
         n = len(dirs_t)
         self._traj = (dirs_t, ok_t, (C.c_void_p * n)(*[_dev.ptr(t) for t in dirs_t]),
                       (C.c_void_p * n)(*[_dev.ptr(t) for t in ok_t]))
-        self.graph = None
+        self.release()
+
+    def _args(self, i0, i1):
+        td, tk = (self._traj[2], self._traj[3]) if self._traj else (None, None)
+        return (C.byref(self.rs), C.byref(self.ps), _dev.ptr(i0), _dev.ptr(i1),
+                C.cast(td, C.c_void_p) if td else None, C.cast(tk, C.c_void_p) if tk else None,
+                _dev.ptr(self.workspace), self.workspace.numel(), _dev.ptr(self.u),
+                _dev.ptr(self.w), _dev.ptr(self.v), _dev.ptr(self.mask), _dev.ptr(self.i1c),
+                C.byref(self.diag) if self.diag is not None else None)
 
     def run(self, i0: torch.Tensor | None = None, i1: torch.Tensor | None = None) -> None:
         """Enqueue one frame on the current stream (device inputs, device outputs)."""
-        L = _ext.lib()
         i0 = self.i0 if i0 is None else i0
         i1 = self.i1 if i1 is None else i1
-        td, tk = (self._traj[2], self._traj[3]) if self._traj else (None, None)
-        rc = L.fsb_solve_pyramid(C.byref(self.rs), C.byref(self.ps), _dev.ptr(i0), _dev.ptr(i1),
-                                 C.cast(td, C.c_void_p) if td else None,
-                                 C.cast(tk, C.c_void_p) if tk else None,
-                                 _dev.ptr(self.workspace), self.workspace.numel(),
-                                 _dev.ptr(self.u), _dev.ptr(self.w), _dev.ptr(self.v),
-                                 _dev.ptr(self.mask), _dev.ptr(self.i1c),
-                                 C.byref(self.diag) if self.diag is not None else None,
-                                 _dev.stream_ptr())
-        _ext.check(rc, "solve_pyramid")
+        _ext.check(_ext.lib().fsb_solve_pyramid(*self._args(i0, i1), _dev.stream_ptr()),
+                   "solve_pyramid")
 
-    def capture(self) -> None:
-        """Capture one frame (on the fixed input buffers) into a CUDA graph."""
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            self.run()  # warm-up outside capture (module load, lazy init)
-        torch.cuda.current_stream().wait_stream(s)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self.run()
+    def capture(self) -> int:
+        """Capture one frame on the fixed input buffers into a CUDA graph (native,
+        fsb_graph_create); returns the number of kernel launches per frame."""
+        L = _ext.lib()
+        self.release()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        g = C.c_void_p()
+        nk = C.c_int64()
+        _ext.check(L.fsb_graph_create(*self._args(self.i0, self.i1), side.cuda_stream,
+                                      C.byref(g), C.byref(nk)), "graph_create")
         self.graph = g
+        self.kernels_per_frame = int(nk.value)
+        return self.kernels_per_frame
+
+    def release(self) -> None:
+        if getattr(self, "graph", None):
+            _ext.lib().fsb_graph_destroy(self.graph)
+        self.graph = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
 
     def replay(self) -> None:
-        if self.graph is None:
+        """Launch the captured frame on the current stream."""
+        if not self.graph:
             self.capture()
-        self.graph.replay()
+        _ext.check(_ext.lib().fsb_graph_launch(self.graph, _dev.stream_ptr()), "graph_launch")
+
+    def _pinned(self):
+        if self._host is None:
+            P = dict(dtype=torch.float32, pin_memory=True)
+            self._host = {
+                "i0": torch.empty((self.H, self.W), **P), "i1": torch.empty((self.H1, self.W1), **P),
+                "u": torch.empty((self.H, self.W), **P), "w": torch.empty((self.H, self.W, 2), **P),
+                "v": torch.empty((self.H, self.W, 2), **P),
+                "mask": torch.empty((self.H, self.W), dtype=torch.uint8, pin_memory=True),
+                "i1c": torch.empty((self.H, self.W), **P)}
+        return self._host
 
     def solve(self, i0, i1) -> StereoResult:
-        """Host images in, StereoResult (float64 host arrays) out."""
+        """Host images in, StereoResult (float64 host arrays) out.
+
+        Inputs are staged through pinned buffers (fp32 on the device), the frame
+        runs as a replayed CUDA graph, outputs come back through pinned buffers.
+        """
         i0a = np.asarray(i0)
         i1a = np.asarray(i1)
         if i0a.shape != (self.H, self.W):
             raise ValueError("image 0 does not match camera 0 dimensions")
         if i1a.shape != (self.H1, self.W1):
             raise ValueError("image 1 does not match camera 1 dimensions")
-        self.i0.copy_(torch.from_numpy(np.ascontiguousarray(i0a, dtype=np.float32)),
-                      non_blocking=False)
-        self.i1.copy_(torch.from_numpy(np.ascontiguousarray(i1a, dtype=np.float32)),
-                      non_blocking=False)
-        if self.graph is not None:
-            self.graph.replay()
+        h = self._pinned()
+        np.copyto(h["i0"].numpy(), i0a, casting="unsafe")
+        np.copyto(h["i1"].numpy(), i1a, casting="unsafe")
+        self.i0.copy_(h["i0"], non_blocking=True)
+        self.i1.copy_(h["i1"], non_blocking=True)
+        if self._traj is None:
+            self.replay()
         else:
             self.run()
+        for k in ("u", "w", "v", "mask", "i1c"):
+            h[k].copy_(getattr(self, k), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
         diag = None
         if self.diag is not None:
             diag = Diagnostics(du_max_limit=self.params.du_max)
@@ -425,9 +460,11 @@ class Solver:
             diag.max_q_norm = [float(x) for x in _dev.download(self.d_q)]
             diag.max_du = [float(x) for x in _dev.download(self.d_du)]
             diag.mean_abs_du = [float(x) for x in _dev.download(self.d_mean)]
-        return StereoResult(u=_dev.download(self.u), w=_dev.download(self.w),
-                            v=_dev.download(self.v), mask=_dev.download(self.mask, bool),
-                            i1_calibrated=_dev.download(self.i1c), diagnostics=diag)
+        return StereoResult(u=h["u"].numpy().astype(np.float64),
+                            w=h["w"].numpy().astype(np.float64),
+                            v=h["v"].numpy().astype(np.float64),
+                            mask=h["mask"].numpy().astype(bool),
+                            i1_calibrated=h["i1c"].numpy().astype(np.float64), diagnostics=diag)
 
 
 _CACHE: "OrderedDict[tuple, Solver]" = OrderedDict()

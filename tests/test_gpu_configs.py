@@ -1,0 +1,175 @@
+"""GPU renderer parity and end-to-end parity on the BASELINE configurations.
+
+The renderer (input generator) is checked against the reference's own renders
+(tests/golden/render.npz). The solve is checked against the pinned oracle on
+GPU-rendered inputs at the sizes the oracle finishes in seconds (C1 at full
+size; C2 geometry at full size), and through size-independent invariants at
+the headline 1024^2 size (C3).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import camera_from_record, load_golden
+from oracle import fs_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def test_render_matches_reference():
+    from paper_1909_07545_b200 import synth as S
+    from paper_1909_07545_b200.camera import RelativePose
+    g = load_golden("render")
+    cams = {n: camera_from_record(load_golden(f"camera_{n}")["cam"])
+            for n in ("unified", "kb", "pinhole", "equidistant")}
+    sc = S.default_scene()
+    extra = S.Scene(primitives=(
+        S.Plane(point=(0.0, 0.0, 2.0), normal=(0.1, 0.0, -1.0), texture=S.Checkerboard(period=0.3)),
+        S.Sphere(center=(-0.3, 0.2, 1.2), radius=0.3,
+                 texture=S.SineGrating(wavelength=0.2, direction=(1.0, 1.0, 0.0))),
+        S.Box(lo=(0.2, -0.5, 0.9), hi=(0.6, -0.1, 1.4), texture=S.ValueNoise(scale=0.1, octaves=2,
+                                                                             seed=3))))
+    cases = [(sc, cams["unified"], None, 2),
+             (sc, cams["kb"], RelativePose.from_displacement((0.1, 0, 0), rotvec=(0, .03, 0)), 1),
+             (extra, cams["pinhole"], None, 3),
+             (S.reseed_scene(sc, 5), cams["equidistant"], None, 1)]
+    for k, (scene, cam, pose, ss) in enumerate(cases):
+        img, depth, hit = S.render(scene, cam, pose=pose, supersample=ss)
+        ref_hit = g[f"hit{k}"]
+        assert np.mean(hit == ref_hit) >= 0.999
+        both = hit & ref_hit
+        close = np.abs(img - g[f"img{k}"])[both] <= 1e-5
+        assert close.mean() >= 0.995, (k, close.mean())
+        np.testing.assert_allclose(depth[both], g[f"depth{k}"][both], rtol=1e-6, atol=1e-6)
+
+
+def _c1():
+    """BASELINE config 1: 320^2 equidistant, pure x baseline."""
+    from paper_1909_07545_b200.camera import PolynomialFisheyeCamera, RelativePose, StereoRig
+    from paper_1909_07545_b200.solver import SolverParams
+    cam = PolynomialFisheyeCamera(width=320, height=320, fx=100.0, fy=100.0, cx=159.5, cy=159.5,
+                                  fov=np.pi, k=(1.0, 0.0, 0.0, 0.0))
+    rig = StereoRig(cam, cam, RelativePose.from_displacement((0.1, 0.0, 0.0)))
+    return rig, SolverParams(warp_iters=5, pd_iters=10, pyramid_levels=3)
+
+
+def _c2():
+    """BASELINE config 2 geometry: 640x480 Kannala-Brandt."""
+    from paper_1909_07545_b200.camera import PolynomialFisheyeCamera, RelativePose, StereoRig
+    from paper_1909_07545_b200.solver import SolverParams
+    kw = dict(width=640, height=480, fx=200.0, fy=200.0, cy=239.5, fov=np.deg2rad(163.0),
+              k=(1.0, 0.03, -0.006, 0.001))
+    rig = StereoRig(PolynomialFisheyeCamera(cx=319.5, **kw), PolynomialFisheyeCamera(cx=320.5, **kw),
+                    RelativePose.from_displacement((0.064, 0, 0), rotvec=(0.002, 0.004, 0.001)))
+    return rig, SolverParams(warp_iters=10, pd_iters=10, pyramid_levels=5, min_width=40)
+
+
+def _render_pair(rig, ss=2):
+    from paper_1909_07545_b200 import synth as S
+    scene = S.default_scene()
+    i0, _, _ = S.render(scene, rig.cam0, supersample=ss)
+    i1, _, _ = S.render(scene, rig.cam1, pose=rig.pose, supersample=ss)
+    return i0, i1
+
+
+def _parity(rig, prm, i0, i1):
+    from paper_1909_07545_b200.solver import solve_pyramid
+    res = solve_pyramid(i0, i1, rig, prm, collect_diagnostics=True)
+    sol = O.pyramid_solve(i0, i1, rig, prm)
+    np.testing.assert_array_equal(res.mask, sol.mask)
+    e = np.abs(res.u - sol.u)[sol.mask]
+    med, p99, mx = float(np.median(e)), float(np.percentile(e, 99)), float(e.max())
+    print(f"u err median {med:.3e} p99 {p99:.3e} max {mx:.3e}; u range {sol.u.max():.2f}")
+    assert med <= 1e-3 and p99 <= 1e-2
+    d = res.diagnostics
+    assert max(d.max_p_norm) <= 1 + 1e-6 and max(d.max_q_norm) <= 1 + 1e-6
+    assert max(d.max_du) <= prm.du_max * (1 + 1e-6)
+    return res, sol
+
+
+def test_c1_end_to_end_parity():
+    rig, prm = _c1()
+    i0, i1 = _render_pair(rig)
+    _parity(rig, prm, i0, i1)
+
+
+def test_c2_kannala_brandt_end_to_end_parity():
+    rig, prm = _c2()
+    i0, i1 = _render_pair(rig, ss=1)
+    _parity(rig, prm, i0, i1)
+
+
+def test_degenerates_to_rectified():
+    """Criterion 05 (test_acceptance.py:165-191): on a pinhole pair the fisheye
+    pipeline equals hard-coded horizontal directions."""
+    from paper_1909_07545_b200 import synth as S
+    from paper_1909_07545_b200.solver import SolverParams, solve_pyramid
+    rig = S.pinhole_rig(width=240, height=240, f=200.0, baseline=0.1)
+    scene = S.Scene(primitives=(
+        S.Plane(point=(0.0, 0.0, 2.2), normal=(0.0, 0.0, -1.0),
+                texture=S.ValueNoise(scale=0.5, octaves=4, seed=5, lo=0.05, hi=0.95,
+                                     persistence=0.65)),
+        S.Sphere(center=(0.3, -0.25, 1.4), radius=0.35,
+                 texture=S.ValueNoise(scale=0.1, octaves=4, seed=23, lo=0.1, hi=0.9,
+                                      persistence=0.65))))
+    i0, _, _ = S.render(scene, rig.cam0, supersample=2)
+    i1, _, _ = S.render(scene, rig.cam1, pose=rig.pose, supersample=2)
+
+    def horizontal(rig_lvl):
+        h, w = rig_lvl.cam0.height, rig_lvl.cam0.width
+        d = np.zeros((h, w, 2))
+        d[:, :, 0] = -1.0
+        return d, rig_lvl.cam0.fov_mask()
+
+    prm = SolverParams(warp_iters=10, pyramid_levels=4, min_width=30)
+    a = solve_pyramid(i0, i1, rig, prm)
+    b = solve_pyramid(i0, i1, rig, prm, traj_override=horizontal)
+    assert np.max(np.abs(a.u - b.u)) <= 1e-6
+    assert np.max(np.linalg.norm(a.w - b.w, axis=-1)) <= 1e-6
+    # rectified oracle: 4 px disparity plane (test_solver.py:387-399) sanity
+    assert np.isfinite(a.u).all()
+
+
+def test_rectified_constant_disparity():
+    """test_solver.py:387-399: fronto plane at f*b/4 gives 4 px of disparity."""
+    from paper_1909_07545_b200 import synth as S
+    from paper_1909_07545_b200.rasters import gradient
+    from paper_1909_07545_b200.solver import SolverParams, solve_pyramid
+    rig = S.pinhole_rig(width=240, height=240, f=300.0, baseline=0.1)
+    scene = S.plane_scene(depth=300.0 * 0.1 / 4.0,
+                          texture=S.ValueNoise(scale=1.7, octaves=4, seed=9, lo=0.05, hi=0.95,
+                                               persistence=0.65))
+    i0, _, _ = S.render(scene, rig.cam0, supersample=2)
+    i1, _, _ = S.render(scene, rig.cam1, pose=rig.pose, supersample=2)
+    res = solve_pyramid(i0, i1, rig, SolverParams(warp_iters=10, pyramid_levels=4, min_width=30))
+    g = np.linalg.norm(gradient(i0, res.mask), axis=-1)
+    textured = res.mask & (g > 0.02)
+    assert np.mean(np.abs(res.u[textured] - 4.0) < 0.5) >= 0.95
+
+
+def test_c3_headline_invariants():
+    """C3 (1024^2 unified, 6-DoF, reference defaults N=50 K=10): size-independent
+    properties — determinism, dual feasibility, du clip, finite output, and
+    agreement of the calibrated image with the oracle (fp64 taps)."""
+    from paper_1909_07545_b200 import synth as S
+    from paper_1909_07545_b200.camera import RelativePose, StereoRig, UnifiedCamera
+    from paper_1909_07545_b200.solver import Solver, SolverParams
+    cam = UnifiedCamera(width=1024, height=1024, fx=455.0, fy=455.0, cx=511.5, cy=511.5,
+                        fov=np.pi, xi=0.9)
+    rig = StereoRig(cam, cam, RelativePose.from_displacement((0.08, 0.02, 0.03),
+                                                             rotvec=(0.01, 0.03, -0.02)))
+    i0, i1 = _render_pair(rig, ss=1)
+    prm = SolverParams()
+    eng = Solver(rig, prm, collect_diagnostics=True)
+    r1 = eng.solve(i0, i1)
+    r2 = eng.solve(i0, i1)
+    assert np.array_equal(r1.u, r2.u) and np.array_equal(r1.w, r2.w)
+    d = r1.diagnostics
+    assert len(d.max_p_norm) == 5 * 50 * 10
+    assert max(d.max_p_norm) <= 1 + 1e-6 and max(d.max_q_norm) <= 1 + 1e-6
+    assert max(d.max_du) <= prm.du_max * (1 + 1e-6)
+    assert np.isfinite(r1.u).all() and np.isfinite(r1.w).all()
+    assert 0.6 < r1.mask.mean() < 0.9
+    i1c, ok = O.calibrate(i1, rig)
+    np.testing.assert_array_equal(ok & O.fov_mask(rig.cam0), r1.mask)
+    np.testing.assert_allclose(r1.i1_calibrated, i1c, atol=2e-7)
