@@ -183,6 +183,14 @@ typedef struct fsb_level {
   float* dirs;           /* (h,w,2) sampled unit directions                */
   uint8_t* dir_ok;
   double* partials;      /* reduction scratch (fsb_level_partials(h,w))    */
+  /* Optional buffers of the temporally blocked path (all NULL = one-iteration
+   * kernels): a second state set of 12 planes (u, u_bar, v x2, v_bar x2, p x2,
+   * q x4) for ping-pong, and a second set of per-warp samples. */
+  float* state_b;
+  float* i1w_b;
+  uint8_t* i1w_ok_b;
+  float* dirs_b;
+  uint8_t* dir_ok_b;
 } fsb_level;
 
 size_t fsb_level_partials(int32_t h, int32_t w);

@@ -30,10 +30,11 @@ UNITS = [
     ("rasters.cu", ["-fmad=false"]),
     ("setup.cu", ["-fmad=false"]),
     ("pd.cu", []),
+    ("pd_block.cu", []),
     ("solver.cu", []),
     ("synth.cu", ["-fmad=false"]),
 ]
-HEADERS = [CSRC / "fsb_common.cuh", ROOT / "include" / "fsb200.h"]
+HEADERS = [*sorted(CSRC.glob("*.cuh")), ROOT / "include" / "fsb200.h"]
 
 
 def nvcc() -> str:

@@ -9,7 +9,7 @@
 // multi-channel state (v, v_bar, p, q, tensor, steps) is stored as consecutive
 // planes so every load of a warp is a coalesced 128-byte line.
 
-#include "fsb_common.cuh"
+#include "pd_math.cuh"
 
 namespace fsb {
 
@@ -35,19 +35,6 @@ __device__ __forceinline__ bool ey_at(const uint8_t* __restrict__ m, int h, int 
   return y + 1 < h && m[i] && m[i + w];
 }
 
-// thresholding_step (solver.py:205-218): the closed-form prox of
-// lam*|rho_hat + (u - u_hat) iu| + (u - u_hat)^2 / (2 tau_u); iu == 0 passes through.
-template <typename T>
-__device__ __forceinline__ T shrink_step(T u_hat, T rho_hat, T g, T tau_u, T lam) {
-  const T tl = tau_u * lam;
-  const T th = (tl * g) * g;
-  T step;
-  if (rho_hat < -th) step = tl * g;
-  else if (rho_hat > th) step = -(tl * g);
-  else step = g != T(0) ? -(rho_hat / g) : T(0);
-  return g != T(0) ? u_hat + step : u_hat;
-}
-
 __global__ void k_threshold(const double* __restrict__ u_hat, const double* __restrict__ rho_hat,
                             const double* __restrict__ iu, const double* __restrict__ tau_u,
                             double lam, int64_t n, double* __restrict__ out) {
@@ -55,7 +42,7 @@ __global__ void k_threshold(const double* __restrict__ u_hat, const double* __re
   if (i < n) out[i] = shrink_step<double>(u_hat[i], rho_hat[i], iu[i], tau_u[i], lam);
 }
 
-// Dual ascent with unit-ball projection (solver.py:290-293).
+// Dual ascent with unit-ball projection (solver.py:290-293), one pixel per thread.
 template <bool kDiag>
 __global__ void __launch_bounds__(256) k_pd_dual(PD s, float* __restrict__ dp, float* __restrict__ dq) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
@@ -69,19 +56,10 @@ __global__ void __launch_bounds__(256) k_pd_dual(PD s, float* __restrict__ dp, f
     float gx = 0.f, gy = 0.f, g00 = 0.f, g01 = 0.f, g10 = 0.f, g11 = 0.f;
     if (ex) { gx = s.u_bar[i + 1] - ub; g00 = s.v_bar[i + 1] - vb0; g10 = s.v_bar[n + i + 1] - vb1; }
     if (ey) { gy = s.u_bar[i + s.w] - ub; g01 = s.v_bar[i + s.w] - vb0; g11 = s.v_bar[n + i + s.w] - vb1; }
-    const float a = s.T[i], b = s.T[n + i], c = s.T[2 * n + i];
-    const float sp = s.S[i] * s.alpha1;
-    float p0 = s.p[i] + sp * ((a * gx + b * gy) - vb0);
-    float p1 = s.p[n + i] + sp * ((b * gx + c * gy) - vb1);
-    float pnorm = sqrtf(p0 * p0 + p1 * p1);
-    float pd = fmaxf(1.f, pnorm);
-    p0 = p0 / pd; p1 = p1 / pd;
-    const float sq = s.sigma_q * s.alpha0;
-    float q0 = s.q[i] + sq * g00, q1 = s.q[n + i] + sq * g01;
-    float q2 = s.q[2 * n + i] + sq * g10, q3 = s.q[3 * n + i] + sq * g11;
-    float qnorm = sqrtf((q0 * q0 + q1 * q1) + (q2 * q2 + q3 * q3));
-    float qd = fmaxf(1.f, qnorm);
-    q0 = q0 / qd; q1 = q1 / qd; q2 = q2 / qd; q3 = q3 / qd;
+    float p0 = s.p[i], p1 = s.p[n + i];
+    float q0 = s.q[i], q1 = s.q[n + i], q2 = s.q[2 * n + i], q3 = s.q[3 * n + i];
+    dual_update(s.T[i], s.T[n + i], s.T[2 * n + i], s.S[i] * s.alpha1, s.sigma_q * s.alpha0, gx,
+                gy, g00, g01, g10, g11, vb0, vb1, p0, p1, q0, q1, q2, q3);
     s.p[i] = p0; s.p[n + i] = p1;
     s.q[i] = q0; s.q[n + i] = q1; s.q[2 * n + i] = q2; s.q[3 * n + i] = q3;
     if (kDiag) {
@@ -95,42 +73,33 @@ __global__ void __launch_bounds__(256) k_pd_dual(PD s, float* __restrict__ dp, f
   }
 }
 
+__device__ __forceinline__ Flux flux_at(const PD& s, size_t i, int x, int y) {
+  const size_t n = s.n;
+  const bool ex = ex_at(s.m, s.w, x, i), ey = ey_at(s.m, s.h, s.w, y, i);
+  return make_flux(s.T[i], s.T[n + i], s.T[2 * n + i], ex, ey, s.p[i], s.p[n + i], s.q[i],
+                   s.q[n + i], s.q[2 * n + i], s.q[3 * n + i]);
+}
+
 // Primal descent, data-term shrinkage and over-relaxation (solver.py:295-303).
 __global__ void __launch_bounds__(256) k_pd_primal(PD s) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= s.w || y >= s.h) return;
   const size_t i = (size_t)y * s.w + x, n = s.n;
-  const int w = s.w;
-  const bool ex = ex_at(s.m, w, x, i), ey = ey_at(s.m, s.h, w, y, i);
-  const bool exl = x > 0 && ex_at(s.m, w, x - 1, i - 1);
-  const bool eyu = y > 0 && ey_at(s.m, s.h, w, y - 1, i - w);
-  const float p0 = s.p[i], p1 = s.p[n + i];
-  // divergence(T p) with Dirichlet edges (rasters.py:158-172)
-  float dv = ex ? s.T[i] * p0 + s.T[n + i] * p1 : 0.f;
-  if (exl) dv -= s.T[i - 1] * s.p[i - 1] + s.T[n + i - 1] * s.p[n + i - 1];
-  if (ey) dv += s.T[n + i] * p0 + s.T[2 * n + i] * p1;
-  if (eyu) dv -= s.T[n + i - w] * s.p[i - w] + s.T[2 * n + i - w] * s.p[n + i - w];
-  // divergence of q[0:2] and q[2:4]
-  float d0 = ex ? s.q[i] : 0.f, d1 = ex ? s.q[2 * n + i] : 0.f;
-  if (exl) { d0 -= s.q[i - 1]; d1 -= s.q[2 * n + i - 1]; }
-  if (ey) { d0 += s.q[n + i]; d1 += s.q[3 * n + i]; }
-  if (eyu) { d0 -= s.q[n + i - w]; d1 -= s.q[3 * n + i - w]; }
-
-  const float tau_u = s.S[n + i], tau_v = s.S[2 * n + i];
-  const float u = s.u[i];
-  const float u_hat = u + (tau_u * s.alpha1) * dv;
-  const float g = s.iu[i];
-  const float rho_hat = s.rho0[i] + (u_hat - s.u_omega[i]) * g;
-  const float u_new = shrink_step<float>(u_hat, rho_hat, g, tau_u, s.lam);
-  const float v0 = s.v[i], v1 = s.v[n + i];
-  const float v0n = v0 + tau_v * (s.alpha0 * d0 + s.alpha1 * p0);
-  const float v1n = v1 + tau_v * (s.alpha0 * d1 + s.alpha1 * p1);
-  s.u[i] = u_new;
-  s.v[i] = v0n; s.v[n + i] = v1n;
-  s.u_bar[i] = u_new + s.theta * (u_new - u);
-  s.v_bar[i] = v0n + s.theta * (v0n - v0);
-  s.v_bar[n + i] = v1n + s.theta * (v1n - v1);
+  const Flux f = flux_at(s, i, x, y);
+  const Flux fl = x > 0 ? flux_at(s, i - 1, x - 1, y) : Flux{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const Flux fu = y > 0 ? flux_at(s, i - s.w, x, y - 1) : Flux{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  // backward differences in the reference's order: ((f - f_left) + f_y) - f_up
+  const float dv = ((f.px - fl.px) + f.py) - fu.py;
+  const float d0 = ((f.q0x - fl.q0x) + f.q0y) - fu.q0y;
+  const float d1 = ((f.q1x - fl.q1x) + f.q1y) - fu.q1y;
+  float u = s.u[i], v0 = s.v[i], v1 = s.v[n + i], ub, vb0, vb1;
+  primal_update(dv, d0, d1, s.S[n + i], s.S[2 * n + i], s.iu[i], s.rho0[i], s.u_omega[i], s.p[i],
+                s.p[n + i], s.lam, s.alpha0, s.alpha1, s.theta, u, v0, v1, ub, vb0, vb1);
+  s.u[i] = u;
+  s.v[i] = v0; s.v[n + i] = v1;
+  s.u_bar[i] = ub;
+  s.v_bar[i] = vb0; s.v_bar[n + i] = vb1;
 }
 
 // Warp prologue part 1 (solver.py:332-337): i1w at x+w, trajectory direction
@@ -269,6 +238,18 @@ int warp_linearize_internal(const fsb_level* L, cudaStream_t st) {
   dim3 blk(kBX, kBY), grd = grid2d(L->w, L->h, blk);
   k_warp_sample<<<grd, blk, 0, st>>>(*L);
   k_warp_linearize<<<grd, blk, 0, st>>>(*L);
+  return launch_status();
+}
+
+int warp_sample_internal(const fsb_level* L, cudaStream_t st) {
+  dim3 blk(kBX, kBY), grd = grid2d(L->w, L->h, blk);
+  k_warp_sample<<<grd, blk, 0, st>>>(*L);
+  return launch_status();
+}
+
+int mean_finish_internal(const double* partials, int nparts, const uint8_t* mask, size_t n,
+                         double* out, cudaStream_t st) {
+  k_mean_finish<<<1, 256, 0, st>>>(partials, nparts, mask, n, out);
   return launch_status();
 }
 

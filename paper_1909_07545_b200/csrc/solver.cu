@@ -6,6 +6,7 @@
 // fields.py:159-167 (translation_only_rig), camera.py:66-77 (scaled_to).
 
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -37,6 +38,30 @@ int warp_linearize_internal(const fsb_level* L, cudaStream_t st);
 int warp_finish_internal(const fsb_level* L, const fsb_params* prm, float* dmax, double* dmean,
                          cudaStream_t st);
 size_t level_partials_internal(int h, int w);
+int warp_sample_internal(const fsb_level* L, cudaStream_t st);
+int mean_finish_internal(const double* partials, int nparts, const uint8_t* mask, size_t n,
+                         double* out, cudaStream_t st);
+struct StateSet {
+  float* u; float* ub; float* v; float* vb; float* p; float* q;
+};
+struct BlockArgs {
+  int h, w;
+  size_t n;
+  StateSet src, dst;
+  const uint8_t* mask;
+  const float* T;
+  const float* S;
+  float* iu; float* rho0; float* u_omega;
+  float lam, alpha0, alpha1, theta, sigma_q, du_max;
+  int iters;
+  const float* i0; const float* i1w; const uint8_t* i1w_ok; const float* dirs;
+  const uint8_t* dir_ok;
+  float* wv; const float* i1; const float* traj; const uint8_t* traj_ok;
+  float* i1w_next; uint8_t* i1w_ok_next; float* dirs_next; uint8_t* dir_ok_next;
+  float* diag_p; float* diag_q; float* diag_du; double* partials;
+};
+int pd_block_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st,
+                    int* nblocks);
 
 namespace {
 
@@ -93,6 +118,8 @@ struct LevelState {  // state buffers sized for the finest level, reused per lev
   float *u_bar, *v, *v_bar, *p, *q, *T, *S, *u_omega, *iu, *rho0, *i1w, *dirs;
   uint8_t *i1w_ok, *dir_ok;
   double* partials;
+  float *state_b, *i1w_b, *dirs_b;
+  uint8_t *i1w_ok_b, *dir_ok_b;
 };
 
 struct Plan {
@@ -158,6 +185,11 @@ int make_plan(const fsb_rig* rig, const fsb_params* prm, void* base, Plan& P) {
   s.i1w_ok = c.take<uint8_t>(n0);
   s.dir_ok = c.take<uint8_t>(n0);
   s.partials = c.take<double>(level_partials_internal(H, W) + 64);
+  s.state_b = c.take<float>(12 * n0);
+  s.i1w_b = c.take<float>(n0);
+  s.dirs_b = c.take<float>(2 * n0);
+  s.i1w_ok_b = c.take<uint8_t>(n0);
+  s.dir_ok_b = c.take<uint8_t>(n0);
   P.bytes = c.off;
   return FSB_OK;
 }
@@ -172,6 +204,136 @@ __global__ void k_and_mask(const uint8_t* __restrict__ a, const uint8_t* __restr
 
 size_t level_partials_count(int h, int w) { return level_partials_internal(h, w) + 64; }
 
+namespace {
+
+// PD iterations per launch of the blocked kernel (= its halo). FSB_PD_HALO
+// overrides for tuning experiments (1, 2, 3 or 5).
+int pd_halo(int K) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("FSB_PD_HALO");
+    env = e ? atoi(e) : 0;
+  }
+  int h = env > 0 ? env : 5;
+  if (K < h) h = K <= 1 ? 1 : (K == 2 ? 2 : (K == 3 ? 3 : 5));
+  return h;
+}
+
+StateSet set_a(const fsb_level* L) {
+  return StateSet{L->u, L->u_bar, L->v, L->v_bar, L->p, L->q};
+}
+StateSet set_b(const fsb_level* L) {
+  const size_t n = (size_t)L->h * L->w;
+  float* B = L->state_b;
+  return StateSet{B, B + n, B + 2 * n, B + 4 * n, B + 6 * n, B + 8 * n};
+}
+
+void copy_set(const StateSet& d, const StateSet& s, size_t n, cudaStream_t st) {
+  cudaMemcpyAsync(d.u, s.u, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(d.ub, s.ub, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(d.v, s.v, 2 * n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(d.vb, s.vb, 2 * n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(d.p, s.p, 2 * n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(d.q, s.q, 4 * n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+}
+
+// The warp loop with the temporally blocked kernel: per warp ceil(K / halo)
+// launches, the first fusing the linearisation, the last the clip/accumulate
+// epilogue and the next warp's samples (solver.py:331-365).
+int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag* diag,
+                      int64_t pd_off, int64_t warp_off, cudaStream_t st) {
+  const size_t n = (size_t)L->h * L->w;
+  const int N = prm->warp_iters, K = prm->pd_iters;
+  const int halo = pd_halo(K);
+  int rc = warp_sample_internal(L, st);  // samples of warp 0 into buffer 0
+  if (rc) return rc;
+  StateSet sets[2] = {set_a(L), set_b(L)};
+  float* i1w[2] = {L->i1w, L->i1w_b};
+  uint8_t* i1w_ok[2] = {L->i1w_ok, L->i1w_ok_b};
+  float* dirs[2] = {L->dirs, L->dirs_b};
+  uint8_t* dir_ok[2] = {L->dir_ok, L->dir_ok_b};
+  int cur = 0, wb = 0;
+  BlockArgs A;
+  memset(&A, 0, sizeof(A));
+  A.h = L->h; A.w = L->w; A.n = n;
+  A.mask = L->mask; A.T = L->tensor; A.S = L->steps;
+  A.iu = L->iu; A.rho0 = L->rho0; A.u_omega = L->u_omega;
+  A.lam = (float)prm->lam; A.alpha0 = (float)prm->alpha0; A.alpha1 = (float)prm->alpha1;
+  A.theta = (float)prm->theta; A.sigma_q = (float)(1.0 / (2.0 * prm->alpha0));
+  A.du_max = (float)prm->du_max;
+  A.i0 = L->i0; A.wv = L->wv; A.i1 = L->i1; A.traj = L->traj; A.traj_ok = L->traj_ok;
+  A.partials = L->partials;
+  const bool dpq = diag && diag->max_p_norm && diag->max_q_norm;
+  const bool ddu = diag && diag->max_du && diag->mean_abs_du;
+  for (int wi = 0; wi < N; ++wi) {
+    A.i1w = i1w[wb]; A.i1w_ok = i1w_ok[wb]; A.dirs = dirs[wb]; A.dir_ok = dir_ok[wb];
+    const bool last_warp = wi == N - 1;
+    A.i1w_next = last_warp ? nullptr : i1w[wb ^ 1];
+    A.i1w_ok_next = i1w_ok[wb ^ 1]; A.dirs_next = dirs[wb ^ 1]; A.dir_ok_next = dir_ok[wb ^ 1];
+    int done = 0, nblocks = 0;
+    while (done < K) {
+      const int it = K - done < halo ? K - done : halo;
+      const bool lin = done == 0, fin = done + it == K;
+      A.src = sets[cur]; A.dst = sets[cur ^ 1];
+      A.iters = it;
+      A.diag_p = dpq ? diag->max_p_norm + pd_off + (int64_t)wi * K + done : nullptr;
+      A.diag_q = dpq ? diag->max_q_norm + pd_off + (int64_t)wi * K + done : nullptr;
+      A.diag_du = (fin && ddu) ? diag->max_du + warp_off + wi : nullptr;
+      rc = pd_block_launch(A, halo, lin, fin, st, &nblocks);
+      if (rc) return rc;
+      cur ^= 1;
+      done += it;
+    }
+    if (ddu) {
+      rc = mean_finish_internal(L->partials, nblocks, L->mask, n,
+                                diag->mean_abs_du + warp_off + wi, st);
+      if (rc) return rc;
+    }
+    wb ^= 1;
+  }
+  if (cur != 0) copy_set(sets[0], sets[1], n, st);
+  if (wb != 0) {  // leave the last samples in the primary buffers (per-stage API contract)
+    cudaMemcpyAsync(L->dirs, L->dirs_b, 2 * n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(L->dir_ok, L->dir_ok_b, n, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(L->i1w, L->i1w_b, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(L->i1w_ok, L->i1w_ok_b, n, cudaMemcpyDeviceToDevice, st);
+  }
+  return launch_status();
+}
+
+// `iters` plain PD cycles with the blocked kernel (no fused prologue/epilogue);
+// the result ends in the primary state set.
+int pd_iterate_blocked(const fsb_level* L, const fsb_params* prm, int iters, float* dp, float* dq,
+                       cudaStream_t st) {
+  const size_t n = (size_t)L->h * L->w;
+  const int halo = pd_halo(iters);
+  StateSet sets[2] = {set_a(L), set_b(L)};
+  BlockArgs A;
+  memset(&A, 0, sizeof(A));
+  A.h = L->h; A.w = L->w; A.n = n;
+  A.mask = L->mask; A.T = L->tensor; A.S = L->steps;
+  A.iu = L->iu; A.rho0 = L->rho0; A.u_omega = L->u_omega;
+  A.lam = (float)prm->lam; A.alpha0 = (float)prm->alpha0; A.alpha1 = (float)prm->alpha1;
+  A.theta = (float)prm->theta; A.sigma_q = (float)(1.0 / (2.0 * prm->alpha0));
+  A.du_max = (float)prm->du_max;
+  int cur = 0, done = 0;
+  while (done < iters) {
+    const int it = iters - done < halo ? iters - done : halo;
+    A.src = sets[cur]; A.dst = sets[cur ^ 1];
+    A.iters = it;
+    A.diag_p = (dp && dq) ? dp + done : nullptr;
+    A.diag_q = (dp && dq) ? dq + done : nullptr;
+    int rc = pd_block_launch(A, halo, false, false, st, nullptr);
+    if (rc) return rc;
+    cur ^= 1;
+    done += it;
+  }
+  if (cur != 0) copy_set(sets[0], sets[1], n, st);
+  return launch_status();
+}
+
+}  // namespace
+
 int solve_level_internal(const fsb_level* L, const fsb_params* prm, const fsb_diag* diag,
                          int64_t pd_off, int64_t warp_off, void* scratch, size_t scratch_bytes,
                          cudaStream_t st) {
@@ -184,6 +346,8 @@ int solve_level_internal(const fsb_level* L, const fsb_params* prm, const fsb_di
   cudaMemsetAsync(L->p, 0, 2 * n * sizeof(float), st);
   cudaMemsetAsync(L->q, 0, 4 * n * sizeof(float), st);
   cudaMemcpyAsync(L->u_bar, L->u, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  if (L->state_b && L->i1w_b && L->i1w_ok_b && L->dirs_b && L->dir_ok_b)
+    return warp_loop_blocked(L, prm, diag, pd_off, warp_off, st);
   const int N = prm->warp_iters, K = prm->pd_iters;
   for (int wi = 0; wi < N; ++wi) {
     rc = warp_linearize_internal(L, st);
@@ -296,6 +460,8 @@ int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const floa
     L.u = u; L.u_bar = S.u_bar; L.v = S.v; L.v_bar = S.v_bar; L.p = S.p; L.q = S.q;
     L.wv = wv; L.u_omega = S.u_omega; L.iu = S.iu; L.rho0 = S.rho0; L.i1w = S.i1w;
     L.i1w_ok = S.i1w_ok; L.dirs = S.dirs; L.dir_ok = S.dir_ok; L.partials = S.partials;
+    L.state_b = S.state_b; L.i1w_b = S.i1w_b; L.i1w_ok_b = S.i1w_ok_b; L.dirs_b = S.dirs_b;
+    L.dir_ok_b = S.dir_ok_b;
     rc = solve_level_internal(&L, prm, diag, pd_off, warp_off, P.setup_scratch,
                               P.setup_scratch_bytes, st);
     if (rc) return rc;
@@ -341,6 +507,7 @@ int fsb_warp_linearize(const fsb_level* lv, void* stream) {
 int fsb_pd_iterate(const fsb_level* lv, const fsb_params* prm, int32_t iters, float* diag_p,
                    float* diag_q, void* stream) {
   if (!lv || !prm || iters < 0 || lv->h < 1 || lv->w < 1) return FSB_EINVAL;
+  if (lv->state_b) return pd_iterate_blocked(lv, prm, iters, diag_p, diag_q, as_stream(stream));
   return pd_iterate_internal(lv, prm, iters, diag_p, diag_q, as_stream(stream));
 }
 

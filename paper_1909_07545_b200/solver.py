@@ -119,7 +119,7 @@ def _from_planes(t: torch.Tensor) -> np.ndarray:
 class _Level:
     """Device buffers of one pyramid level, viewable as the C `fsb_level`."""
 
-    def __init__(self, h: int, w: int):
+    def __init__(self, h: int, w: int, blocked: bool = True):
         self.h, self.w = h, w
         E = _dev.empty
         U8 = torch.uint8
@@ -133,6 +133,12 @@ class _Level:
         self.iu = E((h, w)); self.rho0 = E((h, w)); self.i1w = E((h, w))
         self.i1w_ok = E((h, w), U8); self.dirs = E((h, w, 2)); self.dir_ok = E((h, w), U8)
         self.partials = E((int(_ext.lib().fsb_level_partials(h, w)),), torch.float64)
+        # second state / sample set -> temporally blocked PD kernel (K6)
+        self.state_b = E((12, h, w)) if blocked else None
+        self.i1w_b = E((h, w)) if blocked else None
+        self.i1w_ok_b = E((h, w), U8) if blocked else None
+        self.dirs_b = E((h, w, 2)) if blocked else None
+        self.dir_ok_b = E((h, w), U8) if blocked else None
 
     def struct(self) -> _ext.FsbLevel:
         s = _ext.FsbLevel()
@@ -214,12 +220,17 @@ def thresholding_step(u_hat, rho_hat, iu, tau_u, lam: float):
 
 
 def primal_dual_iterate(state: SolverState, t, iu, rho0, u_omega, params: SolverParams, mask,
-                        steps: _StepSizes | None = None) -> SolverState:
-    """One primal-dual cycle on the GPU (solver.py:279-303)."""
+                        steps: _StepSizes | None = None, *, blocked: bool = False,
+                        iters: int = 1) -> SolverState:
+    """`iters` primal-dual cycles on the GPU (solver.py:279-303); one by default.
+
+    blocked=True runs them in the temporally blocked tile kernel (K6) instead of
+    the one-iteration-per-launch kernels.
+    """
     L = _ext.lib()
     u = np.asarray(state.u, dtype=np.float64)
     h, w = u.shape
-    lv = _Level(h, w)
+    lv = _Level(h, w, blocked=blocked)
     lv.mask.copy_(_dev.upload(np.asarray(mask, dtype=bool), torch.uint8))
     lv.tensor.copy_(_planes(t, 3))
     if steps is None:
@@ -232,8 +243,8 @@ def primal_dual_iterate(state: SolverState, t, iu, rho0, u_omega, params: Solver
     lv.u_omega.copy_(_dev.upload(u_omega))
     prm = _ext.params_struct(params)
     st = lv.struct()
-    _ext.check(L.fsb_pd_iterate(C.byref(st), C.byref(prm), 1, None, None, _dev.stream_ptr()),
-               "primal_dual_iterate")
+    _ext.check(L.fsb_pd_iterate(C.byref(st), C.byref(prm), int(iters), None, None,
+                                _dev.stream_ptr()), "primal_dual_iterate")
     return SolverState(u=_dev.download(lv.u), v=_from_planes(lv.v), p=_from_planes(lv.p),
                        q=_from_planes(lv.q), u_bar=_dev.download(lv.u_bar),
                        v_bar=_from_planes(lv.v_bar))
@@ -257,12 +268,18 @@ def image_derivative_along(dirs, i1w, i1w_valid, mask):
 
 
 def solve_level(i0, i1, traj_dirs, traj_valid, params: SolverParams, mask, init: WarpState,
-                diagnostics: Diagnostics | None = None) -> tuple[WarpState, SolverState]:
-    """Warping loop on one pyramid level, all on the GPU (solver.py:306-367)."""
+                diagnostics: Diagnostics | None = None, *,
+                blocked: bool = True) -> tuple[WarpState, SolverState]:
+    """Warping loop on one pyramid level, all on the GPU (solver.py:306-367).
+
+    `blocked=False` selects the one-iteration-per-launch kernels (the v1 path,
+    kept as an on-device cross-check of the temporally blocked kernel).
+    """
     L = _ext.lib()
     m = np.asarray(mask, dtype=bool)
     h, w = m.shape
-    lv = _Level(h, w)
+    record = diagnostics is not None and diagnostics.record_increments
+    lv = _Level(h, w, blocked=blocked and not record)
     lv.i1.copy_(_dev.upload(i1))
     lv.traj.copy_(_dev.upload(traj_dirs))
     lv.traj_ok.copy_(_dev.upload(np.asarray(traj_valid, dtype=bool), torch.uint8))
@@ -272,7 +289,6 @@ def solve_level(i0, i1, traj_dirs, traj_valid, params: SolverParams, mask, init:
     N, K = params.warp_iters, params.pd_iters
     if diagnostics is not None:
         diagnostics.du_max_limit = params.du_max
-    record = diagnostics is not None and diagnostics.record_increments
     dp = _dev.zeros((N * K,)); dq = _dev.zeros((N * K,))
     dmx = _dev.zeros((N,)); dmean = _dev.zeros((N,), torch.float64)
     if not record:
