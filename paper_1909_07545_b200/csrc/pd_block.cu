@@ -18,6 +18,8 @@
 // State is ping-ponged between two plane sets (src -> dst) because halos read
 // neighbours' old values while their owners write new ones.
 
+#include <stdlib.h>
+
 #include "pd_math.cuh"
 
 namespace fsb {
@@ -304,22 +306,41 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_block(const BlockArgs A) {
   }
 }
 
-// Tile shape: 64 x 32 extended tile, 256 threads, 8 pixels per thread.
-constexpr int kCX = 2, kNW = 8, kPY = 4;
-
-template <int R, bool LIN, bool FIN>
-int launch_block(const BlockArgs& A, cudaStream_t st, int* nblocks) {
-  using TL = Tile<kCX, kNW, kPY, R>;
+// Tile shapes (FSB_PD_TILE selects for tuning):
+//   0: 64 x 32 ext tile, 256 threads x 8 px     1: 64 x 32, 512 threads x 4 px
+//   2: 128 x 32, 512 threads x 8 px            3: 64 x 64, 512 threads x 8 px
+template <int CX, int NW, int PY, int R, bool LIN, bool FIN>
+int launch_shape(const BlockArgs& A, cudaStream_t st, int* nblocks) {
+  using TL = Tile<CX, NW, PY, R>;
   static bool attr = false;
-  auto kern = k_pd_block<kCX, kNW, kPY, R, LIN, FIN>;
+  auto kern = k_pd_block<CX, NW, PY, R, LIN, FIN>;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TL::SMEM);
     attr = true;
   }
   dim3 grd((A.w + TL::TW - 1) / TL::TW, (A.h + TL::TH - 1) / TL::TH);
   if (nblocks) *nblocks = (int)(grd.x * grd.y);
-  kern<<<grd, kNW * 32, TL::SMEM, st>>>(A);
+  kern<<<grd, NW * 32, TL::SMEM, st>>>(A);
   return launch_status();
+}
+
+int tile_choice() {
+  static int t = -1;
+  if (t < 0) {
+    const char* e = getenv("FSB_PD_TILE");
+    t = e ? atoi(e) : 1;
+  }
+  return t;
+}
+
+template <int R, bool LIN, bool FIN>
+int launch_block(const BlockArgs& A, cudaStream_t st, int* nblocks) {
+  switch (tile_choice()) {
+    case 0: return launch_shape<2, 8, 4, R, LIN, FIN>(A, st, nblocks);
+    case 2: return launch_shape<4, 16, 2, R, LIN, FIN>(A, st, nblocks);
+    case 3: return launch_shape<2, 16, 4, R, LIN, FIN>(A, st, nblocks);
+    default: return launch_shape<2, 16, 2, R, LIN, FIN>(A, st, nblocks);
+  }
 }
 
 template <int R>
@@ -335,10 +356,6 @@ int launch_r(const BlockArgs& A, bool lin, bool fin, cudaStream_t st, int* nb) {
 // Halo (= maximum iterations per launch) compiled in.
 int pd_block_max_iters() { return 5; }
 
-size_t pd_block_partials(int h, int w) {
-  using TL = Tile<kCX, kNW, kPY, 1>;
-  return (size_t)((w + TL::TW - 1) / TL::TW) * ((h + TL::TH - 1) / TL::TH);
-}
 
 int pd_block_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st,
                     int* nblocks) {

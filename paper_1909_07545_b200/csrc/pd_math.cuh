@@ -32,18 +32,21 @@ FSB_INLINE void dual_update(float a, float b, float c, float sp, float sq, float
                             float& p0, float& p1, float& q0, float& q1, float& q2, float& q3) {
   p0 = p0 + sp * ((a * gx + b * gy) - vb0);
   p1 = p1 + sp * ((b * gx + c * gy) - vb1);
+  // x / max(1, |x|): the divisor is exactly 1 inside the ball, where the
+  // approximate reciprocal is exact too; elsewhere <= 2 ulp (fp32 path).
   const float pd = fmaxf(1.f, sqrtf(p0 * p0 + p1 * p1));
-  p0 = p0 / pd;
-  p1 = p1 / pd;
+  p0 = __fdividef(p0, pd);
+  p1 = __fdividef(p1, pd);
   q0 = q0 + sq * g00;
   q1 = q1 + sq * g01;
   q2 = q2 + sq * g10;
   q3 = q3 + sq * g11;
   const float qd = fmaxf(1.f, sqrtf((q0 * q0 + q1 * q1) + (q2 * q2 + q3 * q3)));
-  q0 = q0 / qd;
-  q1 = q1 / qd;
-  q2 = q2 / qd;
-  q3 = q3 / qd;
+  const float rq = __fdividef(1.f, qd);
+  q0 = q0 * rq;
+  q1 = q1 * rq;
+  q2 = q2 * rq;
+  q3 = q3 * rq;
 }
 
 // Edge-masked fluxes of one pixel: the x / y components of T p and of the two
