@@ -62,6 +62,13 @@ struct Tile {
   static_assert(TW > 0 && TH > 0, "halo larger than tile");
 };
 
+// Skipping rows outside the shrinking valid region saves ~15% of the work but
+// splits the unrolled pixel loop into per-row branches (less ILP).
+#ifndef FSB_PD_SKIP_ROWS
+#define FSB_PD_SKIP_ROWS 0
+#endif
+constexpr bool kSkipRows = FSB_PD_SKIP_ROWS != 0;
+
 __device__ __forceinline__ int sidx(int r, int c, int SW) { return (r + 1) * SW + (c + 1); }
 
 // Next warp's samples at x + w (solver.py:332-337), one pixel.
@@ -103,9 +110,18 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_block(const BlockArgs A) {
   const int ox = (int)blockIdx.x * TL::TW - R, oy = (int)blockIdx.y * TL::TH - R;
   const size_t n = A.n;
 
-  for (int k = threadIdx.x; k < TL::NPLANES * PL; k += NW * 32) smem[k] = 0.f;
-  for (int k = threadIdx.x; k < PL; k += NW * 32) s_m[k] = 0;
-  __syncthreads();
+  // zero the 1-px pad ring of every plane (interior cells are all written below)
+  constexpr int RING = 2 * (EW + 2) + 2 * EH;
+  for (int k = threadIdx.x; k < RING; k += NW * 32) {
+    int idx;
+    if (k < EW + 2) idx = k;                                   // top pad row
+    else if (k < 2 * (EW + 2)) idx = (EH + 1) * SW + (k - (EW + 2));  // bottom pad row
+    else if (k < 2 * (EW + 2) + EH) idx = (k - 2 * (EW + 2) + 1) * SW;  // left pad column
+    else idx = (k - 2 * (EW + 2) - EH + 1) * SW + EW + 1;        // right pad column
+#pragma unroll
+    for (int pl = 0; pl < TL::NPLANES; ++pl) smem[pl * PL + idx] = 0.f;
+    s_m[idx] = 0;
+  }
 
   // per-pixel registers
   float u[NPX], v0[NPX], v1[NPX], p0[NPX], p1[NPX], q0[NPX], q1[NPX], q2[NPX], q3[NPX];
@@ -181,7 +197,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_block(const BlockArgs A) {
 #pragma unroll
     for (int j = 0; j < PY; ++j) {
       const int r = warp + NW * j;
-      if (r < it - 1 || r > EH - 1 - it) continue;
+      if (kSkipRows && (r < it - 1 || r > EH - 1 - it)) continue;
 #pragma unroll
       for (int cx = 0; cx < CX; ++cx) {
         const int k = j * CX + cx;
@@ -227,7 +243,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_block(const BlockArgs A) {
 #pragma unroll
     for (int j = 0; j < PY; ++j) {
       const int r = warp + NW * j;
-      if (r < it || r > EH - 1 - it) continue;
+      if (kSkipRows && (r < it || r > EH - 1 - it)) continue;
 #pragma unroll
       for (int cx = 0; cx < CX; ++cx) {
         const int k = j * CX + cx;
@@ -306,9 +322,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_block(const BlockArgs A) {
   }
 }
 
-// Tile shapes (FSB_PD_TILE selects for tuning):
+// Tile shapes (FSB_PD_TILE selects for tuning; larger tiles spill at 512 threads):
 //   0: 64 x 32 ext tile, 256 threads x 8 px     1: 64 x 32, 512 threads x 4 px
-//   2: 128 x 32, 512 threads x 8 px            3: 64 x 64, 512 threads x 8 px
 template <int CX, int NW, int PY, int R, bool LIN, bool FIN>
 int launch_shape(const BlockArgs& A, cudaStream_t st, int* nblocks) {
   using TL = Tile<CX, NW, PY, R>;
@@ -337,8 +352,6 @@ template <int R, bool LIN, bool FIN>
 int launch_block(const BlockArgs& A, cudaStream_t st, int* nblocks) {
   switch (tile_choice()) {
     case 0: return launch_shape<2, 8, 4, R, LIN, FIN>(A, st, nblocks);
-    case 2: return launch_shape<4, 16, 2, R, LIN, FIN>(A, st, nblocks);
-    case 3: return launch_shape<2, 16, 4, R, LIN, FIN>(A, st, nblocks);
     default: return launch_shape<2, 16, 2, R, LIN, FIN>(A, st, nblocks);
   }
 }

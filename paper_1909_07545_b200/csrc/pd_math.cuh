@@ -32,17 +32,18 @@ FSB_INLINE void dual_update(float a, float b, float c, float sp, float sq, float
                             float& p0, float& p1, float& q0, float& q1, float& q2, float& q3) {
   p0 = p0 + sp * ((a * gx + b * gy) - vb0);
   p1 = p1 + sp * ((b * gx + c * gy) - vb1);
-  // x / max(1, |x|): the divisor is exactly 1 inside the ball, where the
-  // approximate reciprocal is exact too; elsewhere <= 2 ulp (fp32 path).
-  const float pd = fmaxf(1.f, sqrtf(p0 * p0 + p1 * p1));
-  p0 = __fdividef(p0, pd);
-  p1 = __fdividef(p1, pd);
+  // x / max(1, |x|) (solver.py:221-223): identity inside the unit ball (exactly
+  // as the reference, divisor 1), x * rsqrt(|x|^2) outside (<= 2 ulp, fp32 path).
+  const float pn2 = p0 * p0 + p1 * p1;
+  const float rp = pn2 > 1.f ? rsqrtf(pn2) : 1.f;
+  p0 = p0 * rp;
+  p1 = p1 * rp;
   q0 = q0 + sq * g00;
   q1 = q1 + sq * g01;
   q2 = q2 + sq * g10;
   q3 = q3 + sq * g11;
-  const float qd = fmaxf(1.f, sqrtf((q0 * q0 + q1 * q1) + (q2 * q2 + q3 * q3)));
-  const float rq = __fdividef(1.f, qd);
+  const float qn2 = (q0 * q0 + q1 * q1) + (q2 * q2 + q3 * q3);
+  const float rq = qn2 > 1.f ? rsqrtf(qn2) : 1.f;
   q0 = q0 * rq;
   q1 = q1 * rq;
   q2 = q2 * rq;
