@@ -191,6 +191,11 @@ typedef struct fsb_level {
   uint8_t* i1w_ok_b;
   float* dirs_b;
   uint8_t* dir_ok_b;
+  /* Optional gather fast path: (h,w,4) {i1, traj.x, traj.y, 0} and a byte map
+   * whose bit0 / bit1 say all 16 bicubic taps around (x,y) are in bounds and in
+   * mask / traj_ok (filled by fsb_level_setup when non-NULL). */
+  float* packed;
+  uint8_t* full16;
 } fsb_level;
 
 size_t fsb_level_partials(int32_t h, int32_t w);

@@ -10,6 +10,7 @@
 // planes so every load of a warp is a coalesced 128-byte line.
 
 #include "pd_math.cuh"
+#include "warp_math.cuh"
 
 namespace fsb {
 
@@ -109,22 +110,42 @@ __global__ void __launch_bounds__(256) k_warp_sample(fsb_level L) {
   int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= L.w || y >= L.h) return;
   const size_t i = (size_t)y * L.w + x;
-  const float2 wv = reinterpret_cast<const float2*>(L.wv)[i];
-  const double px = (double)x + (double)wv.x, py = (double)y + (double)wv.y;
-  float iv[1];
-  bool wok = bicubic_sample<1, float>(L.i1, L.mask, L.h, L.w, px, py, iv);
-  float dr[2];
-  bool dok = bicubic_sample<2, float>(L.traj, L.traj_ok, L.h, L.w, px, py, dr);
-  const bool mk = L.mask[i] != 0;
-  float d0 = 0.f, d1 = 0.f;
-  if (dok) {
-    float nrm = sqrtf(dr[0] * dr[0] + dr[1] * dr[1]);
-    if (nrm > 0.5f && mk) { d0 = dr[0] / nrm; d1 = dr[1] / nrm; } else dok = false;
-  }
-  L.i1w[i] = wok ? iv[0] : 0.f;
-  L.i1w_ok[i] = wok && mk;
-  reinterpret_cast<float2*>(L.dirs)[i] = make_float2(d0, d1);
+  const SampleSrc S{L.i1, L.mask, L.traj, L.traj_ok, reinterpret_cast<const float4*>(L.packed),
+                    L.full16, L.h, L.w};
+  float iw;
+  bool iok, dok;
+  float2 d;
+  warp_sample_px(S, x, y, reinterpret_cast<const float2*>(L.wv)[i], L.mask[i] != 0, iw, iok, d,
+                 dok);
+  L.i1w[i] = iw;
+  L.i1w_ok[i] = iok;
+  reinterpret_cast<float2*>(L.dirs)[i] = d;
   L.dir_ok[i] = dok;
+}
+
+// Per-level gather tables: packed {i1, traj} texels and the all-16-taps-valid
+// flags of the mask and of traj_ok.
+__global__ void k_pack_level(fsb_level L) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
+  int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= L.w || y >= L.h) return;
+  const size_t i = (size_t)y * L.w + x;
+  const float2 t = reinterpret_cast<const float2*>(L.traj)[i];
+  reinterpret_cast<float4*>(L.packed)[i] = make_float4(L.i1[i], t.x, t.y, 0.f);
+  uint8_t fl = 0;
+  if (x >= 1 && x + 2 < L.w && y >= 1 && y + 2 < L.h) {
+    bool am = true, at = true;
+#pragma unroll
+    for (int a = -1; a <= 2; ++a)
+#pragma unroll
+      for (int b = -1; b <= 2; ++b) {
+        const size_t k = (size_t)(y + a) * L.w + (x + b);
+        am = am && L.mask[k];
+        at = at && L.traj_ok[k];
+      }
+    fl = (am ? 1 : 0) | (at ? 2 : 0);
+  }
+  L.full16[i] = fl;
 }
 
 // Warp prologue part 2 (solver.py:339-346 with image_derivative_along 192-202):
@@ -244,6 +265,12 @@ int warp_linearize_internal(const fsb_level* L, cudaStream_t st) {
 int warp_sample_internal(const fsb_level* L, cudaStream_t st) {
   dim3 blk(kBX, kBY), grd = grid2d(L->w, L->h, blk);
   k_warp_sample<<<grd, blk, 0, st>>>(*L);
+  return launch_status();
+}
+
+int pack_level_internal(const fsb_level* L, cudaStream_t st) {
+  dim3 blk(kBX, kBY), grd = grid2d(L->w, L->h, blk);
+  k_pack_level<<<grd, blk, 0, st>>>(*L);
   return launch_status();
 }
 

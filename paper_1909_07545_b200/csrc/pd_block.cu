@@ -21,6 +21,7 @@
 #include <stdlib.h>
 
 #include "pd_math.cuh"
+#include "warp_math.cuh"
 
 namespace fsb {
 
@@ -44,6 +45,7 @@ struct BlockArgs {
   // FIN: accumulate w, then sample the next warp into the *_next buffers
   float* wv; const float* i1; const float* traj; const uint8_t* traj_ok;
   float* i1w_next; uint8_t* i1w_ok_next; float* dirs_next; uint8_t* dir_ok_next;
+  const float* packed; const uint8_t* full16;
   // diagnostics (nullptr = off)
   float* diag_p; float* diag_q; float* diag_du; double* partials;
 };
@@ -74,19 +76,15 @@ __device__ __forceinline__ int sidx(int r, int c, int SW) { return (r + 1) * SW 
 // Next warp's samples at x + w (solver.py:332-337), one pixel.
 __device__ __forceinline__ void sample_next(const BlockArgs& A, int gx, int gy, size_t gi,
                                             float2 wv, bool mk) {
-  const double px = (double)gx + (double)wv.x, py = (double)gy + (double)wv.y;
-  float iv[1];
-  const bool wok = bicubic_sample<1, float>(A.i1, A.mask, A.h, A.w, px, py, iv);
-  float dr[2];
-  bool dok = bicubic_sample<2, float>(A.traj, A.traj_ok, A.h, A.w, px, py, dr);
-  float d0 = 0.f, d1 = 0.f;
-  if (dok) {
-    const float nrm = sqrtf(dr[0] * dr[0] + dr[1] * dr[1]);
-    if (nrm > 0.5f && mk) { d0 = dr[0] / nrm; d1 = dr[1] / nrm; } else dok = false;
-  }
-  A.i1w_next[gi] = wok ? iv[0] : 0.f;
-  A.i1w_ok_next[gi] = wok && mk;
-  reinterpret_cast<float2*>(A.dirs_next)[gi] = make_float2(d0, d1);
+  const SampleSrc S{A.i1, A.mask, A.traj, A.traj_ok, reinterpret_cast<const float4*>(A.packed),
+                    A.full16, A.h, A.w};
+  float iw;
+  bool iok, dok;
+  float2 d;
+  warp_sample_px(S, gx, gy, wv, mk, iw, iok, d, dok);
+  A.i1w_next[gi] = iw;
+  A.i1w_ok_next[gi] = iok;
+  reinterpret_cast<float2*>(A.dirs_next)[gi] = d;
   A.dir_ok_next[gi] = dok;
 }
 

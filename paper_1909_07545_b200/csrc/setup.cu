@@ -296,9 +296,5 @@ int fsb_precondition_steps(const float* tensor, const uint8_t* mask, int32_t h, 
   return launch_status();
 }
 
-int fsb_level_setup(const fsb_level* lv, const fsb_params* prm, void* scratch,
-                    size_t scratch_bytes, void* stream) {
-  return level_setup_internal(lv, prm, scratch, scratch_bytes, as_stream(stream));
-}
 
 }  // extern "C"

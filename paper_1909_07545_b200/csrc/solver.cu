@@ -39,6 +39,7 @@ int warp_finish_internal(const fsb_level* L, const fsb_params* prm, float* dmax,
                          cudaStream_t st);
 size_t level_partials_internal(int h, int w);
 int warp_sample_internal(const fsb_level* L, cudaStream_t st);
+int pack_level_internal(const fsb_level* L, cudaStream_t st);
 int mean_finish_internal(const double* partials, int nparts, const uint8_t* mask, size_t n,
                          double* out, cudaStream_t st);
 struct StateSet {
@@ -58,6 +59,7 @@ struct BlockArgs {
   const uint8_t* dir_ok;
   float* wv; const float* i1; const float* traj; const uint8_t* traj_ok;
   float* i1w_next; uint8_t* i1w_ok_next; float* dirs_next; uint8_t* dir_ok_next;
+  const float* packed; const uint8_t* full16;
   float* diag_p; float* diag_q; float* diag_du; double* partials;
 };
 int pd_block_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st,
@@ -120,6 +122,8 @@ struct LevelState {  // state buffers sized for the finest level, reused per lev
   double* partials;
   float *state_b, *i1w_b, *dirs_b;
   uint8_t *i1w_ok_b, *dir_ok_b;
+  float* packed;
+  uint8_t* full16;
 };
 
 struct Plan {
@@ -190,6 +194,8 @@ int make_plan(const fsb_rig* rig, const fsb_params* prm, void* base, Plan& P) {
   s.dirs_b = c.take<float>(2 * n0);
   s.i1w_ok_b = c.take<uint8_t>(n0);
   s.dir_ok_b = c.take<uint8_t>(n0);
+  s.packed = c.take<float>(4 * n0);
+  s.full16 = c.take<uint8_t>(n0);
   P.bytes = c.off;
   return FSB_OK;
 }
@@ -217,6 +223,17 @@ int pd_halo(int K) {
   int h = env > 0 ? env : 5;
   if (K < h) h = K <= 1 ? 1 : (K == 2 ? 2 : (K == 3 ? 3 : 5));
   return h;
+}
+
+// Sample the next warp inside the fused epilogue (1) or in a separate
+// full-occupancy kernel after it (0). FSB_FUSED_SAMPLE overrides.
+bool fused_sample() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("FSB_FUSED_SAMPLE");
+    env = e ? atoi(e) : 0;
+  }
+  return env != 0;
 }
 
 StateSet set_a(const fsb_level* L) {
@@ -262,13 +279,15 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
   A.theta = (float)prm->theta; A.sigma_q = (float)(1.0 / (2.0 * prm->alpha0));
   A.du_max = (float)prm->du_max;
   A.i0 = L->i0; A.wv = L->wv; A.i1 = L->i1; A.traj = L->traj; A.traj_ok = L->traj_ok;
+  A.packed = L->packed; A.full16 = L->full16;
   A.partials = L->partials;
   const bool dpq = diag && diag->max_p_norm && diag->max_q_norm;
   const bool ddu = diag && diag->max_du && diag->mean_abs_du;
   for (int wi = 0; wi < N; ++wi) {
     A.i1w = i1w[wb]; A.i1w_ok = i1w_ok[wb]; A.dirs = dirs[wb]; A.dir_ok = dir_ok[wb];
     const bool last_warp = wi == N - 1;
-    A.i1w_next = last_warp ? nullptr : i1w[wb ^ 1];
+    const bool fused = fused_sample();
+    A.i1w_next = (last_warp || !fused) ? nullptr : i1w[wb ^ 1];
     A.i1w_ok_next = i1w_ok[wb ^ 1]; A.dirs_next = dirs[wb ^ 1]; A.dir_ok_next = dir_ok[wb ^ 1];
     int done = 0, nblocks = 0;
     while (done < K) {
@@ -283,6 +302,13 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
       if (rc) return rc;
       cur ^= 1;
       done += it;
+    }
+    if (!fused && !last_warp) {  // next warp's samples at the updated w
+      fsb_level Ln = *L;
+      Ln.i1w = i1w[wb ^ 1]; Ln.i1w_ok = i1w_ok[wb ^ 1];
+      Ln.dirs = dirs[wb ^ 1]; Ln.dir_ok = dir_ok[wb ^ 1];
+      rc = warp_sample_internal(&Ln, st);
+      if (rc) return rc;
     }
     if (ddu) {
       rc = mean_finish_internal(L->partials, nblocks, L->mask, n,
@@ -299,6 +325,15 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
     cudaMemcpyAsync(L->i1w_ok, L->i1w_ok_b, n, cudaMemcpyDeviceToDevice, st);
   }
   return launch_status();
+}
+
+// Level setup (tensor, steps) plus the gather tables when the level has them.
+int level_prepare(const fsb_level* L, const fsb_params* prm, void* scratch, size_t scratch_bytes,
+                  cudaStream_t st) {
+  int rc = level_setup_internal(L, prm, scratch, scratch_bytes, st);
+  if (rc) return rc;
+  if (L->packed && L->full16) return pack_level_internal(L, st);
+  return FSB_OK;
 }
 
 // `iters` plain PD cycles with the blocked kernel (no fused prologue/epilogue);
@@ -338,7 +373,7 @@ int solve_level_internal(const fsb_level* L, const fsb_params* prm, const fsb_di
                          int64_t pd_off, int64_t warp_off, void* scratch, size_t scratch_bytes,
                          cudaStream_t st) {
   const size_t n = (size_t)L->h * L->w;
-  int rc = level_setup_internal(L, prm, scratch, scratch_bytes, st);
+  int rc = level_prepare(L, prm, scratch, scratch_bytes, st);
   if (rc) return rc;
   // solver.py:323-327: v, p, q, v_bar start at zero, u_bar = u
   cudaMemsetAsync(L->v, 0, 2 * n * sizeof(float), st);
@@ -462,6 +497,7 @@ int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const floa
     L.i1w_ok = S.i1w_ok; L.dirs = S.dirs; L.dir_ok = S.dir_ok; L.partials = S.partials;
     L.state_b = S.state_b; L.i1w_b = S.i1w_b; L.i1w_ok_b = S.i1w_ok_b; L.dirs_b = S.dirs_b;
     L.dir_ok_b = S.dir_ok_b;
+    L.packed = S.packed; L.full16 = S.full16;
     rc = solve_level_internal(&L, prm, diag, pd_off, warp_off, P.setup_scratch,
                               P.setup_scratch_bytes, st);
     if (rc) return rc;
@@ -498,6 +534,12 @@ using namespace fsb;
 extern "C" {
 
 size_t fsb_level_partials(int32_t h, int32_t w) { return level_partials_count(h, w); }
+
+int fsb_level_setup(const fsb_level* lv, const fsb_params* prm, void* scratch,
+                    size_t scratch_bytes, void* stream) {
+  if (!lv || !prm || lv->h < 1 || lv->w < 1) return FSB_EINVAL;
+  return level_prepare(lv, prm, scratch, scratch_bytes, as_stream(stream));
+}
 
 int fsb_warp_linearize(const fsb_level* lv, void* stream) {
   if (!lv || lv->h < 1 || lv->w < 1) return FSB_EINVAL;

@@ -139,6 +139,8 @@ class _Level:
         self.i1w_ok_b = E((h, w), U8) if blocked else None
         self.dirs_b = E((h, w, 2)) if blocked else None
         self.dir_ok_b = E((h, w), U8) if blocked else None
+        self.packed = E((h, w, 4)) if blocked else None
+        self.full16 = E((h, w), U8) if blocked else None
 
     def struct(self) -> _ext.FsbLevel:
         s = _ext.FsbLevel()
