@@ -183,14 +183,10 @@ typedef struct fsb_level {
   float* dirs;           /* (h,w,2) sampled unit directions                */
   uint8_t* dir_ok;
   double* partials;      /* reduction scratch (fsb_level_partials(h,w))    */
-  /* Optional buffers of the temporally blocked path (all NULL = one-iteration
-   * kernels): a second state set of 12 planes (u, u_bar, v x2, v_bar x2, p x2,
-   * q x4) for ping-pong, and a second set of per-warp samples. */
+  /* Optional second state set of 12 planes (u, u_bar, v x2, v_bar x2, p x2,
+   * q x4) for the ping-pong of the temporally blocked PD kernel; NULL selects
+   * the one-iteration-per-launch kernels. */
   float* state_b;
-  float* i1w_b;
-  uint8_t* i1w_ok_b;
-  float* dirs_b;
-  uint8_t* dir_ok_b;
   /* Optional gather fast path: (h,w,4) {i1, traj.x, traj.y, 0} and a byte map
    * whose bit0 / bit1 say all 16 bicubic taps around (x,y) are in bounds and in
    * mask / traj_ok (filled by fsb_level_setup when non-NULL). */

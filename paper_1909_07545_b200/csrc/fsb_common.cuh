@@ -189,17 +189,19 @@ FSB_INLINE bool split_pos(double x, double y, int h, int w, int& ix, int& iy, Ac
   return true;
 }
 
-template <int C>
+template <int C, bool kGlobal = true>
 FSB_INLINE void load_tap(const float* __restrict__ f, int idx, float v[C]) {
   if constexpr (C == 1) {
-    v[0] = __ldg(f + idx);
+    v[0] = kGlobal ? __ldg(f + idx) : f[idx];
   } else {
-    float2 t = __ldg(reinterpret_cast<const float2*>(f) + idx);
+    float2 t = kGlobal ? __ldg(reinterpret_cast<const float2*>(f) + idx)
+                       : reinterpret_cast<const float2*>(f)[idx];
     v[0] = t.x; v[1] = t.y;
   }
 }
 
-template <int C, typename Acc>
+// kGlobal = false reads field and mask through generic loads (shared-memory tiles).
+template <int C, typename Acc, bool kGlobal = true>
 FSB_INLINE bool bicubic_at(const float* __restrict__ field, const uint8_t* __restrict__ mask, int h,
                            int w, int ix, int iy, Acc fx, Acc fy, Acc out[C]) {
   Acc wx[4], wy[4];
@@ -220,11 +222,12 @@ FSB_INLINE bool bicubic_at(const float* __restrict__ field, const uint8_t* __res
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int c = ix + b - 1;
-      const bool ok = rin && (unsigned)c < (unsigned)w && __ldg(mask + (size_t)r * w + c);
+      const bool ok = rin && (unsigned)c < (unsigned)w &&
+                      (kGlobal ? __ldg(mask + (size_t)r * w + c) : mask[r * w + c]);
       float vf[C];
 #pragma unroll
       for (int k = 0; k < C; ++k) vf[k] = 0.f;
-      if (ok) load_tap<C>(field, r * w + c, vf);
+      if (ok) load_tap<C, kGlobal>(field, r * w + c, vf);
       all_ok &= ok;
       any_ok |= ok;
       const Acc wt = wy[a] * wx[b];

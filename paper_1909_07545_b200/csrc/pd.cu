@@ -123,6 +123,69 @@ __global__ void __launch_bounds__(256) k_warp_sample(fsb_level L) {
   L.dir_ok[i] = dok;
 }
 
+// Fused warp prologue (solver.py:332-346 with image_derivative_along 192-202):
+// i1w / directions at x + w for the output tile plus a 3-px halo into shared
+// memory, then I_u = i1w(x + dir) - i1w(x) from that tile, and rho0.
+// One kernel, no global round trip of i1w between the two gathers.
+constexpr int kPTX = 32, kPTY = 32;               // output tile
+// halo 3 on every side: |dir| <= 1 (+1 ulp) puts the stencil base within 2 px
+constexpr int kPH = 3;
+constexpr int kPSW = kPTX + 2 * kPH, kPSH = kPTY + 2 * kPH;
+
+__global__ void __launch_bounds__(256) k_warp_prologue(fsb_level L) {
+  __shared__ float s_iw[kPSH * kPSW];
+  __shared__ uint8_t s_ok[kPSH * kPSW];
+  __shared__ float2 s_dir[kPTY * kPTX];
+  __shared__ uint8_t s_dok[kPTY * kPTX];
+  const int ox = blockIdx.x * kPTX, oy = blockIdx.y * kPTY;
+  const SampleSrc S{L.i1, L.mask, L.traj, L.traj_ok, reinterpret_cast<const float4*>(L.packed),
+                    L.full16, L.h, L.w};
+  for (int k = threadIdx.x; k < kPSH * kPSW; k += blockDim.x) {
+    const int r = k / kPSW, c = k - r * kPSW;
+    const int gx = ox - kPH + c, gy = oy - kPH + r;
+    float iw = 0.f;
+    bool iok = false;
+    if ((unsigned)gx < (unsigned)L.w && (unsigned)gy < (unsigned)L.h) {
+      const size_t gi = (size_t)gy * L.w + gx;
+      float2 d;
+      bool dok;
+      warp_sample_px(S, gx, gy, reinterpret_cast<const float2*>(L.wv)[gi], L.mask[gi] != 0, iw,
+                     iok, d, dok);
+      const int tr = r - kPH, tc = c - kPH;
+      if (tr >= 0 && tr < kPTY && tc >= 0 && tc < kPTX) {
+        s_dir[tr * kPTX + tc] = d;
+        s_dok[tr * kPTX + tc] = dok;
+        L.i1w[gi] = iw;
+        L.i1w_ok[gi] = iok;
+        reinterpret_cast<float2*>(L.dirs)[gi] = d;
+        L.dir_ok[gi] = dok;
+      }
+    }
+    s_iw[k] = iw;
+    s_ok[k] = iok;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < kPTY * kPTX; k += blockDim.x) {
+    const int tr = k / kPTX, tc = k - tr * kPTX;
+    const int gx = ox + tc, gy = oy + tr;
+    if (gx >= L.w || gy >= L.h) continue;
+    const size_t gi = (size_t)gy * L.w + gx;
+    const float2 d = s_dir[k];
+    int ix, iy;
+    float fx, fy, ahead[1];
+    bool ok = split_pos<float>((double)gx + (double)d.x, (double)gy + (double)d.y, L.h, L.w, ix,
+                               iy, fx, fy);
+    // the tile covers every tap of |d| <= 1; out-of-image taps carry ok = 0
+    if (ok) ok = bicubic_at<1, float, false>(s_iw, s_ok, kPSH, kPSW, ix - (ox - kPH),
+                                             iy - (oy - kPH), fx, fy, ahead);
+    const int si = (tr + kPH) * kPSW + (tc + kPH);
+    const float iw = s_iw[si];
+    const bool data_ok = ok && s_ok[si] && s_dok[k];
+    L.iu[gi] = data_ok ? ahead[0] - iw : 0.f;
+    L.rho0[gi] = data_ok ? iw - L.i0[gi] : 0.f;
+  }
+}
+
 // Per-level gather tables: packed {i1, traj} texels and the all-16-taps-valid
 // flags of the mask and of traj_ok.
 __global__ void k_pack_level(fsb_level L) {
@@ -265,6 +328,12 @@ int warp_linearize_internal(const fsb_level* L, cudaStream_t st) {
 int warp_sample_internal(const fsb_level* L, cudaStream_t st) {
   dim3 blk(kBX, kBY), grd = grid2d(L->w, L->h, blk);
   k_warp_sample<<<grd, blk, 0, st>>>(*L);
+  return launch_status();
+}
+
+int warp_prologue_internal(const fsb_level* L, cudaStream_t st) {
+  dim3 grd((L->w + kPTX - 1) / kPTX, (L->h + kPTY - 1) / kPTY);
+  k_warp_prologue<<<grd, 256, 0, st>>>(*L);
   return launch_status();
 }
 

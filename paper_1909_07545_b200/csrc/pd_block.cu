@@ -10,10 +10,9 @@
 // state once per `iters` iterations instead of once per iteration.
 //
 // Fused into the same launch when requested:
-//   LIN: the warp prologue (solver.py:339-346 with image_derivative_along
-//        192-202): I_u, rho0 and the u_omega / u_bar / v_bar resets;
-//   FIN: the warp epilogue (solver.py:356-360: clip, accumulate u, w) and the
-//        next warp's samples at x + w (solver.py:332-337).
+//   LIN: the warp-start resets u_omega = u, u_bar = u, v_bar = v
+//        (solver.py:344-346; I_u and rho0 come from k_warp_prologue);
+//   FIN: the warp epilogue (solver.py:356-360: clip, accumulate u and w).
 //
 // State is ping-ponged between two plane sets (src -> dst) because halos read
 // neighbours' old values while their owners write new ones.
@@ -21,7 +20,6 @@
 #include <stdlib.h>
 
 #include "pd_math.cuh"
-#include "warp_math.cuh"
 
 namespace fsb {
 
@@ -39,13 +37,9 @@ struct BlockArgs {
   float* iu; float* rho0; float* u_omega;
   float lam, alpha0, alpha1, theta, sigma_q, du_max;
   int iters;
-  // LIN: this warp's samples (written by the previous FIN or k_warp_sample)
-  const float* i0; const float* i1w; const uint8_t* i1w_ok; const float* dirs;
-  const uint8_t* dir_ok;
-  // FIN: accumulate w, then sample the next warp into the *_next buffers
-  float* wv; const float* i1; const float* traj; const uint8_t* traj_ok;
-  float* i1w_next; uint8_t* i1w_ok_next; float* dirs_next; uint8_t* dir_ok_next;
-  const float* packed; const uint8_t* full16;
+  // FIN: w += du * dirs with this warp's directions (from k_warp_prologue)
+  const float* dirs;
+  float* wv;
   // diagnostics (nullptr = off)
   float* diag_p; float* diag_q; float* diag_du; double* partials;
 };
@@ -72,21 +66,6 @@ struct Tile {
 constexpr bool kSkipRows = FSB_PD_SKIP_ROWS != 0;
 
 __device__ __forceinline__ int sidx(int r, int c, int SW) { return (r + 1) * SW + (c + 1); }
-
-// Next warp's samples at x + w (solver.py:332-337), one pixel.
-__device__ __forceinline__ void sample_next(const BlockArgs& A, int gx, int gy, size_t gi,
-                                            float2 wv, bool mk) {
-  const SampleSrc S{A.i1, A.mask, A.traj, A.traj_ok, reinterpret_cast<const float4*>(A.packed),
-                    A.full16, A.h, A.w};
-  float iw;
-  bool iok, dok;
-  float2 d;
-  warp_sample_px(S, gx, gy, wv, mk, iw, iok, d, dok);
-  A.i1w_next[gi] = iw;
-  A.i1w_ok_next[gi] = iok;
-  reinterpret_cast<float2*>(A.dirs_next)[gi] = d;
-  A.dir_ok_next[gi] = dok;
-}
 
 template <int CX, int NW, int PY, int R, bool LIN, bool FIN>
 __global__ void __launch_bounds__(NW * 32, 1) k_pd_block(const BlockArgs A) {
@@ -160,17 +139,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_block(const BlockArgs A) {
         q2[k] = A.src.q[2 * n + gi]; q3[k] = A.src.q[3 * n + gi];
         ta[k] = A.T[gi]; tb[k] = A.T[n + gi]; tc[k] = A.T[2 * n + gi];
         sp[k] = A.S[gi] * A.alpha1; tu[k] = A.S[n + gi]; tv[k] = A.S[2 * n + gi];
-        if (LIN) {
-          // I_u and rho0 of this warp (needs i1w on the +-2 neighbourhood)
-          const float2 d = reinterpret_cast<const float2*>(A.dirs)[gi];
-          float ahead[1];
-          const bool ok = bicubic_sample<1, float>(A.i1w, A.i1w_ok, A.h, A.w,
-                                                   (double)gx + (double)d.x,
-                                                   (double)gy + (double)d.y, ahead);
-          const float iw = A.i1w[gi];
-          const bool data_ok = ok && A.i1w_ok[gi] && A.dir_ok[gi];
-          g[k] = data_ok ? ahead[0] - iw : 0.f;
-          rh[k] = data_ok ? iw - A.i0[gi] : 0.f;
+        if (LIN) {  // warp start: u_omega = u, u_bar = u, v_bar = v (solver.py:344-346)
+          g[k] = A.iu[gi]; rh[k] = A.rho0[gi];
           uo[k] = u[k];
           ub = u[k]; vb0 = v0[k]; vb1 = v1[k];
         } else {
@@ -288,13 +258,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_block(const BlockArgs A) {
         reinterpret_cast<float2*>(A.wv)[gi] = wv;
         dmax = fmaxf(dmax, fabsf(du));
         dsum += (double)fabsf(du);
-        if (A.i1w_next) sample_next(A, gx, gy, gi, wv, mk);
       }
-      if (LIN) {
-        A.iu[gi] = g[k];
-        A.rho0[gi] = rh[k];
-        A.u_omega[gi] = uo[k];
-      }
+      if (LIN) A.u_omega[gi] = uo[k];
       A.dst.u[gi] = uu;
       A.dst.ub[gi] = ub;
       A.dst.v[gi] = v0[k]; A.dst.v[n + gi] = v1[k];

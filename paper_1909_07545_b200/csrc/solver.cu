@@ -40,6 +40,7 @@ int warp_finish_internal(const fsb_level* L, const fsb_params* prm, float* dmax,
 size_t level_partials_internal(int h, int w);
 int warp_sample_internal(const fsb_level* L, cudaStream_t st);
 int pack_level_internal(const fsb_level* L, cudaStream_t st);
+int warp_prologue_internal(const fsb_level* L, cudaStream_t st);
 int mean_finish_internal(const double* partials, int nparts, const uint8_t* mask, size_t n,
                          double* out, cudaStream_t st);
 struct StateSet {
@@ -55,11 +56,8 @@ struct BlockArgs {
   float* iu; float* rho0; float* u_omega;
   float lam, alpha0, alpha1, theta, sigma_q, du_max;
   int iters;
-  const float* i0; const float* i1w; const uint8_t* i1w_ok; const float* dirs;
-  const uint8_t* dir_ok;
-  float* wv; const float* i1; const float* traj; const uint8_t* traj_ok;
-  float* i1w_next; uint8_t* i1w_ok_next; float* dirs_next; uint8_t* dir_ok_next;
-  const float* packed; const uint8_t* full16;
+  const float* dirs;
+  float* wv;
   float* diag_p; float* diag_q; float* diag_du; double* partials;
 };
 int pd_block_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st,
@@ -120,8 +118,7 @@ struct LevelState {  // state buffers sized for the finest level, reused per lev
   float *u_bar, *v, *v_bar, *p, *q, *T, *S, *u_omega, *iu, *rho0, *i1w, *dirs;
   uint8_t *i1w_ok, *dir_ok;
   double* partials;
-  float *state_b, *i1w_b, *dirs_b;
-  uint8_t *i1w_ok_b, *dir_ok_b;
+  float* state_b;
   float* packed;
   uint8_t* full16;
 };
@@ -190,10 +187,6 @@ int make_plan(const fsb_rig* rig, const fsb_params* prm, void* base, Plan& P) {
   s.dir_ok = c.take<uint8_t>(n0);
   s.partials = c.take<double>(level_partials_internal(H, W) + 64);
   s.state_b = c.take<float>(12 * n0);
-  s.i1w_b = c.take<float>(n0);
-  s.dirs_b = c.take<float>(2 * n0);
-  s.i1w_ok_b = c.take<uint8_t>(n0);
-  s.dir_ok_b = c.take<uint8_t>(n0);
   s.packed = c.take<float>(4 * n0);
   s.full16 = c.take<uint8_t>(n0);
   P.bytes = c.off;
@@ -225,17 +218,6 @@ int pd_halo(int K) {
   return h;
 }
 
-// Sample the next warp inside the fused epilogue (1) or in a separate
-// full-occupancy kernel after it (0). FSB_FUSED_SAMPLE overrides.
-bool fused_sample() {
-  static int env = -1;
-  if (env < 0) {
-    const char* e = getenv("FSB_FUSED_SAMPLE");
-    env = e ? atoi(e) : 0;
-  }
-  return env != 0;
-}
-
 StateSet set_a(const fsb_level* L) {
   return StateSet{L->u, L->u_bar, L->v, L->v_bar, L->p, L->q};
 }
@@ -262,14 +244,8 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
   const size_t n = (size_t)L->h * L->w;
   const int N = prm->warp_iters, K = prm->pd_iters;
   const int halo = pd_halo(K);
-  int rc = warp_sample_internal(L, st);  // samples of warp 0 into buffer 0
-  if (rc) return rc;
   StateSet sets[2] = {set_a(L), set_b(L)};
-  float* i1w[2] = {L->i1w, L->i1w_b};
-  uint8_t* i1w_ok[2] = {L->i1w_ok, L->i1w_ok_b};
-  float* dirs[2] = {L->dirs, L->dirs_b};
-  uint8_t* dir_ok[2] = {L->dir_ok, L->dir_ok_b};
-  int cur = 0, wb = 0;
+  int cur = 0;
   BlockArgs A;
   memset(&A, 0, sizeof(A));
   A.h = L->h; A.w = L->w; A.n = n;
@@ -278,17 +254,14 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
   A.lam = (float)prm->lam; A.alpha0 = (float)prm->alpha0; A.alpha1 = (float)prm->alpha1;
   A.theta = (float)prm->theta; A.sigma_q = (float)(1.0 / (2.0 * prm->alpha0));
   A.du_max = (float)prm->du_max;
-  A.i0 = L->i0; A.wv = L->wv; A.i1 = L->i1; A.traj = L->traj; A.traj_ok = L->traj_ok;
-  A.packed = L->packed; A.full16 = L->full16;
+  A.wv = L->wv; A.dirs = L->dirs;
   A.partials = L->partials;
   const bool dpq = diag && diag->max_p_norm && diag->max_q_norm;
   const bool ddu = diag && diag->max_du && diag->mean_abs_du;
+  int rc = FSB_OK;
   for (int wi = 0; wi < N; ++wi) {
-    A.i1w = i1w[wb]; A.i1w_ok = i1w_ok[wb]; A.dirs = dirs[wb]; A.dir_ok = dir_ok[wb];
-    const bool last_warp = wi == N - 1;
-    const bool fused = fused_sample();
-    A.i1w_next = (last_warp || !fused) ? nullptr : i1w[wb ^ 1];
-    A.i1w_ok_next = i1w_ok[wb ^ 1]; A.dirs_next = dirs[wb ^ 1]; A.dir_ok_next = dir_ok[wb ^ 1];
+    rc = warp_prologue_internal(L, st);  // samples at x + w, I_u, rho0 (solver.py:332-343)
+    if (rc) return rc;
     int done = 0, nblocks = 0;
     while (done < K) {
       const int it = K - done < halo ? K - done : halo;
@@ -303,27 +276,13 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
       cur ^= 1;
       done += it;
     }
-    if (!fused && !last_warp) {  // next warp's samples at the updated w
-      fsb_level Ln = *L;
-      Ln.i1w = i1w[wb ^ 1]; Ln.i1w_ok = i1w_ok[wb ^ 1];
-      Ln.dirs = dirs[wb ^ 1]; Ln.dir_ok = dir_ok[wb ^ 1];
-      rc = warp_sample_internal(&Ln, st);
-      if (rc) return rc;
-    }
     if (ddu) {
       rc = mean_finish_internal(L->partials, nblocks, L->mask, n,
                                 diag->mean_abs_du + warp_off + wi, st);
       if (rc) return rc;
     }
-    wb ^= 1;
   }
   if (cur != 0) copy_set(sets[0], sets[1], n, st);
-  if (wb != 0) {  // leave the last samples in the primary buffers (per-stage API contract)
-    cudaMemcpyAsync(L->dirs, L->dirs_b, 2 * n * sizeof(float), cudaMemcpyDeviceToDevice, st);
-    cudaMemcpyAsync(L->dir_ok, L->dir_ok_b, n, cudaMemcpyDeviceToDevice, st);
-    cudaMemcpyAsync(L->i1w, L->i1w_b, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
-    cudaMemcpyAsync(L->i1w_ok, L->i1w_ok_b, n, cudaMemcpyDeviceToDevice, st);
-  }
   return launch_status();
 }
 
@@ -381,7 +340,7 @@ int solve_level_internal(const fsb_level* L, const fsb_params* prm, const fsb_di
   cudaMemsetAsync(L->p, 0, 2 * n * sizeof(float), st);
   cudaMemsetAsync(L->q, 0, 4 * n * sizeof(float), st);
   cudaMemcpyAsync(L->u_bar, L->u, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
-  if (L->state_b && L->i1w_b && L->i1w_ok_b && L->dirs_b && L->dir_ok_b)
+  if (L->state_b)
     return warp_loop_blocked(L, prm, diag, pd_off, warp_off, st);
   const int N = prm->warp_iters, K = prm->pd_iters;
   for (int wi = 0; wi < N; ++wi) {
@@ -495,8 +454,7 @@ int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const floa
     L.u = u; L.u_bar = S.u_bar; L.v = S.v; L.v_bar = S.v_bar; L.p = S.p; L.q = S.q;
     L.wv = wv; L.u_omega = S.u_omega; L.iu = S.iu; L.rho0 = S.rho0; L.i1w = S.i1w;
     L.i1w_ok = S.i1w_ok; L.dirs = S.dirs; L.dir_ok = S.dir_ok; L.partials = S.partials;
-    L.state_b = S.state_b; L.i1w_b = S.i1w_b; L.i1w_ok_b = S.i1w_ok_b; L.dirs_b = S.dirs_b;
-    L.dir_ok_b = S.dir_ok_b;
+    L.state_b = S.state_b;
     L.packed = S.packed; L.full16 = S.full16;
     rc = solve_level_internal(&L, prm, diag, pd_off, warp_off, P.setup_scratch,
                               P.setup_scratch_bytes, st);

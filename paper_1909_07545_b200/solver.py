@@ -133,12 +133,8 @@ class _Level:
         self.iu = E((h, w)); self.rho0 = E((h, w)); self.i1w = E((h, w))
         self.i1w_ok = E((h, w), U8); self.dirs = E((h, w, 2)); self.dir_ok = E((h, w), U8)
         self.partials = E((int(_ext.lib().fsb_level_partials(h, w)),), torch.float64)
-        # second state / sample set -> temporally blocked PD kernel (K6)
+        # second state set (ping-pong) -> temporally blocked PD kernel (K6)
         self.state_b = E((12, h, w)) if blocked else None
-        self.i1w_b = E((h, w)) if blocked else None
-        self.i1w_ok_b = E((h, w), U8) if blocked else None
-        self.dirs_b = E((h, w, 2)) if blocked else None
-        self.dir_ok_b = E((h, w), U8) if blocked else None
         self.packed = E((h, w, 4)) if blocked else None
         self.full16 = E((h, w), U8) if blocked else None
 
