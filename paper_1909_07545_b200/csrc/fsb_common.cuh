@@ -201,64 +201,87 @@ FSB_INLINE void load_tap(const float* __restrict__ f, int idx, float v[C]) {
 }
 
 // kGlobal = false reads field and mask through generic loads (shared-memory tiles).
+// The 16 tap validities are gathered first (bit 4a+b, scan order dy outer / dx
+// inner); the all-valid case is a plain Catmull-Rom sum, the fallbacks visit only
+// valid taps — identical sums to the reference, whose invalid taps add exact zeros.
 template <int C, typename Acc, bool kGlobal = true>
 FSB_INLINE bool bicubic_at(const float* __restrict__ field, const uint8_t* __restrict__ mask, int h,
                            int w, int ix, int iy, Acc fx, Acc fy, Acc out[C]) {
-  Acc wx[4], wy[4];
-  cubic_weights(fx, wx);
-  cubic_weights(fy, wy);
-  Acc cub[C], bil[C], near[C];
+  unsigned okb = 0;
+  const bool inner = ix >= 1 && ix + 2 < w && iy >= 1 && iy + 2 < h;
 #pragma unroll
-  for (int k = 0; k < C; ++k) { cub[k] = Acc(0); bil[k] = Acc(0); near[k] = Acc(0); }
-  Acc bws = Acc(0);
-  Acc nd2 = Acc(INFINITY);
-  bool all_ok = true, any_ok = false;
-  const Acc bx[2] = {Acc(1) - fx, fx};
-  const Acc by[2] = {Acc(1) - fy, fy};
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int r = iy + a - 1;
-    const bool rin = (unsigned)r < (unsigned)h;
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int c = ix + b - 1;
-      const bool ok = rin && (unsigned)c < (unsigned)w &&
-                      (kGlobal ? __ldg(mask + (size_t)r * w + c) : mask[r * w + c]);
-      float vf[C];
+      const int r = iy + a - 1, c = ix + b - 1;
+      const bool in = inner || ((unsigned)r < (unsigned)h && (unsigned)c < (unsigned)w);
+      const int idx = r * w + c;
+      const bool v = in && (kGlobal ? __ldg(mask + idx) : mask[idx]);
+      okb |= (v ? 1u : 0u) << (4 * a + b);
+    }
+  if (okb == 0) return false;
+  if (okb == 0xFFFFu) {
+    Acc wx[4], wy[4];
+    cubic_weights(fx, wx);
+    cubic_weights(fy, wy);
+    Acc cub[C];
 #pragma unroll
-      for (int k = 0; k < C; ++k) vf[k] = 0.f;
-      if (ok) load_tap<C, kGlobal>(field, r * w + c, vf);
-      all_ok &= ok;
-      any_ok |= ok;
-      const Acc wt = wy[a] * wx[b];
+    for (int k = 0; k < C; ++k) cub[k] = Acc(0);
 #pragma unroll
-      for (int k = 0; k < C; ++k) cub[k] += wt * (Acc)vf[k];
-      if (a >= 1 && a <= 2 && b >= 1 && b <= 2) {
-        const Acc bw = ok ? by[a - 1] * bx[b - 1] : Acc(0);
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        float vf[C];
+        load_tap<C, kGlobal>(field, (iy + a - 1) * w + (ix + b - 1), vf);
+        const Acc wt = wy[a] * wx[b];
+#pragma unroll
+        for (int k = 0; k < C; ++k) cub[k] += wt * (Acc)vf[k];
+      }
+#pragma unroll
+    for (int k = 0; k < C; ++k) out[k] = cub[k];
+    return true;
+  }
+  // bilinear over the valid inner 2x2, renormalised
+  const Acc bx[2] = {Acc(1) - fx, fx};
+  const Acc by[2] = {Acc(1) - fy, fy};
+  Acc bil[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) bil[k] = Acc(0);
+  Acc bws = Acc(0);
+#pragma unroll
+  for (int a = 1; a <= 2; ++a)
+#pragma unroll
+    for (int b = 1; b <= 2; ++b)
+      if (okb >> (4 * a + b) & 1u) {
+        float vf[C];
+        load_tap<C, kGlobal>(field, (iy + a - 1) * w + (ix + b - 1), vf);
+        const Acc bw = by[a - 1] * bx[b - 1];
 #pragma unroll
         for (int k = 0; k < C; ++k) bil[k] += bw * (Acc)vf[k];
         bws += bw;
       }
-      const Acc ddx = Acc(b - 1) - fx, ddy = Acc(a - 1) - fy;
-      const Acc d2 = ddx * ddx + ddy * ddy;
-      if (ok && d2 < nd2) {
-        nd2 = d2;
-#pragma unroll
-        for (int k = 0; k < C; ++k) near[k] = (Acc)vf[k];
-      }
-    }
-  }
-  if (all_ok) {
-#pragma unroll
-    for (int k = 0; k < C; ++k) out[k] = cub[k];
-  } else if (bws > Acc(1e-12)) {
+  if (bws > Acc(1e-12)) {
 #pragma unroll
     for (int k = 0; k < C; ++k) out[k] = bil[k] / bws;
-  } else {
-#pragma unroll
-    for (int k = 0; k < C; ++k) out[k] = near[k];
+    return true;
   }
-  return any_ok;
+  // nearest valid tap, strict '<' in scan order
+  Acc nd2 = Acc(INFINITY);
+  int best = 0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (okb >> (4 * a + b) & 1u) {
+        const Acc ddx = Acc(b - 1) - fx, ddy = Acc(a - 1) - fy;
+        const Acc d2 = ddx * ddx + ddy * ddy;
+        if (d2 < nd2) { nd2 = d2; best = 4 * a + b; }
+      }
+  float vf[C];
+  load_tap<C, kGlobal>(field, (iy + (best >> 2) - 1) * w + (ix + (best & 3) - 1), vf);
+#pragma unroll
+  for (int k = 0; k < C; ++k) out[k] = (Acc)vf[k];
+  return true;
 }
 
 // Full sample at a continuous position: returns validity, out untouched when
