@@ -200,25 +200,11 @@ FSB_INLINE void load_tap(const float* __restrict__ f, int idx, float v[C]) {
   }
 }
 
-// kGlobal = false reads field and mask through generic loads (shared-memory tiles).
-// The 16 tap validities are gathered first (bit 4a+b, scan order dy outer / dx
-// inner); the all-valid case is a plain Catmull-Rom sum, the fallbacks visit only
-// valid taps — identical sums to the reference, whose invalid taps add exact zeros.
+// Evaluation given the 16 tap validities `okb` (bit 4a+b, a = dy+1 outer, b = dx+1
+// inner); taps are read only where valid. Returns false when no tap is valid.
 template <int C, typename Acc, bool kGlobal = true>
-FSB_INLINE bool bicubic_at(const float* __restrict__ field, const uint8_t* __restrict__ mask, int h,
-                           int w, int ix, int iy, Acc fx, Acc fy, Acc out[C]) {
-  unsigned okb = 0;
-  const bool inner = ix >= 1 && ix + 2 < w && iy >= 1 && iy + 2 < h;
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int r = iy + a - 1, c = ix + b - 1;
-      const bool in = inner || ((unsigned)r < (unsigned)h && (unsigned)c < (unsigned)w);
-      const int idx = r * w + c;
-      const bool v = in && (kGlobal ? __ldg(mask + idx) : mask[idx]);
-      okb |= (v ? 1u : 0u) << (4 * a + b);
-    }
+FSB_INLINE bool bicubic_bits(const float* __restrict__ field, unsigned okb, int w, int ix, int iy,
+                             Acc fx, Acc fy, Acc out[C]) {
   if (okb == 0) return false;
   if (okb == 0xFFFFu) {
     Acc wx[4], wy[4];
@@ -282,6 +268,28 @@ FSB_INLINE bool bicubic_at(const float* __restrict__ field, const uint8_t* __res
 #pragma unroll
   for (int k = 0; k < C; ++k) out[k] = (Acc)vf[k];
   return true;
+}
+
+// kGlobal = false reads field and mask through generic loads (shared-memory tiles).
+// The 16 tap validities are gathered first (bit 4a+b, scan order dy outer / dx
+// inner); the all-valid case is a plain Catmull-Rom sum, the fallbacks visit only
+// valid taps — identical sums to the reference, whose invalid taps add exact zeros.
+template <int C, typename Acc, bool kGlobal = true>
+FSB_INLINE bool bicubic_at(const float* __restrict__ field, const uint8_t* __restrict__ mask, int h,
+                           int w, int ix, int iy, Acc fx, Acc fy, Acc out[C]) {
+  unsigned okb = 0;
+  const bool inner = ix >= 1 && ix + 2 < w && iy >= 1 && iy + 2 < h;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = iy + a - 1, c = ix + b - 1;
+      const bool in = inner || ((unsigned)r < (unsigned)h && (unsigned)c < (unsigned)w);
+      const int idx = r * w + c;
+      const bool v = in && (kGlobal ? __ldg(mask + idx) : mask[idx]);
+      okb |= (v ? 1u : 0u) << (4 * a + b);
+    }
+  return bicubic_bits<C, Acc, kGlobal>(field, okb, w, ix, iy, fx, fy, out);
 }
 
 // Full sample at a continuous position: returns validity, out untouched when

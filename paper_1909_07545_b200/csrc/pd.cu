@@ -125,36 +125,39 @@ __global__ void __launch_bounds__(256) k_warp_sample(fsb_level L) {
 
 // Fused warp prologue (solver.py:332-346 with image_derivative_along 192-202):
 // i1w / directions at x + w for the output tile plus a 3-px halo into shared
-// memory, then I_u = i1w(x + dir) - i1w(x) from that tile, and rho0.
-// One kernel, no global round trip of i1w between the two gathers.
-constexpr int kPTX = 32, kPTY = 32;               // output tile
-// halo 3 on every side: |dir| <= 1 (+1 ulp) puts the stencil base within 2 px
-constexpr int kPH = 3;
-constexpr int kPSW = kPTX + 2 * kPH, kPSH = kPTY + 2 * kPH;
-
+// memory, then I_u = i1w(x + dir) - i1w(x) from that tile, and rho0. One
+// kernel, no global round trip of i1w between the two gathers. Pixels outside
+// the level mask are skipped: their i1w_ok / dir_ok are false by definition
+// (solver.py:336, 339), so nothing downstream reads their samples.
+template <int TX, int TY>
 __global__ void __launch_bounds__(256) k_warp_prologue(fsb_level L) {
-  __shared__ float s_iw[kPSH * kPSW];
-  __shared__ uint8_t s_ok[kPSH * kPSW];
-  __shared__ float2 s_dir[kPTY * kPTX];
-  __shared__ uint8_t s_dok[kPTY * kPTX];
-  const int ox = blockIdx.x * kPTX, oy = blockIdx.y * kPTY;
+  constexpr int H = 3;  // |dir| <= 1 (+1 ulp) puts the stencil base within 2 px
+  constexpr int SW = TX + 2 * H, SH = TY + 2 * H;
+  static_assert(SW <= 64, "row validity words are 64-bit");
+  __shared__ float s_iw[SH * SW];
+  __shared__ unsigned long long s_okrow[SH];  // bit c of row r: i1w_ok of tile pixel (r, c)
+  __shared__ float2 s_dir[TY * TX];
+  __shared__ uint8_t s_dok[TY * TX];
+  const int ox = blockIdx.x * TX, oy = blockIdx.y * TY;
   const SampleSrc S{L.i1, L.mask, L.traj, L.traj_ok, reinterpret_cast<const float4*>(L.packed),
                     L.full16, L.h, L.w};
-  for (int k = threadIdx.x; k < kPSH * kPSW; k += blockDim.x) {
-    const int r = k / kPSW, c = k - r * kPSW;
-    const int gx = ox - kPH + c, gy = oy - kPH + r;
+  for (int k = threadIdx.x; k < SH; k += blockDim.x) s_okrow[k] = 0ull;
+  __syncthreads();
+  for (int k = threadIdx.x; k < SH * SW; k += blockDim.x) {
+    const int r = k / SW, c = k - r * SW;
+    const int gx = ox - H + c, gy = oy - H + r;
     float iw = 0.f;
-    bool iok = false;
+    bool iok = false, dok = false;
+    float2 d = make_float2(0.f, 0.f);
     if ((unsigned)gx < (unsigned)L.w && (unsigned)gy < (unsigned)L.h) {
       const size_t gi = (size_t)gy * L.w + gx;
-      float2 d;
-      bool dok;
-      warp_sample_px(S, gx, gy, reinterpret_cast<const float2*>(L.wv)[gi], L.mask[gi] != 0, iw,
-                     iok, d, dok);
-      const int tr = r - kPH, tc = c - kPH;
-      if (tr >= 0 && tr < kPTY && tc >= 0 && tc < kPTX) {
-        s_dir[tr * kPTX + tc] = d;
-        s_dok[tr * kPTX + tc] = dok;
+      if (L.mask[gi])
+        warp_sample_px(S, gx, gy, reinterpret_cast<const float2*>(L.wv)[gi], true, iw, iok, d,
+                       dok);
+      const int tr = r - H, tc = c - H;
+      if (tr >= 0 && tr < TY && tc >= 0 && tc < TX) {
+        s_dir[tr * TX + tc] = d;
+        s_dok[tr * TX + tc] = dok;
         L.i1w[gi] = iw;
         L.i1w_ok[gi] = iok;
         reinterpret_cast<float2*>(L.dirs)[gi] = d;
@@ -162,27 +165,38 @@ __global__ void __launch_bounds__(256) k_warp_prologue(fsb_level L) {
       }
     }
     s_iw[k] = iw;
-    s_ok[k] = iok;
+    if (iok) atomicOr(&s_okrow[r], 1ull << c);
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < kPTY * kPTX; k += blockDim.x) {
-    const int tr = k / kPTX, tc = k - tr * kPTX;
+  for (int k = threadIdx.x; k < TY * TX; k += blockDim.x) {
+    const int tr = k / TX, tc = k - tr * TX;
     const int gx = ox + tc, gy = oy + tr;
     if (gx >= L.w || gy >= L.h) continue;
     const size_t gi = (size_t)gy * L.w + gx;
-    const float2 d = s_dir[k];
-    int ix, iy;
-    float fx, fy, ahead[1];
-    bool ok = split_pos<float>((double)gx + (double)d.x, (double)gy + (double)d.y, L.h, L.w, ix,
-                               iy, fx, fy);
-    // the tile covers every tap of |d| <= 1; out-of-image taps carry ok = 0
-    if (ok) ok = bicubic_at<1, float, false>(s_iw, s_ok, kPSH, kPSW, ix - (ox - kPH),
-                                             iy - (oy - kPH), fx, fy, ahead);
-    const int si = (tr + kPH) * kPSW + (tc + kPH);
-    const float iw = s_iw[si];
-    const bool data_ok = ok && s_ok[si] && s_dok[k];
-    L.iu[gi] = data_ok ? ahead[0] - iw : 0.f;
-    L.rho0[gi] = data_ok ? iw - L.i0[gi] : 0.f;
+    const int si = (tr + H) * SW + (tc + H);
+    const bool own_ok = (s_okrow[tr + H] >> (tc + H)) & 1ull;
+    float iu = 0.f, rho0 = 0.f;
+    if (own_ok && s_dok[k]) {
+      const float2 d = s_dir[k];
+      int ix, iy;
+      float fx, fy;
+      if (split_pos<float>((double)gx + (double)d.x, (double)gy + (double)d.y, L.h, L.w, ix, iy,
+                           fx, fy)) {
+        const int lx = ix - (ox - H), ly = iy - (oy - H);  // tile-local stencil base
+        unsigned okb = 0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+          okb |= (unsigned)((s_okrow[ly + a - 1] >> (lx - 1)) & 0xFull) << (4 * a);
+        float ahead;
+        if (okb && bicubic_bits<1, float, false>(s_iw, okb, SW, lx, ly, fx, fy, &ahead)) {
+          const float iw = s_iw[si];
+          iu = ahead - iw;
+          rho0 = iw - L.i0[gi];
+        }
+      }
+    }
+    L.iu[gi] = iu;
+    L.rho0[gi] = rho0;
   }
 }
 
@@ -332,8 +346,14 @@ int warp_sample_internal(const fsb_level* L, cudaStream_t st) {
 }
 
 int warp_prologue_internal(const fsb_level* L, cudaStream_t st) {
-  dim3 grd((L->w + kPTX - 1) / kPTX, (L->h + kPTY - 1) / kPTY);
-  k_warp_prologue<<<grd, 256, 0, st>>>(*L);
+  // small levels: 16 x 16 tiles so the grid still spreads over the SMs
+  if ((size_t)L->w * L->h >= (size_t)512 * 512) {
+    dim3 grd((L->w + 31) / 32, (L->h + 31) / 32);
+    k_warp_prologue<32, 32><<<grd, 256, 0, st>>>(*L);
+  } else {
+    dim3 grd((L->w + 15) / 16, (L->h + 15) / 16);
+    k_warp_prologue<16, 16><<<grd, 256, 0, st>>>(*L);
+  }
   return launch_status();
 }
 
