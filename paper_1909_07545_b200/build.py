@@ -31,6 +31,7 @@ UNITS = [
     ("setup.cu", ["-fmad=false"]),
     ("pd.cu", []),
     ("pd_block.cu", []),
+    ("pd_pair.cu", []),
     ("solver.cu", []),
     ("synth.cu", ["-fmad=false"]),
 ]

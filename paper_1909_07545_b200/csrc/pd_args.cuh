@@ -1,0 +1,37 @@
+// Launch arguments of the temporally blocked primal-dual kernels
+// (pd_block.cu per-pixel tiles, pd_pair.cu packed pixel pairs) and the driver.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace fsb {
+
+struct StateSet {   // plane stride n: v, vb, p hold 2 planes, q holds 4
+  float* u; float* ub; float* v; float* vb; float* p; float* q;
+};
+
+struct BlockArgs {
+  int h, w;
+  size_t n;
+  StateSet src, dst;
+  const uint8_t* mask;
+  const float* T;   // a, b, c planes
+  const float* S;   // sigma_p, tau_u, tau_v planes
+  float* iu; float* rho0; float* u_omega;
+  float lam, alpha0, alpha1, theta, sigma_q, du_max;
+  int iters;
+  // FIN: w += du * dirs with this warp's directions (from k_warp_prologue)
+  const float* dirs;
+  float* wv;
+  // diagnostics (nullptr = off)
+  float* diag_p; float* diag_q; float* diag_du; double* partials;
+};
+
+int pd_block_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st,
+                    int* nblocks);
+int pd_pair_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st,
+                   int* nblocks);
+
+}  // namespace fsb

@@ -19,30 +19,12 @@
 
 #include <stdlib.h>
 
+#include "pd_args.cuh"
 #include "pd_math.cuh"
 
 namespace fsb {
 
-struct StateSet {   // plane stride n: v, vb, p hold 2 planes, q holds 4
-  float* u; float* ub; float* v; float* vb; float* p; float* q;
-};
 
-struct BlockArgs {
-  int h, w;
-  size_t n;
-  StateSet src, dst;
-  const uint8_t* mask;
-  const float* T;   // a, b, c planes
-  const float* S;   // sigma_p, tau_u, tau_v planes
-  float* iu; float* rho0; float* u_omega;
-  float lam, alpha0, alpha1, theta, sigma_q, du_max;
-  int iters;
-  // FIN: w += du * dirs with this warp's directions (from k_warp_prologue)
-  const float* dirs;
-  float* wv;
-  // diagnostics (nullptr = off)
-  float* diag_p; float* diag_q; float* diag_du; double* partials;
-};
 
 namespace {
 

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "fsb_common.cuh"
+#include "pd_args.cuh"
 
 namespace fsb {
 
@@ -43,25 +44,7 @@ int pack_level_internal(const fsb_level* L, cudaStream_t st);
 int warp_prologue_internal(const fsb_level* L, cudaStream_t st);
 int mean_finish_internal(const double* partials, int nparts, const uint8_t* mask, size_t n,
                          double* out, cudaStream_t st);
-struct StateSet {
-  float* u; float* ub; float* v; float* vb; float* p; float* q;
-};
-struct BlockArgs {
-  int h, w;
-  size_t n;
-  StateSet src, dst;
-  const uint8_t* mask;
-  const float* T;
-  const float* S;
-  float* iu; float* rho0; float* u_omega;
-  float lam, alpha0, alpha1, theta, sigma_q, du_max;
-  int iters;
-  const float* dirs;
-  float* wv;
-  float* diag_p; float* diag_q; float* diag_du; double* partials;
-};
-int pd_block_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st,
-                    int* nblocks);
+
 
 namespace {
 
@@ -218,6 +201,17 @@ int pd_halo(int K) {
   return h;
 }
 
+// Blocked PD kernel: packed pixel pairs (default) or the per-pixel tile kernel.
+int pd_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st, int* nblocks) {
+  static int which = -1;
+  if (which < 0) {
+    const char* e = getenv("FSB_PD_KERNEL");
+    which = (e && strcmp(e, "block") == 0) ? 1 : 0;
+  }
+  return which ? pd_block_launch(A, halo, lin, fin, st, nblocks)
+               : pd_pair_launch(A, halo, lin, fin, st, nblocks);
+}
+
 StateSet set_a(const fsb_level* L) {
   return StateSet{L->u, L->u_bar, L->v, L->v_bar, L->p, L->q};
 }
@@ -271,7 +265,7 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
       A.diag_p = dpq ? diag->max_p_norm + pd_off + (int64_t)wi * K + done : nullptr;
       A.diag_q = dpq ? diag->max_q_norm + pd_off + (int64_t)wi * K + done : nullptr;
       A.diag_du = (fin && ddu) ? diag->max_du + warp_off + wi : nullptr;
-      rc = pd_block_launch(A, halo, lin, fin, st, &nblocks);
+      rc = pd_launch(A, halo, lin, fin, st, &nblocks);
       if (rc) return rc;
       cur ^= 1;
       done += it;
@@ -317,7 +311,7 @@ int pd_iterate_blocked(const fsb_level* L, const fsb_params* prm, int iters, flo
     A.iters = it;
     A.diag_p = (dp && dq) ? dp + done : nullptr;
     A.diag_q = (dp && dq) ? dq + done : nullptr;
-    int rc = pd_block_launch(A, halo, false, false, st, nullptr);
+    int rc = pd_launch(A, halo, false, false, st, nullptr);
     if (rc) return rc;
     cur ^= 1;
     done += it;
