@@ -32,13 +32,30 @@ typedef float2 f2;
 FSB_INLINE f2 mk2(float a, float b) { return make_float2(a, b); }
 FSB_INLINE f2 add2(f2 a, f2 b) { return __fadd2_rn(a, b); }
 FSB_INLINE f2 sub2(f2 a, f2 b) { return __fadd2_rn(a, mk2(-b.x, -b.y)); }
+FSB_INLINE f2 neg2(f2 a) { return mk2(-a.x, -a.y); }
 FSB_INLINE f2 mul2(f2 a, f2 b) { return __fmul2_rn(a, b); }
 FSB_INLINE f2 fma2(f2 a, f2 b, f2 c) { return __ffma2_rn(a, b, c); }
-FSB_INLINE f2 sel2(bool cx, bool cy, f2 a) { return mk2(cx ? a.x : 0.f, cy ? a.y : 0.f); }
+// edge masks are kept as 0/1 floats: x * 1 == x exactly, x * 0 == +-0 (finite x),
+// one FMUL2 per pixel pair instead of two selects on predicate bits
+FSB_INLINE f2 sub2(f2 a, f2 b);
 
 // x / max(1, |x|) on two pixels at once (see dual_update in pd_math.cuh)
 FSB_INLINE f2 unit_scale2(f2 n2) {
   return mk2(n2.x > 1.f ? rsqrtf(n2.x) : 1.f, n2.y > 1.f ? rsqrtf(n2.y) : 1.f);
+}
+
+// thresholding_step (solver.py:205-218) on two pixels, branch-free;
+// tl = tau_u * lam. The interior case divides with the approximate reciprocal
+// (<= 2 ulp, fp32 path); iu == 0 passes through exactly.
+FSB_INLINE float shrink1(float uh, float rh, float g, float tl) {
+  const float a = tl * g;
+  const float th = a * g;
+  const float q = g != 0.f ? __fdividef(rh, g) : 0.f;
+  const float step = rh < -th ? a : (rh > th ? -a : -q);
+  return g != 0.f ? uh + step : uh;
+}
+FSB_INLINE f2 shrink2(f2 uh, f2 rh, f2 g, f2 tl) {
+  return mk2(shrink1(uh.x, rh.x, g.x, tl.x), shrink1(uh.y, rh.y, g.y, tl.y));
 }
 
 template <int NW, int PY, int R>
@@ -49,7 +66,7 @@ struct PairTile {
   static_assert(6 * PY <= 32, "mask bits");
 };
 
-template <int NW, int PY, int R, bool LIN, bool FIN>
+template <int NW, int PY, int R, bool LIN, bool FIN, bool DIAG>
 __global__ void __launch_bounds__(NW * 32, 1) k_pd_pair(const BlockArgs A) {
   using TL = PairTile<NW, PY, R>;
   constexpr int EH = TL::EH;
@@ -76,6 +93,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_pair(const BlockArgs A) {
   f2 u[PY], v0[PY], v1[PY], p0[PY], p1[PY], q0[PY], q1[PY], q2[PY], q3[PY];
   f2 ub[PY], vb0[PY], vb1[PY];
   f2 ta[PY], tb[PY], tc[PY], sp[PY], tu[PY], tv[PY], g[PY], rh[PY], uo[PY];
+  f2 exf[PY], eyf[PY];  // forward-edge indicators as 0/1 floats
   unsigned bits = 0;  // per row j: m.x m.y ex.x ex.y ey.x ey.y at bit 6j
   const float a1 = A.alpha1;
 
@@ -88,6 +106,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_pair(const BlockArgs A) {
     b |= (s_m[r][c0] && s_m[r][c0 + 1] ? 4u : 0u) | (s_m[r][c0 + 1] && s_m[r][c0 + 2] ? 8u : 0u);
     b |= (s_m[r][c0] && s_m[r + 1][c0] ? 16u : 0u) | (s_m[r][c0 + 1] && s_m[r + 1][c0 + 1] ? 32u : 0u);
     bits |= b << (6 * j);
+    exf[j] = mk2(b & 4u ? 1.f : 0.f, b & 8u ? 1.f : 0.f);
+    eyf[j] = mk2(b & 16u ? 1.f : 0.f, b & 32u ? 1.f : 0.f);
     float lu[2], lv0[2], lv1[2], lp0[2], lp1[2], lq0[2], lq1[2], lq2[2], lq3[2], lub[2], lvb0[2],
         lvb1[2], la[2], lb[2], lc[2], lsp[2], ltu[2], ltv[2], lg[2], lrh[2], luo[2];
 #pragma unroll
@@ -131,6 +151,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_pair(const BlockArgs A) {
   const f2 al0 = mk2(A.alpha0, A.alpha0), al1 = mk2(a1, a1), th2 = mk2(A.theta, A.theta);
   const f2 ta1 = al1;  // tau_u * alpha1 uses alpha1
   const f2 zero = mk2(0.f, 0.f);
+  const f2 lam2 = mk2(A.lam, A.lam);
 
   for (int it = 1; it <= A.iters; ++it) {
     // publish this strip's first row of u_bar / v_bar for the strip above
@@ -143,13 +164,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_pair(const BlockArgs A) {
     f2 fpx[PY], fpy[PY], fq0x[PY], fq0y[PY], fq1x[PY], fq1y[PY];
 #pragma unroll
     for (int j = 0; j < PY; ++j) {
-      const unsigned b = bits >> (6 * j);
-      const bool exx = b & 4u, exy = b & 8u, eyx = b & 16u, eyy = b & 32u;
-      // right neighbours: own .y for .x, next lane's .x for .y (pad 0 past the tile)
-      float nub = __shfl_down_sync(FULL, ub[j].x, 1);
-      float nvb0 = __shfl_down_sync(FULL, vb0[j].x, 1);
-      float nvb1 = __shfl_down_sync(FULL, vb1[j].x, 1);
-      if (lane == 31) nub = nvb0 = nvb1 = 0.f;
+      // right neighbours: own .y for .x, next lane's .x for .y. Lane 31's .y is
+      // tile column 63, inside the halo and without an x-edge: any finite value.
+      const float nub = __shfl_down_sync(FULL, ub[j].x, 1);
+      const float nvb0 = __shfl_down_sync(FULL, vb0[j].x, 1);
+      const float nvb1 = __shfl_down_sync(FULL, vb1[j].x, 1);
       // down neighbours: own next row, or the next strip's published first row
       f2 dub, dvb0, dvb1;
       if (j + 1 < PY) {
@@ -160,12 +179,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_pair(const BlockArgs A) {
       } else {
         dub = dvb0 = dvb1 = zero;
       }
-      const f2 gx = sel2(exx, exy, sub2(mk2(ub[j].y, nub), ub[j]));
-      const f2 gy = sel2(eyx, eyy, sub2(dub, ub[j]));
-      const f2 g00 = sel2(exx, exy, sub2(mk2(vb0[j].y, nvb0), vb0[j]));
-      const f2 g01 = sel2(eyx, eyy, sub2(dvb0, vb0[j]));
-      const f2 g10 = sel2(exx, exy, sub2(mk2(vb1[j].y, nvb1), vb1[j]));
-      const f2 g11 = sel2(eyx, eyy, sub2(dvb1, vb1[j]));
+      const f2 gx = mul2(exf[j], sub2(mk2(ub[j].y, nub), ub[j]));
+      const f2 gy = mul2(eyf[j], sub2(dub, ub[j]));
+      const f2 g00 = mul2(exf[j], sub2(mk2(vb0[j].y, nvb0), vb0[j]));
+      const f2 g01 = mul2(eyf[j], sub2(dvb0, vb0[j]));
+      const f2 g10 = mul2(exf[j], sub2(mk2(vb1[j].y, nvb1), vb1[j]));
+      const f2 g11 = mul2(eyf[j], sub2(dvb1, vb1[j]));
       // dual ascent (solver.py:290-293), two pixels per instruction
       f2 t0 = sub2(fma2(ta[j], gx, mul2(tb[j], gy)), vb0[j]);
       f2 t1 = sub2(fma2(tb[j], gx, mul2(tc[j], gy)), vb1[j]);
@@ -180,11 +199,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_pair(const BlockArgs A) {
       const f2 rq = unit_scale2(qn2);
       q0[j] = mul2(qq0, rq); q1[j] = mul2(qq1, rq); q2[j] = mul2(qq2, rq); q3[j] = mul2(qq3, rq);
       // edge-masked fluxes
-      fpx[j] = sel2(exx, exy, fma2(ta[j], p0[j], mul2(tb[j], p1[j])));
-      fpy[j] = sel2(eyx, eyy, fma2(tb[j], p0[j], mul2(tc[j], p1[j])));
-      fq0x[j] = sel2(exx, exy, q0[j]); fq0y[j] = sel2(eyx, eyy, q1[j]);
-      fq1x[j] = sel2(exx, exy, q2[j]); fq1y[j] = sel2(eyx, eyy, q3[j]);
-      if (A.diag_p) {
+      fpx[j] = mul2(exf[j], fma2(ta[j], p0[j], mul2(tb[j], p1[j])));
+      fpy[j] = mul2(eyf[j], fma2(tb[j], p0[j], mul2(tc[j], p1[j])));
+      fq0x[j] = mul2(exf[j], q0[j]); fq0y[j] = mul2(eyf[j], q1[j]);
+      fq1x[j] = mul2(exf[j], q2[j]); fq1y[j] = mul2(eyf[j], q3[j]);
+      if (DIAG) {
         const int r = r0 + j, gyy = oy + r;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -200,10 +219,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_pair(const BlockArgs A) {
         }
       }
     }
-    if (A.diag_p) {
+    if (DIAG) {
       pmax = warp_max(pmax);
       qmax = warp_max(qmax);
-      if (lane == 0) {
+      if (lane == 0 && A.diag_p && A.diag_q) {
         atomic_max_nonneg(A.diag_p + it - 1, pmax);
         atomic_max_nonneg(A.diag_q + it - 1, qmax);
       }
@@ -216,11 +235,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_pair(const BlockArgs A) {
 
 #pragma unroll
     for (int j = 0; j < PY; ++j) {
-      // left neighbours: previous lane's .y for .x (pad 0 before the tile), own .x for .y
-      float lpx = __shfl_up_sync(FULL, fpx[j].y, 1);
-      float lq0 = __shfl_up_sync(FULL, fq0x[j].y, 1);
-      float lq1 = __shfl_up_sync(FULL, fq1x[j].y, 1);
-      if (lane == 0) lpx = lq0 = lq1 = 0.f;
+      // left neighbours: previous lane's .y for .x, own .x for .y. Lane 0's .x is
+      // tile column 0, inside the halo: the value it reads only feeds halo pixels.
+      const float lpx = __shfl_up_sync(FULL, fpx[j].y, 1);
+      const float lq0 = __shfl_up_sync(FULL, fq0x[j].y, 1);
+      const float lq1 = __shfl_up_sync(FULL, fq1x[j].y, 1);
       f2 upy, uq0, uq1;
       if (j > 0) {
         upy = fpy[j - 1]; uq0 = fq0y[j - 1]; uq1 = fq1y[j - 1];
@@ -237,8 +256,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_pair(const BlockArgs A) {
       // primal descent + shrinkage + relaxation (solver.py:295-302)
       const f2 uhat = fma2(mul2(tu[j], ta1), dv, u[j]);
       const f2 rhat = fma2(sub2(uhat, uo[j]), g[j], rh[j]);
-      const f2 un = mk2(shrink_step<float>(uhat.x, rhat.x, g[j].x, tu[j].x, A.lam),
-                        shrink_step<float>(uhat.y, rhat.y, g[j].y, tu[j].y, A.lam));
+      const f2 un = shrink2(uhat, rhat, g[j], mul2(tu[j], lam2));
       const f2 v0n = fma2(tv[j], fma2(al0, d0, mul2(al1, p0[j])), v0[j]);
       const f2 v1n = fma2(tv[j], fma2(al0, d1, mul2(al1, p1[j])), v1[j]);
       ub[j] = fma2(th2, sub2(un, u[j]), un);
@@ -291,7 +309,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_pair(const BlockArgs A) {
       A.dst.q[3 * n + gi] = e ? q3[j].y : q3[j].x;
     }
   }
-  if (FIN && A.diag_du) {
+  if (FIN && DIAG && A.diag_du) {
     __shared__ double red_s[NW];
     __shared__ float red_m[NW];
     dmax = warp_max(dmax);
@@ -313,7 +331,10 @@ int launch_pair_shape(const BlockArgs& A, cudaStream_t st, int* nblocks) {
   using TL = PairTile<NW, PY, R>;
   dim3 grd((A.w + TL::TW - 1) / TL::TW, (A.h + TL::TH - 1) / TL::TH);
   if (nblocks) *nblocks = (int)(grd.x * grd.y);
-  k_pd_pair<NW, PY, R, LIN, FIN><<<grd, NW * 32, 0, st>>>(A);
+  if (A.diag_p || A.diag_du)
+    k_pd_pair<NW, PY, R, LIN, FIN, true><<<grd, NW * 32, 0, st>>>(A);
+  else
+    k_pd_pair<NW, PY, R, LIN, FIN, false><<<grd, NW * 32, 0, st>>>(A);
   return launch_status();
 }
 
