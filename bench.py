@@ -302,6 +302,16 @@ def pd_roofline(eng, rig, prm, img0, iters=50):
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     t_iter = e0.elapsed_time(e1) / 1e3 / iters
+    # launch cost model: one launch of k iterations, k = 1 .. halo (fixed + k * per-iteration)
+    model = {}
+    for k in (1, 2, 3, 4, 5):
+        reps = 20
+        e0.record(stream)
+        for _ in range(reps):
+            _ext.check(L.fsb_pd_iterate(C.byref(st), C.byref(ps), k, None, None, sp), "pd")
+        e1.record(stream)
+        torch.cuda.synchronize()
+        model[k] = e0.elapsed_time(e1) * 1e3 / reps
     bytes_iter = PD_BYTES_PER_PIXEL_ITER * H * W
     peak, peak_src = measured_peak()
     achieved = bytes_iter / t_iter / 1e9
@@ -310,7 +320,8 @@ def pd_roofline(eng, rig, prm, img0, iters=50):
             "kernel": "primal-dual iteration (fsb_pd_iterate: k_pd_dual + k_pd_primal)",
             "algorithmic_bytes_per_launch": bytes_iter,
             "per_unit": f"{PD_BYTES_PER_PIXEL_ITER} B per pixel-iteration x {H}x{W} px",
-            "us_per_launch": t_iter * 1e6, "peak_source": peak_src}
+            "us_per_launch": t_iter * 1e6, "peak_source": peak_src,
+            "us_per_call_by_iters": model}
 
 
 def run_b200(a) -> None:
