@@ -135,14 +135,13 @@ __global__ void __launch_bounds__(256) k_warp_prologue(fsb_level L) {
   constexpr int SW = TX + 2 * H, SH = TY + 2 * H;
   static_assert(SW <= 64, "row validity words are 64-bit");
   __shared__ float s_iw[SH * SW];
+  __shared__ uint8_t s_okb[SH * SW];
   __shared__ unsigned long long s_okrow[SH];  // bit c of row r: i1w_ok of tile pixel (r, c)
   __shared__ float2 s_dir[TY * TX];
   __shared__ uint8_t s_dok[TY * TX];
   const int ox = blockIdx.x * TX, oy = blockIdx.y * TY;
   const SampleSrc S{L.i1, L.mask, L.traj, L.traj_ok, reinterpret_cast<const float4*>(L.packed),
                     L.full16, L.h, L.w};
-  for (int k = threadIdx.x; k < SH; k += blockDim.x) s_okrow[k] = 0ull;
-  __syncthreads();
   for (int k = threadIdx.x; k < SH * SW; k += blockDim.x) {
     const int r = k / SW, c = k - r * SW;
     const int gx = ox - H + c, gy = oy - H + r;
@@ -165,7 +164,17 @@ __global__ void __launch_bounds__(256) k_warp_prologue(fsb_level L) {
       }
     }
     s_iw[k] = iw;
-    if (iok) atomicOr(&s_okrow[r], 1ull << c);
+    s_okb[k] = iok;
+  }
+  __syncthreads();
+  {  // pack the validity bytes into one 64-bit word per tile row (warp ballots)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int r = warp; r < SH; r += nwarps) {
+      const unsigned lo = __ballot_sync(0xffffffffu, lane < SW && s_okb[r * SW + lane]);
+      const unsigned hi =
+          __ballot_sync(0xffffffffu, lane + 32 < SW && s_okb[r * SW + lane + 32]);
+      if (lane == 0) s_okrow[r] = (unsigned long long)lo | ((unsigned long long)hi << 32);
+    }
   }
   __syncthreads();
   for (int k = threadIdx.x; k < TY * TX; k += blockDim.x) {
