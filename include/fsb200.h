@@ -192,6 +192,11 @@ typedef struct fsb_level {
    * mask / traj_ok (filled by fsb_level_setup when non-NULL). */
   float* packed;
   uint8_t* full16;
+  /* Optional 0/1 float copy of `mask` (filled by fsb_level_setup when non-NULL).
+   * When u, u_bar, v, v_bar, p, q form one block of 12 planes of stride h*w,
+   * state_b likewise, tensor, steps, iu, rho0, u_omega, maskf one block of 10
+   * planes, and w % 4 == 0, the PD iterations run in the persistent TMA kernel. */
+  float* maskf;
 } fsb_level;
 
 size_t fsb_level_partials(int32_t h, int32_t w);

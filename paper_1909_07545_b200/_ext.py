@@ -66,7 +66,7 @@ class FsbLevel(C.Structure):
         (name, C.c_void_p) for name in (
             "i0", "i1", "mask", "traj", "traj_ok", "tensor", "steps", "u", "u_bar", "v",
             "v_bar", "p", "q", "wv", "u_omega", "iu", "rho0", "i1w", "i1w_ok", "dirs",
-            "dir_ok", "partials", "state_b", "packed", "full16")]
+            "dir_ok", "partials", "state_b", "packed", "full16", "maskf")]
 
 
 class FsbPrim(C.Structure):

@@ -32,6 +32,7 @@ UNITS = [
     ("pd.cu", []),
     ("pd_block.cu", []),
     ("pd_pair.cu", []),
+    ("pd_tma.cu", []),
     ("solver.cu", []),
     ("synth.cu", ["-fmad=false"]),
 ]

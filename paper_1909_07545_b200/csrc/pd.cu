@@ -232,6 +232,7 @@ __global__ void k_pack_level(fsb_level L) {
     fl = (am ? 1 : 0) | (at ? 2 : 0);
   }
   L.full16[i] = fl;
+  if (L.maskf) L.maskf[i] = L.mask[i] ? 1.f : 0.f;
 }
 
 // Warp prologue part 2 (solver.py:339-346 with image_derivative_along 192-202):

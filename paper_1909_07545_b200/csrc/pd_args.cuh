@@ -2,6 +2,7 @@
 // (pd_block.cu per-pixel tiles, pd_pair.cu packed pixel pairs) and the driver.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -28,6 +29,17 @@ struct BlockArgs {
   // diagnostics (nullptr = off)
   float* diag_p; float* diag_q; float* diag_du; double* partials;
 };
+
+// TMA descriptors of one level for the persistent kernel (pd_tma.cu): the two
+// 12-plane state blocks and the 10-plane constant block, 64 x 32 boxes.
+struct TmaMaps {
+  CUtensorMap state[2];
+  CUtensorMap consts;
+};
+bool pd_tma_maps(TmaMaps* maps, const float* state_a, const float* state_b, const float* consts,
+                 int w, int h);
+int pd_tma_launch(const BlockArgs& A, const TmaMaps& maps, int src_set, int halo, bool lin,
+                  bool fin, cudaStream_t st, int* nparts);
 
 int pd_block_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st,
                     int* nblocks);

@@ -1,0 +1,442 @@
+// K6 (v4): persistent, TMA-fed pixel-pair primal-dual kernel.
+//
+// Same cycles as k_pd_pair (pd_pair.cu) — packed fp32x2 arithmetic on pixel
+// pairs, shuffles for x-neighbours, strip-edge shared-memory exchange for
+// y-neighbours, R-pixel halo, `iters` cycles per launch — but the per-tile
+// load is issued by one thread as two 3-D TMA boxes (cp.async.bulk.tensor):
+// the 12 state planes and the 10 constant planes (tensor a b c, steps,
+// I_u, rho0, u_omega, mask) of a 64 x 32 tile, zero-filled outside the image,
+// landing in shared memory under an mbarrier. CTAs are persistent (one per
+// SM) and prefetch tile t + gridDim while they iterate on tile t, so the
+// 176 KB tile load overlaps the cycles instead of stalling them.
+//
+// Requirements (checked by the driver, else it uses k_pd_pair): both state
+// sets and the constants are plane blocks of stride n = h*w, w % 4 == 0.
+
+#include <cuda.h>
+#include <stdlib.h>
+
+#include "pd_args.cuh"
+#include "pd_math.cuh"
+
+namespace fsb {
+namespace {
+
+typedef float2 f2;
+
+FSB_INLINE f2 mk2(float a, float b) { return make_float2(a, b); }
+FSB_INLINE f2 add2(f2 a, f2 b) { return __fadd2_rn(a, b); }
+FSB_INLINE f2 sub2(f2 a, f2 b) { return __fadd2_rn(a, mk2(-b.x, -b.y)); }
+FSB_INLINE f2 mul2(f2 a, f2 b) { return __fmul2_rn(a, b); }
+FSB_INLINE f2 fma2(f2 a, f2 b, f2 c) { return __ffma2_rn(a, b, c); }
+FSB_INLINE f2 unit_scale2(f2 n2) {
+  return mk2(n2.x > 1.f ? rsqrtf(n2.x) : 1.f, n2.y > 1.f ? rsqrtf(n2.y) : 1.f);
+}
+FSB_INLINE float shrink1(float uh, float rh, float g, float tl) {
+  const float a = tl * g;
+  const float th = a * g;
+  const float q = g != 0.f ? __fdividef(rh, g) : 0.f;
+  const float step = rh < -th ? a : (rh > th ? -a : -q);
+  return g != 0.f ? uh + step : uh;
+}
+FSB_INLINE f2 shrink2(f2 uh, f2 rh, f2 g, f2 tl) {
+  return mk2(shrink1(uh.x, rh.x, g.x, tl.x), shrink1(uh.y, rh.y, g.y, tl.y));
+}
+
+FSB_INLINE uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+FSB_INLINE void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+FSB_INLINE void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+FSB_INLINE void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+FSB_INLINE void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kNW = 16, kPY = 2, kEW = 64, kEH = kNW * kPY;
+constexpr int kStatePlanes = 12, kConstPlanes = 10;
+constexpr int kPlane = kEW * kEH;  // floats per plane in the staging tile
+constexpr uint32_t kTileBytes = (kStatePlanes + kConstPlanes) * kPlane * sizeof(float);
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + kTileBytes +
+                              2 * sizeof(f2) * kNW * 3 * 32 /*s_top, s_bot*/ + 64 /*mbarrier*/;
+
+// staging plane indices
+enum { SU, SUB, SV0, SV1, SVB0, SVB1, SP0, SP1, SQ0, SQ1, SQ2, SQ3 };
+enum { CA, CB, CC, CSP, CTU, CTV, CIU, CRH, CUO, CM };
+
+template <int R, bool LIN, bool FIN, bool DIAG>
+__global__ void __launch_bounds__(kNW * 32, 1)
+    k_pd_tma(const BlockArgs A, const __grid_constant__ CUtensorMap tm_src,
+             const __grid_constant__ CUtensorMap tm_const, int ntx, int ntiles) {
+  constexpr int TW = kEW - 2 * R, TH = kEH - 2 * R, NW = kNW, PY = kPY, EH = kEH;
+  constexpr unsigned FULL = 0xffffffffu;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* st = reinterpret_cast<float*>(base);  // [12 + 10][EH][64]
+  const float* cs = st + kStatePlanes * kPlane;
+  f2(*s_top)[3][32] = reinterpret_cast<f2(*)[3][32]>(base + kTileBytes);
+  f2(*s_bot)[3][32] = s_top + NW;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(s_bot + NW);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = warp * PY, c0 = 2 * lane;
+  const size_t n = A.n;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int tile) {
+    if (threadIdx.x == 0) {
+      const int tx = tile % ntx, ty = tile / ntx;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar, kTileBytes);
+      tma_load_3d(st, &tm_src, tx * TW - R, ty * TH - R, 0, bar);
+      tma_load_3d(st + kStatePlanes * kPlane, &tm_const, tx * TW - R, ty * TH - R, 0, bar);
+    }
+  };
+
+  uint32_t parity = 0;
+  int tile = blockIdx.x;
+  if (tile < ntiles) issue(tile);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int ox = (tile % ntx) * TW - R, oy = (tile / ntx) * TH - R;
+    mbar_wait(bar, parity);
+    parity ^= 1;
+
+    f2 u[PY], v0[PY], v1[PY], p0[PY], p1[PY], q0[PY], q1[PY], q2[PY], q3[PY];
+    f2 ub[PY], vb0[PY], vb1[PY];
+    f2 ta[PY], tb[PY], tc[PY], sp[PY], tu[PY], tv[PY], g[PY], rh[PY], uo[PY];
+    f2 exf[PY], eyf[PY];
+    unsigned mbits = 0;  // mask of the two pixels of row j at bits 2j, 2j+1
+    const f2 a1 = mk2(A.alpha1, A.alpha1);
+#pragma unroll
+    for (int j = 0; j < PY; ++j) {
+      const int r = r0 + j;
+      const int o = r * kEW + c0;
+      auto S2 = [&](int plane) { return *reinterpret_cast<const f2*>(st + plane * kPlane + o); };
+      auto C2 = [&](int plane) { return *reinterpret_cast<const f2*>(cs + plane * kPlane + o); };
+      u[j] = S2(SU); v0[j] = S2(SV0); v1[j] = S2(SV1);
+      p0[j] = S2(SP0); p1[j] = S2(SP1);
+      q0[j] = S2(SQ0); q1[j] = S2(SQ1); q2[j] = S2(SQ2); q3[j] = S2(SQ3);
+      ta[j] = C2(CA); tb[j] = C2(CB); tc[j] = C2(CC);
+      sp[j] = mul2(C2(CSP), a1); tu[j] = C2(CTU); tv[j] = C2(CTV);
+      g[j] = C2(CIU); rh[j] = C2(CRH);
+      if (LIN) {  // warp start (solver.py:344-346)
+        uo[j] = u[j]; ub[j] = u[j]; vb0[j] = v0[j]; vb1[j] = v1[j];
+      } else {
+        uo[j] = C2(CUO); ub[j] = S2(SUB); vb0[j] = S2(SVB0); vb1[j] = S2(SVB1);
+      }
+      // mask (0/1 floats; zero outside the image and past the tile edge)
+      const f2 m = C2(CM);
+      const float mr = c0 + 2 < kEW ? cs[CM * kPlane + o + 2] : 0.f;
+      const f2 md = r + 1 < EH ? *reinterpret_cast<const f2*>(cs + CM * kPlane + o + kEW)
+                               : mk2(0.f, 0.f);
+      exf[j] = mk2(m.x * m.y, m.y * mr);
+      eyf[j] = mk2(m.x * md.x, m.y * md.y);
+      mbits |= (m.x != 0.f ? 1u : 0u) << (2 * j);
+      mbits |= (m.y != 0.f ? 1u : 0u) << (2 * j + 1);
+    }
+    __syncthreads();  // staging consumed: prefetch the next tile behind the cycles
+    if (tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x);
+
+    const f2 sq2 = mk2(A.sigma_q * A.alpha0, A.sigma_q * A.alpha0);
+    const f2 al0 = mk2(A.alpha0, A.alpha0), th2 = mk2(A.theta, A.theta);
+    const f2 lam2 = mk2(A.lam, A.lam), zero = mk2(0.f, 0.f);
+
+    for (int it = 1; it <= A.iters; ++it) {
+      s_top[warp][0][lane] = ub[0];
+      s_top[warp][1][lane] = vb0[0];
+      s_top[warp][2][lane] = vb1[0];
+      __syncthreads();
+      float pmax = 0.f, qmax = 0.f;
+      f2 fpx[PY], fpy[PY], fq0x[PY], fq0y[PY], fq1x[PY], fq1y[PY];
+#pragma unroll
+      for (int j = 0; j < PY; ++j) {
+        const float nub = __shfl_down_sync(FULL, ub[j].x, 1);
+        const float nvb0 = __shfl_down_sync(FULL, vb0[j].x, 1);
+        const float nvb1 = __shfl_down_sync(FULL, vb1[j].x, 1);
+        f2 dub, dvb0, dvb1;
+        if (j + 1 < PY) {
+          dub = ub[j + 1]; dvb0 = vb0[j + 1]; dvb1 = vb1[j + 1];
+        } else if (warp + 1 < NW) {
+          dub = s_top[warp + 1][0][lane]; dvb0 = s_top[warp + 1][1][lane];
+          dvb1 = s_top[warp + 1][2][lane];
+        } else {
+          dub = dvb0 = dvb1 = zero;
+        }
+        const f2 gx = mul2(exf[j], sub2(mk2(ub[j].y, nub), ub[j]));
+        const f2 gy = mul2(eyf[j], sub2(dub, ub[j]));
+        const f2 g00 = mul2(exf[j], sub2(mk2(vb0[j].y, nvb0), vb0[j]));
+        const f2 g01 = mul2(eyf[j], sub2(dvb0, vb0[j]));
+        const f2 g10 = mul2(exf[j], sub2(mk2(vb1[j].y, nvb1), vb1[j]));
+        const f2 g11 = mul2(eyf[j], sub2(dvb1, vb1[j]));
+        const f2 t0 = sub2(fma2(ta[j], gx, mul2(tb[j], gy)), vb0[j]);
+        const f2 t1 = sub2(fma2(tb[j], gx, mul2(tc[j], gy)), vb1[j]);
+        const f2 pp0 = fma2(sp[j], t0, p0[j]);
+        const f2 pp1 = fma2(sp[j], t1, p1[j]);
+        const f2 rp = unit_scale2(fma2(pp0, pp0, mul2(pp1, pp1)));
+        p0[j] = mul2(pp0, rp);
+        p1[j] = mul2(pp1, rp);
+        const f2 qq0 = fma2(sq2, g00, q0[j]), qq1 = fma2(sq2, g01, q1[j]);
+        const f2 qq2 = fma2(sq2, g10, q2[j]), qq3 = fma2(sq2, g11, q3[j]);
+        const f2 rq = unit_scale2(add2(fma2(qq0, qq0, mul2(qq1, qq1)),
+                                       fma2(qq2, qq2, mul2(qq3, qq3))));
+        q0[j] = mul2(qq0, rq); q1[j] = mul2(qq1, rq);
+        q2[j] = mul2(qq2, rq); q3[j] = mul2(qq3, rq);
+        fpx[j] = mul2(exf[j], fma2(ta[j], p0[j], mul2(tb[j], p1[j])));
+        fpy[j] = mul2(eyf[j], fma2(tb[j], p0[j], mul2(tc[j], p1[j])));
+        fq0x[j] = mul2(exf[j], q0[j]); fq0y[j] = mul2(eyf[j], q1[j]);
+        fq1x[j] = mul2(exf[j], q2[j]); fq1y[j] = mul2(eyf[j], q3[j]);
+        if (DIAG) {
+          const int r = r0 + j, gyy = oy + r;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c = c0 + e, gxx = ox + c;
+            if (r >= R && r < EH - R && c >= R && c < kEW - R &&
+                (unsigned)gxx < (unsigned)A.w && (unsigned)gyy < (unsigned)A.h) {
+              const float a0 = e ? p0[j].y : p0[j].x, a1_ = e ? p1[j].y : p1[j].x;
+              const float b0 = e ? q0[j].y : q0[j].x, b1 = e ? q1[j].y : q1[j].x;
+              const float b2 = e ? q2[j].y : q2[j].x, b3 = e ? q3[j].y : q3[j].x;
+              pmax = fmaxf(pmax, sqrtf(a0 * a0 + a1_ * a1_));
+              qmax = fmaxf(qmax, sqrtf((b0 * b0 + b1 * b1) + (b2 * b2 + b3 * b3)));
+            }
+          }
+        }
+      }
+      if (DIAG) {
+        pmax = warp_max(pmax);
+        qmax = warp_max(qmax);
+        if (lane == 0 && A.diag_p && A.diag_q) {
+          atomic_max_nonneg(A.diag_p + it - 1, pmax);
+          atomic_max_nonneg(A.diag_q + it - 1, qmax);
+        }
+      }
+      s_bot[warp][0][lane] = fpy[PY - 1];
+      s_bot[warp][1][lane] = fq0y[PY - 1];
+      s_bot[warp][2][lane] = fq1y[PY - 1];
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < PY; ++j) {
+        const float lpx = __shfl_up_sync(FULL, fpx[j].y, 1);
+        const float lq0 = __shfl_up_sync(FULL, fq0x[j].y, 1);
+        const float lq1 = __shfl_up_sync(FULL, fq1x[j].y, 1);
+        f2 upy, uq0, uq1;
+        if (j > 0) {
+          upy = fpy[j - 1]; uq0 = fq0y[j - 1]; uq1 = fq1y[j - 1];
+        } else if (warp > 0) {
+          upy = s_bot[warp - 1][0][lane]; uq0 = s_bot[warp - 1][1][lane];
+          uq1 = s_bot[warp - 1][2][lane];
+        } else {
+          upy = uq0 = uq1 = zero;
+        }
+        const f2 dv = sub2(add2(sub2(fpx[j], mk2(lpx, fpx[j].x)), fpy[j]), upy);
+        const f2 d0 = sub2(add2(sub2(fq0x[j], mk2(lq0, fq0x[j].x)), fq0y[j]), uq0);
+        const f2 d1 = sub2(add2(sub2(fq1x[j], mk2(lq1, fq1x[j].x)), fq1y[j]), uq1);
+        const f2 uhat = fma2(mul2(tu[j], a1), dv, u[j]);
+        const f2 rhat = fma2(sub2(uhat, uo[j]), g[j], rh[j]);
+        const f2 un = shrink2(uhat, rhat, g[j], mul2(tu[j], lam2));
+        const f2 v0n = fma2(tv[j], fma2(al0, d0, mul2(a1, p0[j])), v0[j]);
+        const f2 v1n = fma2(tv[j], fma2(al0, d1, mul2(a1, p1[j])), v1[j]);
+        ub[j] = fma2(th2, sub2(un, u[j]), un);
+        vb0[j] = fma2(th2, sub2(v0n, v0[j]), v0n);
+        vb1[j] = fma2(th2, sub2(v1n, v1[j]), v1n);
+        u[j] = un; v0[j] = v0n; v1[j] = v1n;
+      }
+    }
+
+    // ---- epilogue + store of the interior
+    float dmax = 0.f;
+    double dsum = 0.0;
+#pragma unroll
+    for (int j = 0; j < PY; ++j) {
+      const int r = r0 + j, gy = oy + r;
+      if (r < R || r >= EH - R || (unsigned)gy >= (unsigned)A.h) continue;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = c0 + e, gx = ox + c;
+        if (c < R || c >= kEW - R || (unsigned)gx >= (unsigned)A.w) continue;
+        const size_t gi = (size_t)gy * A.w + gx;
+        float uu = e ? u[j].y : u[j].x, ubb = e ? ub[j].y : ub[j].x;
+        if (FIN) {  // solver.py:356-360
+          const float uom = e ? uo[j].y : uo[j].x;
+          const bool mk = (mbits >> (2 * j + e)) & 1u;
+          float du = fminf(fmaxf(uu - uom, -A.du_max), A.du_max);
+          if (!mk) du = 0.f;
+          uu = uom + du;
+          ubb = uu;
+          const float2 d = reinterpret_cast<const float2*>(A.dirs)[gi];
+          float2 wv = reinterpret_cast<float2*>(A.wv)[gi];
+          wv.x = wv.x + du * d.x;
+          wv.y = wv.y + du * d.y;
+          reinterpret_cast<float2*>(A.wv)[gi] = wv;
+          dmax = fmaxf(dmax, fabsf(du));
+          dsum += (double)fabsf(du);
+        }
+        if (LIN) A.u_omega[gi] = e ? uo[j].y : uo[j].x;
+        A.dst.u[gi] = uu;
+        A.dst.ub[gi] = ubb;
+        A.dst.v[gi] = e ? v0[j].y : v0[j].x;
+        A.dst.v[n + gi] = e ? v1[j].y : v1[j].x;
+        A.dst.vb[gi] = e ? vb0[j].y : vb0[j].x;
+        A.dst.vb[n + gi] = e ? vb1[j].y : vb1[j].x;
+        A.dst.p[gi] = e ? p0[j].y : p0[j].x;
+        A.dst.p[n + gi] = e ? p1[j].y : p1[j].x;
+        A.dst.q[gi] = e ? q0[j].y : q0[j].x;
+        A.dst.q[n + gi] = e ? q1[j].y : q1[j].x;
+        A.dst.q[2 * n + gi] = e ? q2[j].y : q2[j].x;
+        A.dst.q[3 * n + gi] = e ? q3[j].y : q3[j].x;
+      }
+    }
+    if (FIN && DIAG && A.diag_du) {
+      __shared__ double red_s[NW];
+      __shared__ float red_m[NW];
+      dmax = warp_max(dmax);
+      dsum = warp_sum(dsum);
+      if (lane == 0) { red_s[warp] = dsum; red_m[warp] = dmax; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        float m = 0.f;
+        for (int k = 0; k < NW; ++k) { t += red_s[k]; m = fmaxf(m, red_m[k]); }
+        A.partials[tile] = t;
+        atomic_max_nonneg(A.diag_du, m);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encoder() {
+  static EncodeTiled fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  }
+  return fn;
+}
+
+// planes x h x w fp32 block with plane stride n; box 64 x 32 x planes
+bool make_map(CUtensorMap* m, const float* base, int w, int h, int planes, size_t n) {
+  EncodeTiled enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)planes};
+  cuuint64_t strides[2] = {(cuuint64_t)w * sizeof(float), (cuuint64_t)n * sizeof(float)};
+  cuuint32_t box[3] = {(cuuint32_t)kEW, (cuuint32_t)kEH, (cuuint32_t)planes};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+template <int R, bool LIN, bool FIN, bool DIAG>
+int launch_tma(const BlockArgs& A, const CUtensorMap& ms, const CUtensorMap& mc, cudaStream_t st,
+               int* ntiles_out) {
+  constexpr int TW = kEW - 2 * R, TH = kEH - 2 * R;
+  const int ntx = (A.w + TW - 1) / TW, nty = (A.h + TH - 1) / TH, ntiles = ntx * nty;
+  static bool attr = false;
+  auto kern = k_pd_tma<R, LIN, FIN, DIAG>;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    attr = true;
+  }
+  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  if (ntiles_out) *ntiles_out = ntiles;
+  kern<<<grid, kNW * 32, kSmemBytes, st>>>(A, ms, mc, ntx, ntiles);
+  return launch_status();
+}
+
+template <int R, bool LIN, bool FIN>
+int launch_tma_d(const BlockArgs& A, const CUtensorMap& ms, const CUtensorMap& mc,
+                 cudaStream_t st, int* nt) {
+  if (A.diag_p || A.diag_du) return launch_tma<R, LIN, FIN, true>(A, ms, mc, st, nt);
+  return launch_tma<R, LIN, FIN, false>(A, ms, mc, st, nt);
+}
+
+template <int R>
+int launch_tma_r(const BlockArgs& A, const CUtensorMap& ms, const CUtensorMap& mc, bool lin,
+                 bool fin, cudaStream_t st, int* nt) {
+  if (lin && fin) return launch_tma_d<R, true, true>(A, ms, mc, st, nt);
+  if (lin) return launch_tma_d<R, true, false>(A, ms, mc, st, nt);
+  if (fin) return launch_tma_d<R, false, true>(A, ms, mc, st, nt);
+  return launch_tma_d<R, false, false>(A, ms, mc, st, nt);
+}
+
+}  // namespace
+
+bool pd_tma_maps(TmaMaps* maps, const float* state_a, const float* state_b, const float* consts,
+                 int w, int h) {
+  const size_t n = (size_t)w * h;
+  if (w % 4 != 0) return false;
+  if (((uintptr_t)state_a | (uintptr_t)state_b | (uintptr_t)consts) & 15) return false;
+  return make_map(&maps->state[0], state_a, w, h, kStatePlanes, n) &&
+         make_map(&maps->state[1], state_b, w, h, kStatePlanes, n) &&
+         make_map(&maps->consts, consts, w, h, kConstPlanes, n);
+}
+
+size_t pd_tma_partials(int w, int h, int halo) {
+  const int TW = kEW - 2 * halo, TH = kEH - 2 * halo;
+  return (size_t)((w + TW - 1) / TW) * ((h + TH - 1) / TH);
+}
+
+int pd_tma_launch(const BlockArgs& A, const TmaMaps& maps, int src_set, int halo, bool lin,
+                  bool fin, cudaStream_t st, int* nparts) {
+  if (A.iters < 1 || A.iters > halo) return FSB_EINVAL;
+  const CUtensorMap& ms = maps.state[src_set];
+  switch (halo) {
+    case 1: return launch_tma_r<1>(A, ms, maps.consts, lin, fin, st, nparts);
+    case 2: return launch_tma_r<2>(A, ms, maps.consts, lin, fin, st, nparts);
+    case 3: return launch_tma_r<3>(A, ms, maps.consts, lin, fin, st, nparts);
+    case 5: return launch_tma_r<5>(A, ms, maps.consts, lin, fin, st, nparts);
+    default: return FSB_EINVAL;
+  }
+}
+
+}  // namespace fsb

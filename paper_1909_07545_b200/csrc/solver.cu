@@ -97,11 +97,14 @@ struct Carve {
 };
 
 struct LevelState {  // state buffers sized for the finest level, reused per level
-  float *u[2], *wv[2];
-  float *u_bar, *v, *v_bar, *p, *q, *T, *S, *u_omega, *iu, *rho0, *i1w, *dirs;
+  float* state_a;  // 12 planes u, u_bar, v x2, v_bar x2, p x2, q x4 (plane stride = level n)
+  float* state_b;  // ping-pong copy
+  float* consts;   // 10 planes T x3, steps x3, iu, rho0, u_omega, maskf
+  float* carry_u;  // previous level's u for upsample_state
+  float* wv[2];
+  float *i1w, *dirs;
   uint8_t *i1w_ok, *dir_ok;
   double* partials;
-  float* state_b;
   float* packed;
   uint8_t* full16;
 };
@@ -153,17 +156,10 @@ int make_plan(const fsb_rig* rig, const fsb_params* prm, void* base, Plan& P) {
   P.setup_scratch_bytes = level_setup_scratch_internal(H, W);
   P.setup_scratch = c.take<char>(P.setup_scratch_bytes);
   LevelState& s = P.st;
-  for (int k = 0; k < 2; ++k) { s.u[k] = c.take<float>(n0); s.wv[k] = c.take<float>(2 * n0); }
-  s.u_bar = c.take<float>(n0);
-  s.v = c.take<float>(2 * n0);
-  s.v_bar = c.take<float>(2 * n0);
-  s.p = c.take<float>(2 * n0);
-  s.q = c.take<float>(4 * n0);
-  s.T = c.take<float>(3 * n0);
-  s.S = c.take<float>(3 * n0);
-  s.u_omega = c.take<float>(n0);
-  s.iu = c.take<float>(n0);
-  s.rho0 = c.take<float>(n0);
+  for (int k = 0; k < 2; ++k) s.wv[k] = c.take<float>(2 * n0);
+  s.state_a = c.take<float>(12 * n0);
+  s.consts = c.take<float>(10 * n0);
+  s.carry_u = c.take<float>(n0);
   s.i1w = c.take<float>(n0);
   s.dirs = c.take<float>(2 * n0);
   s.i1w_ok = c.take<uint8_t>(n0);
@@ -206,10 +202,30 @@ int pd_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st,
   static int which = -1;
   if (which < 0) {
     const char* e = getenv("FSB_PD_KERNEL");
-    which = (e && strcmp(e, "block") == 0) ? 1 : 0;
+    which = (e && strcmp(e, "block") == 0) ? 1 : 0;  // otherwise the pixel-pair kernel
   }
   return which ? pd_block_launch(A, halo, lin, fin, st, nblocks)
                : pd_pair_launch(A, halo, lin, fin, st, nblocks);
+}
+
+// The persistent TMA kernel needs plane blocks (see fsb_level in fsb200.h).
+bool tma_layout(const fsb_level* L) {
+  const size_t n = (size_t)L->h * L->w;
+  if (!L->state_b || !L->maskf || L->w % 4 != 0) return false;
+  const float* u = L->u;
+  if (L->u_bar != u + n || L->v != u + 2 * n || L->v_bar != u + 4 * n || L->p != u + 6 * n ||
+      L->q != u + 8 * n)
+    return false;
+  const float* c = L->tensor;
+  if (L->steps != c + 3 * n || L->iu != c + 6 * n || L->rho0 != c + 7 * n ||
+      L->u_omega != c + 8 * n || L->maskf != c + 9 * n)
+    return false;
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("FSB_PD_KERNEL");
+    env = (e && strcmp(e, "tma") != 0) ? 0 : 1;  // FSB_PD_KERNEL=pair|block disables TMA
+  }
+  return env == 1;
 }
 
 StateSet set_a(const fsb_level* L) {
@@ -239,6 +255,8 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
   const int N = prm->warp_iters, K = prm->pd_iters;
   const int halo = pd_halo(K);
   StateSet sets[2] = {set_a(L), set_b(L)};
+  TmaMaps maps;
+  const bool tma = tma_layout(L) && pd_tma_maps(&maps, L->u, L->state_b, L->tensor, L->w, L->h);
   int cur = 0;
   BlockArgs A;
   memset(&A, 0, sizeof(A));
@@ -265,7 +283,8 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
       A.diag_p = dpq ? diag->max_p_norm + pd_off + (int64_t)wi * K + done : nullptr;
       A.diag_q = dpq ? diag->max_q_norm + pd_off + (int64_t)wi * K + done : nullptr;
       A.diag_du = (fin && ddu) ? diag->max_du + warp_off + wi : nullptr;
-      rc = pd_launch(A, halo, lin, fin, st, &nblocks);
+      rc = tma ? pd_tma_launch(A, maps, cur, halo, lin, fin, st, &nblocks)
+               : pd_launch(A, halo, lin, fin, st, &nblocks);
       if (rc) return rc;
       cur ^= 1;
       done += it;
@@ -296,6 +315,8 @@ int pd_iterate_blocked(const fsb_level* L, const fsb_params* prm, int iters, flo
   const size_t n = (size_t)L->h * L->w;
   const int halo = pd_halo(iters);
   StateSet sets[2] = {set_a(L), set_b(L)};
+  TmaMaps maps;
+  const bool tma = tma_layout(L) && pd_tma_maps(&maps, L->u, L->state_b, L->tensor, L->w, L->h);
   BlockArgs A;
   memset(&A, 0, sizeof(A));
   A.h = L->h; A.w = L->w; A.n = n;
@@ -311,7 +332,8 @@ int pd_iterate_blocked(const fsb_level* L, const fsb_params* prm, int iters, flo
     A.iters = it;
     A.diag_p = (dp && dq) ? dp + done : nullptr;
     A.diag_q = (dp && dq) ? dq + done : nullptr;
-    int rc = pd_launch(A, halo, false, false, st, nullptr);
+    int rc = tma ? pd_tma_launch(A, maps, cur, halo, false, false, st, nullptr)
+                 : pd_launch(A, halo, false, false, st, nullptr);
     if (rc) return rc;
     cur ^= 1;
     done += it;
@@ -429,13 +451,13 @@ int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const floa
       tok = P.traj_ok[l];
     }
     LevelState& S = P.st;
-    float* u = S.u[cur];
+    float* u = S.state_a;  // plane 0 of the level's state block
     float* wv = S.wv[cur];
     if (k == 0) {
       cudaMemsetAsync(u, 0, np * sizeof(float), st);
       cudaMemsetAsync(wv, 0, 2 * np * sizeof(float), st);
     } else {
-      rc = upsample_internal(S.u[cur ^ 1], S.wv[cur ^ 1], prev_mask, prev_h, prev_w, P.lvl_mask[l],
+      rc = upsample_internal(S.carry_u, S.wv[cur ^ 1], prev_mask, prev_h, prev_w, P.lvl_mask[l],
                              h, w, u, wv, st);
       if (rc) return rc;
     }
@@ -444,9 +466,11 @@ int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const floa
     L.h = h; L.w = w;
     L.i0 = P.lvl_i0[l]; L.i1 = P.lvl_i1[l]; L.mask = P.lvl_mask[l];
     L.traj = traj; L.traj_ok = tok;
-    L.tensor = S.T; L.steps = S.S;
-    L.u = u; L.u_bar = S.u_bar; L.v = S.v; L.v_bar = S.v_bar; L.p = S.p; L.q = S.q;
-    L.wv = wv; L.u_omega = S.u_omega; L.iu = S.iu; L.rho0 = S.rho0; L.i1w = S.i1w;
+    L.u = u; L.u_bar = u + np; L.v = u + 2 * np; L.v_bar = u + 4 * np; L.p = u + 6 * np;
+    L.q = u + 8 * np;
+    L.tensor = S.consts; L.steps = S.consts + 3 * np; L.iu = S.consts + 6 * np;
+    L.rho0 = S.consts + 7 * np; L.u_omega = S.consts + 8 * np; L.maskf = S.consts + 9 * np;
+    L.wv = wv; L.i1w = S.i1w;
     L.i1w_ok = S.i1w_ok; L.dirs = S.dirs; L.dir_ok = S.dir_ok; L.partials = S.partials;
     L.state_b = S.state_b;
     L.packed = S.packed; L.full16 = S.full16;
@@ -456,13 +480,14 @@ int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const floa
     pd_off += (int64_t)N * K;
     warp_off += N;
     prev_h = h; prev_w = w; prev_mask = P.lvl_mask[l];
+    if (l > 0) cudaMemcpyAsync(S.carry_u, u, np * sizeof(float), cudaMemcpyDeviceToDevice, st);
     if (l == 0) {
       cudaMemcpyAsync(u_out, u, n0 * sizeof(float), cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(w_out, wv, 2 * n0 * sizeof(float), cudaMemcpyDeviceToDevice, st);
       // v planes -> interleaved (H,W,2) output
-      cudaMemcpy2DAsync(v_out, 2 * sizeof(float), S.v, sizeof(float), sizeof(float), n0,
+      cudaMemcpy2DAsync(v_out, 2 * sizeof(float), L.v, sizeof(float), sizeof(float), n0,
                         cudaMemcpyDeviceToDevice, st);
-      cudaMemcpy2DAsync(v_out + 1, 2 * sizeof(float), S.v + n0, sizeof(float), sizeof(float), n0,
+      cudaMemcpy2DAsync(v_out + 1, 2 * sizeof(float), L.v + n0, sizeof(float), sizeof(float), n0,
                         cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(mask_out, P.solve_mask, n0, cudaMemcpyDeviceToDevice, st);
     }

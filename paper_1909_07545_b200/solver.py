@@ -125,12 +125,18 @@ class _Level:
         U8 = torch.uint8
         self.i0 = E((h, w)); self.i1 = E((h, w)); self.mask = E((h, w), U8)
         self.traj = E((h, w, 2)); self.traj_ok = E((h, w), U8)
-        self.tensor = E((3, h, w)); self.steps = E((3, h, w))
-        self.u = E((h, w)); self.u_bar = E((h, w))
-        self.v = E((2, h, w)); self.v_bar = E((2, h, w))
-        self.p = E((2, h, w)); self.q = E((4, h, w))
-        self.wv = E((h, w, 2)); self.u_omega = E((h, w))
-        self.iu = E((h, w)); self.rho0 = E((h, w)); self.i1w = E((h, w))
+        # state planes as one (12, h, w) block and the per-warp constants as one
+        # (10, h, w) block: the layout the TMA-fed PD kernel loads as 3-D boxes
+        self.state_a = E((12, h, w))
+        self.u, self.u_bar = self.state_a[0], self.state_a[1]
+        self.v, self.v_bar = self.state_a[2:4], self.state_a[4:6]
+        self.p, self.q = self.state_a[6:8], self.state_a[8:12]
+        self.consts = E((10, h, w))
+        self.tensor, self.steps = self.consts[0:3], self.consts[3:6]
+        self.iu, self.rho0, self.u_omega = self.consts[6], self.consts[7], self.consts[8]
+        self.maskf = self.consts[9] if blocked else None
+        self.wv = E((h, w, 2))
+        self.i1w = E((h, w))
         self.i1w_ok = E((h, w), U8); self.dirs = E((h, w, 2)); self.dir_ok = E((h, w), U8)
         self.partials = E((int(_ext.lib().fsb_level_partials(h, w)),), torch.float64)
         # second state set (ping-pong) -> temporally blocked PD kernel (K6)
