@@ -110,19 +110,22 @@ __global__ void __launch_bounds__(kNW * 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto issue = [&](int tile) {
-    if (threadIdx.x == 0) {
-      const int tx = tile % ntx, ty = tile / ntx;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(bar, kTileBytes);
-      tma_load_3d(st, &tm_src, tx * TW - R, ty * TH - R, 0, bar);
-      tma_load_3d(st + kStatePlanes * kPlane, &tm_const, tx * TW - R, ty * TH - R, 0, bar);
-    }
-  };
+  // The tensor maps are used straight from the __grid_constant__ parameters
+  // (never copied: TMA needs the descriptor in param/const/global space).
+#define FSB_ISSUE_TILE(TILE)                                                              \
+  do {                                                                                    \
+    if (threadIdx.x == 0) {                                                               \
+      const int tx_ = (TILE) % ntx, ty_ = (TILE) / ntx;                                   \
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");                        \
+      mbar_expect_tx(bar, kTileBytes);                                                    \
+      tma_load_3d(st, &tm_src, tx_ * TW - R, ty_ * TH - R, 0, bar);                        \
+      tma_load_3d(st + kStatePlanes * kPlane, &tm_const, tx_ * TW - R, ty_ * TH - R, 0, bar); \
+    }                                                                                     \
+  } while (0)
 
   uint32_t parity = 0;
   int tile = blockIdx.x;
-  if (tile < ntiles) issue(tile);
+  if (tile < ntiles) FSB_ISSUE_TILE(tile);
   for (; tile < ntiles; tile += gridDim.x) {
     const int ox = (tile % ntx) * TW - R, oy = (tile / ntx) * TH - R;
     mbar_wait(bar, parity);
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       mbits |= (m.y != 0.f ? 1u : 0u) << (2 * j + 1);
     }
     __syncthreads();  // staging consumed: prefetch the next tile behind the cycles
-    if (tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x);
+    if (tile + (int)gridDim.x < ntiles) FSB_ISSUE_TILE(tile + (int)gridDim.x);
 
     const f2 sq2 = mk2(A.sigma_q * A.alpha0, A.sigma_q * A.alpha0);
     const f2 al0 = mk2(A.alpha0, A.alpha0), th2 = mk2(A.theta, A.theta);
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       __syncthreads();
     }
   }
+#undef FSB_ISSUE_TILE
 }
 
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
