@@ -5,7 +5,8 @@
 // y-neighbours, R-pixel halo, `iters` cycles per launch — but the per-tile
 // load is issued by one thread as two 3-D TMA boxes (cp.async.bulk.tensor):
 // the 12 state planes and the 10 constant planes (tensor a b c, steps,
-// I_u, rho0, u_omega, mask) of a 64 x 32 tile, zero-filled outside the image,
+// I_u, rho0, u_omega, mask) of a 64 x 32 tile (68-wide box, see kBoxW),
+// zero-filled outside the image,
 // landing in shared memory under an mbarrier. CTAs are persistent (one per
 // SM) and prefetch tile t + gridDim while they iterate on tile t, so the
 // 176 KB tile load overlaps the cycles instead of stalling them.
@@ -77,7 +78,12 @@ FSB_INLINE void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int
 
 constexpr int kNW = 16, kPY = 2, kEW = 64, kEH = kNW * kPY;
 constexpr int kStatePlanes = 12, kConstPlanes = 10;
-constexpr int kPlane = kEW * kEH;  // floats per plane in the staging tile
+// TMA needs the box's innermost start coordinate 16-byte aligned (measured on
+// this B200 / driver: x0 % 4 != 0 faults). The box is therefore 4 columns wider
+// than the 64-column tile and starts at floor4(ox); the kernel reads with the
+// resulting 0..3 column shift.
+constexpr int kBoxW = kEW + 4;
+constexpr int kPlane = kBoxW * kEH;  // floats per plane in the staging tile
 constexpr uint32_t kTileBytes = (kStatePlanes + kConstPlanes) * kPlane * sizeof(float);
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + kTileBytes +
                               2 * sizeof(f2) * kNW * 3 * 32 /*s_top, s_bot*/ + 64 /*mbarrier*/;
@@ -116,10 +122,11 @@ __global__ void __launch_bounds__(kNW * 32, 1)
   do {                                                                                    \
     if (threadIdx.x == 0) {                                                               \
       const int tx_ = (TILE) % ntx, ty_ = (TILE) / ntx;                                   \
+      const int bx_ = (tx_ * TW - R) & ~3; /* floor to a multiple of 4 */                 \
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");                        \
       mbar_expect_tx(bar, kTileBytes);                                                    \
-      tma_load_3d(st, &tm_src, tx_ * TW - R, ty_ * TH - R, 0, bar);                        \
-      tma_load_3d(st + kStatePlanes * kPlane, &tm_const, tx_ * TW - R, ty_ * TH - R, 0, bar); \
+      tma_load_3d(st, &tm_src, bx_, ty_ * TH - R, 0, bar);                                 \
+      tma_load_3d(st + kStatePlanes * kPlane, &tm_const, bx_, ty_ * TH - R, 0, bar);       \
     }                                                                                     \
   } while (0)
 
@@ -137,12 +144,13 @@ __global__ void __launch_bounds__(kNW * 32, 1)
     f2 exf[PY], eyf[PY];
     unsigned mbits = 0;  // mask of the two pixels of row j at bits 2j, 2j+1
     const f2 a1 = mk2(A.alpha1, A.alpha1);
+    const int shift = ox - (ox & ~3);  // staging column of tile column 0
 #pragma unroll
     for (int j = 0; j < PY; ++j) {
       const int r = r0 + j;
-      const int o = r * kEW + c0;
-      auto S2 = [&](int plane) { return *reinterpret_cast<const f2*>(st + plane * kPlane + o); };
-      auto C2 = [&](int plane) { return *reinterpret_cast<const f2*>(cs + plane * kPlane + o); };
+      const int o = r * kBoxW + c0 + shift;
+      auto S2 = [&](int plane) { return mk2(st[plane * kPlane + o], st[plane * kPlane + o + 1]); };
+      auto C2 = [&](int plane) { return mk2(cs[plane * kPlane + o], cs[plane * kPlane + o + 1]); };
       u[j] = S2(SU); v0[j] = S2(SV0); v1[j] = S2(SV1);
       p0[j] = S2(SP0); p1[j] = S2(SP1);
       q0[j] = S2(SQ0); q1[j] = S2(SQ1); q2[j] = S2(SQ2); q3[j] = S2(SQ3);
@@ -157,7 +165,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       // mask (0/1 floats; zero outside the image and past the tile edge)
       const f2 m = C2(CM);
       const float mr = c0 + 2 < kEW ? cs[CM * kPlane + o + 2] : 0.f;
-      const f2 md = r + 1 < EH ? *reinterpret_cast<const f2*>(cs + CM * kPlane + o + kEW)
+      const f2 md = r + 1 < EH ? mk2(cs[CM * kPlane + o + kBoxW], cs[CM * kPlane + o + kBoxW + 1])
                                : mk2(0.f, 0.f);
       exf[j] = mk2(m.x * m.y, m.y * mr);
       eyf[j] = mk2(m.x * md.x, m.y * md.y);
@@ -361,7 +369,7 @@ bool make_map(CUtensorMap* m, const float* base, int w, int h, int planes, size_
   if (!enc) return false;
   cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)planes};
   cuuint64_t strides[2] = {(cuuint64_t)w * sizeof(float), (cuuint64_t)n * sizeof(float)};
-  cuuint32_t box[3] = {(cuuint32_t)kEW, (cuuint32_t)kEH, (cuuint32_t)planes};
+  cuuint32_t box[3] = {(cuuint32_t)kBoxW, (cuuint32_t)kEH, (cuuint32_t)planes};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
