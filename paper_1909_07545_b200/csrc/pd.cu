@@ -373,6 +373,16 @@ int pack_level_internal(const fsb_level* L, cudaStream_t st) {
   return launch_status();
 }
 
+__global__ void k_mask_to_float(const uint8_t* __restrict__ m, size_t n, float* __restrict__ f) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) f[i] = m[i] ? 1.f : 0.f;
+}
+
+int mask_to_float_internal(const uint8_t* m, size_t n, float* f, cudaStream_t st) {
+  k_mask_to_float<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(m, n, f);
+  return launch_status();
+}
+
 int mean_finish_internal(const double* partials, int nparts, const uint8_t* mask, size_t n,
                          double* out, cudaStream_t st) {
   k_mean_finish<<<1, 256, 0, st>>>(partials, nparts, mask, n, out);

@@ -41,6 +41,7 @@ int warp_finish_internal(const fsb_level* L, const fsb_params* prm, float* dmax,
 size_t level_partials_internal(int h, int w);
 int warp_sample_internal(const fsb_level* L, cudaStream_t st);
 int pack_level_internal(const fsb_level* L, cudaStream_t st);
+int mask_to_float_internal(const uint8_t* m, size_t n, float* f, cudaStream_t st);
 int warp_prologue_internal(const fsb_level* L, cudaStream_t st);
 int mean_finish_internal(const double* partials, int nparts, const uint8_t* mask, size_t n,
                          double* out, cudaStream_t st);
@@ -325,6 +326,10 @@ int pd_iterate_blocked(const fsb_level* L, const fsb_params* prm, int iters, flo
   A.lam = (float)prm->lam; A.alpha0 = (float)prm->alpha0; A.alpha1 = (float)prm->alpha1;
   A.theta = (float)prm->theta; A.sigma_q = (float)(1.0 / (2.0 * prm->alpha0));
   A.du_max = (float)prm->du_max;
+  if (tma) {  // per-stage entry: the level setup has not filled maskf
+    int rc = mask_to_float_internal(L->mask, n, L->maskf, st);
+    if (rc) return rc;
+  }
   int cur = 0, done = 0;
   while (done < iters) {
     const int it = iters - done < halo ? iters - done : halo;
