@@ -317,7 +317,7 @@ def pd_roofline(eng, rig, prm, img0, iters=50):
     achieved = bytes_iter / t_iter / 1e9
     return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": None,
-            "kernel": "primal-dual iteration (fsb_pd_iterate: k_pd_dual + k_pd_primal)",
+            "kernel": "primal-dual iterations (fsb_pd_iterate -> k_pd_tma, 5 cycles per launch)",
             "algorithmic_bytes_per_launch": bytes_iter,
             "per_unit": f"{PD_BYTES_PER_PIXEL_ITER} B per pixel-iteration x {H}x{W} px",
             "us_per_launch": t_iter * 1e6, "peak_source": peak_src,
@@ -401,10 +401,11 @@ def run_b200(a) -> None:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         assert res.u.shape == (H, W)
         e2e = {"value": frames / float(te.item()), "unit": "frames/s",
-               "h2d_bytes_per_step": 2 * H * W * 4,
-               "d2h_bytes_per_step": H * W * (4 + 8 + 8 + 1 + 4),
+               "h2d_bytes_per_step": 2 * H * W * 8,
+               "d2h_bytes_per_step": H * W * (8 + 16 + 16 + 1 + 8),
                "api": "paper_1909_07545_b200.solve_pyramid (float64 host arrays in/out)",
-               "timer": "host wall clock incl. fp64<->fp32 host conversion"}
+               "timer": "host wall clock around the API call (pinned staging, "
+                        "fp64<->fp32 casts on the device)"}
 
     roof = pd_roofline(eng, rig, prm, img0) if rank == 0 else None
     cpu = None
