@@ -63,6 +63,11 @@ def workload(name: str, frame: int = 0):
                                                        rotvec=(0.002, 0.004, 0.001)))
         return (rig, SolverParams(warp_iters=10, pd_iters=10, pyramid_levels=5, min_width=40),
                 "C2: 640x480 Kannala-Brandt, N=10 x K=10, 5 levels (min_width 40)", 1)
+    if name == "c4":
+        from paper_1909_07545_b200.sequence import c4_rig
+        return (c4_rig(0), SolverParams(),
+                "C4: 256-frame sequence of C3-geometry frames (per-frame pose, reseeded scene), "
+                "partitioned in contiguous blocks across ranks; N=50 x K=10, 5 levels", 1)
     if name == "c5":
         cam = UnifiedCamera(width=2048, height=2048, fx=910.0, fy=910.0, cx=1023.5, cy=1023.5,
                             fov=math.pi, xi=0.9)
@@ -348,6 +353,79 @@ def pd_roofline(eng, rig, prm, img0, iters=50):
             "us_per_call_by_iters": model}
 
 
+def run_sequence(a) -> None:
+    """C4: each rank solves its contiguous block of the 256-frame sequence, one
+    frame per step (pose and scene differ per frame; no data-path collective)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1909_07545_b200 import _ext
+    from paper_1909_07545_b200 import synth as S
+    from paper_1909_07545_b200.sequence import c4_rig, max_over_ranks, partition
+    from paper_1909_07545_b200.solver import Solver
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    _, prm, desc, ss = workload("c4")
+    block = list(partition(256, world, rank))
+    K, Wm = a.steps, max(a.warmup, 0)
+    frames = [block[k % len(block)] for k in range(Wm + K)]
+    base = S.default_scene()
+    imgs = []
+    for i in frames:  # inputs rendered before timing, resident in HBM
+        rig = c4_rig(i)
+        sc = S.reseed_scene(base, i)
+        imgs.append((rig, S.render_device(sc, rig.cam0, supersample=ss)[0],
+                     S.render_device(sc, rig.cam1, pose=rig.pose, supersample=ss)[0]))
+    eng = Solver(imgs[0][0], prm)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(k):
+        rig, i0, i1 = imgs[k]
+        eng.rs = _ext.rig_struct(rig)  # per-frame pose; same shapes -> same workspace
+        eng.run(i0, i1)
+
+    for k in range(Wm):
+        step(k)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(K):
+            flush.zero_()
+            ev[k][0].record(stream)
+            step(Wm + k)
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_max = max_over_ranks(sum(s_.elapsed_time(e) for s_, e in ev) / 1e3, device="cuda")
+    fps = world * K / t_max
+    ppf = pixel_iters_per_frame(imgs[0][0], prm)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world, "steps": K,
+            "warmup": a.warmup, "ms_per_step": t_max * 1e3 / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (GPU ray-cast default_scene reseeded per frame, ss=1)",
+            "config": {"workload": desc, "frames_per_step_per_gpu": 1,
+                       "frames_per_rank": len(block), "pixel_iters_per_frame": ppf,
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "parallelism": f"frame-partitioned x{world}, no data-path collective"},
+            "mpix_iter_per_s": fps * ppf / 1e6, "e2e": None, "gpu_launches": None,
+            "roofline": None, "cpu_baseline": None, "clocks": clk.summary()}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_b200(a) -> None:
     import torch
     import torch.distributed as dist
@@ -468,7 +546,7 @@ def main(argv=None) -> int:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=["c3", "c1", "c2", "c5"], default="c3")
+    ap.add_argument("--workload", choices=["c3", "c1", "c2", "c4", "c5"], default="c3")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API e2e leg")
     ap.add_argument("--profile-pd", action="store_true",
@@ -476,6 +554,8 @@ def main(argv=None) -> int:
     a = ap.parse_args(argv)
     if a.impl == "reference":
         run_reference(a)
+    elif a.workload == "c4":
+        run_sequence(a)
     else:
         run_b200(a)
     return 0
