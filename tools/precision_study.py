@@ -1,0 +1,66 @@
+"""Where does fp32 lose parity at N=50? (diagnostic study, CPU, build container)
+
+Runs the pinned fp64 oracle on the reference acceptance pair (default_rig 400^2,
+N=50, K=10, du_max=0.1) with float32 rounding injected at chosen points and
+reports |du| statistics against the pure fp64 run.
+"""
+import sys
+from pathlib import Path
+from types import SimpleNamespace
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, "/root/reference/pkg/src")
+from oracle import fs_oracle as O  # noqa: E402
+
+f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
+
+
+def run(i0, i1, rig, prm, mode):
+    orig_cycle, orig_lin, orig_level = O.pd_cycle, O.linearize, O.level_solve
+
+    def cycle(s, *a, **k):
+        s = orig_cycle(s, *a, **k)
+        if "state" in mode:
+            s = O.PDState(*(f32(getattr(s, f)) for f in ("u", "v", "p", "q", "u_bar", "v_bar")))
+        return s
+
+    def lin(i0_, i1_, traj, tok, mask, w):
+        if "w" in mode:
+            w = f32(w)
+        out = orig_lin(i0_, i1_, traj, tok, mask, w)
+        if "gath" in mode:
+            i1w, wok, dirs, dok, iu, rho0 = out
+            out = (f32(i1w), wok, f32(dirs), dok, f32(iu), f32(rho0))
+        return out
+
+    O.pd_cycle, O.linearize = cycle, lin
+    try:
+        return O.pyramid_solve(i0, i1, rig, prm)
+    finally:
+        O.pd_cycle, O.linearize = orig_cycle, orig_lin
+
+
+def main():
+    from fisheyestereo import synth
+    rig = synth.default_rig()
+    sc = synth.default_scene()
+    i0 = f32(synth.render(sc, rig.cam0, supersample=2)[0])
+    i1 = f32(synth.render(sc, rig.cam1, pose=rig.pose, supersample=2)[0])
+    modes = sys.argv[1:] or ["", "state", "w", "gath", "state+w+gath"]
+    N = 50
+    prm = SimpleNamespace(lam=5.0, alpha0=17.0, alpha1=1.2, beta=9.0, eta=0.85, warp_iters=N,
+                          pd_iters=10, du_max=0.1, pyramid_levels=5, pyramid_scale=2.0,
+                          min_width=50, epsilon_scale=0.1, tensor_sigma=1.0, theta=1.0)
+    ref = run(i0, i1, rig, prm, "")
+    for m in modes[1:] if modes[0] == "" else modes:
+        s = run(i0, i1, rig, prm, m)
+        e = np.abs(s.u - ref.u)[ref.mask]
+        print(f"{m:14s} median {np.median(e):.2e} p99 {np.percentile(e, 99):.2e} "
+              f"max {e.max():.2e}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
