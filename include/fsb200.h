@@ -265,6 +265,17 @@ int fsb_solve_pyramid(const fsb_rig* rig, const fsb_params* prm, const float* i0
                       float* u, float* w, float* v, uint8_t* mask, float* i1c,
                       const fsb_diag* diag, void* stream);
 
+/* fp64 parity path of solve_pyramid: float64 images in, float64 fields out,
+ * float64 storage and IEEE arithmetic in the reference's operation order (one
+ * primal-dual cycle per launch). Matches the reference to round-off at any
+ * warp count; the fp32 fsb_solve_pyramid is the production path. */
+size_t fsb_solve_pyramid_f64_workspace_bytes(const fsb_rig* rig, const fsb_params* prm);
+int fsb_solve_pyramid_f64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
+                          const double* i1, const double* const* traj_dirs,
+                          const uint8_t* const* traj_ok, void* workspace, size_t workspace_bytes,
+                          double* u, double* w, double* v, uint8_t* mask, double* i1c,
+                          const fsb_diag* diag, void* stream);
+
 /* CUDA-graph form of fsb_solve_pyramid: captures one frame (same arguments,
  * fixed buffers) on `stream` into an executable graph; *n_kernels receives the
  * number of kernel nodes per frame. Replay with fsb_graph_launch. */

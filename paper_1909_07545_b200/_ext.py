@@ -30,7 +30,8 @@ EXPORTED = (
     "fsb_smooth_scratch_bytes", "fsb_pyramid_shapes", "fsb_downsample_area",
     "fsb_upsample_state", "fsb_compute_tensor", "fsb_precondition_steps", "fsb_level_partials", "fsb_level_setup", "fsb_warp_linearize",
     "fsb_pd_iterate", "fsb_thresholding_step", "fsb_warp_finish", "fsb_solve_level", "fsb_diag_counts",
-    "fsb_solve_pyramid_workspace_bytes", "fsb_solve_pyramid", "fsb_render", "fsb_graph_create", "fsb_graph_launch", "fsb_graph_destroy",
+    "fsb_solve_pyramid_workspace_bytes", "fsb_solve_pyramid",
+    "fsb_solve_pyramid_f64_workspace_bytes", "fsb_solve_pyramid_f64", "fsb_render", "fsb_graph_create", "fsb_graph_launch", "fsb_graph_destroy",
     "fsb_version",
 )
 
@@ -128,6 +129,9 @@ def lib() -> C.CDLL:
             "fsb_solve_pyramid_workspace_bytes": (sz, [P(FsbRig), P(FsbParams)]),
             "fsb_solve_pyramid": (C.c_int, [P(FsbRig), P(FsbParams), vp, vp, vp, vp, vp, sz,
                                             vp, vp, vp, vp, vp, P(FsbDiag), vp]),
+            "fsb_solve_pyramid_f64_workspace_bytes": (sz, [P(FsbRig), P(FsbParams)]),
+            "fsb_solve_pyramid_f64": (C.c_int, [P(FsbRig), P(FsbParams), vp, vp, vp, vp, vp, sz,
+                                                vp, vp, vp, vp, vp, P(FsbDiag), vp]),
             "fsb_render": (C.c_int, [P(FsbCamera), P(C.c_double), P(C.c_double), vp, i32, i32,
                                      vp, vp, vp, vp]),
             "fsb_graph_create": (C.c_int, [P(FsbRig), P(FsbParams), vp, vp, vp, vp, vp, sz, vp,

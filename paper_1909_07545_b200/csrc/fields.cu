@@ -103,20 +103,21 @@ __global__ void k_calibration_field(Cam c0, Cam c1, Rot R, const int* iters0,
 
 // calibrate_second_image (solver.py:389-398): i1c = bicubic(i1, x + cal, mask1),
 // ok = sample_ok & cal_ok, zero where invalid. f64 accumulation.
+template <typename TI, typename TO>
 __global__ void k_calibrate_image(Cam c0, Cam c1, Rot R, const int* iters0,
-                                  const float* __restrict__ i1, const uint8_t* __restrict__ mask1,
-                                  float* __restrict__ i1c, uint8_t* __restrict__ okout) {
+                                  const TI* __restrict__ i1, const uint8_t* __restrict__ mask1,
+                                  TO* __restrict__ i1c, uint8_t* __restrict__ okout) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= c0.width || y >= c0.height) return;
   double fx, fy;
   bool cal_ok = calib_flow(c0, c1, R, poly_iters_of(c0, iters0), x, y, fx, fy);
   double v[1];
-  bool s_ok = bicubic_sample<1, double>(i1, mask1, c1.height, c1.width, (double)x + fx,
-                                        (double)y + fy, v);
+  bool s_ok = bicubic_sample<1, double, TI>(i1, mask1, c1.height, c1.width, (double)x + fx,
+                                            (double)y + fy, v);
   bool ok = s_ok && cal_ok;
   size_t i = (size_t)y * c0.width + x;
-  i1c[i] = ok ? (float)v[0] : 0.f;
+  i1c[i] = ok ? (TO)v[0] : TO(0);
   okout[i] = ok;
 }
 
@@ -195,7 +196,8 @@ __global__ void k_traj_b(Cam c, Vec3 that, double depth, double eps_scale, TrajS
   if (__any_sync(0xffffffffu, degen) && (threadIdx.x & 31) == 0) atomicOr(s.flags + 1, 1);
 }
 
-__global__ void k_traj_c(int w, int h, TrajScratch s, float* __restrict__ dirs,
+template <typename TO>
+__global__ void k_traj_c(int w, int h, TrajScratch s, TO* __restrict__ dirs,
                          uint8_t* __restrict__ ok) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -216,8 +218,8 @@ __global__ void k_traj_c(int w, int h, TrajScratch s, float* __restrict__ dirs,
     good = good && !blocked;
     if (!good) { dx = 0.0; dy = 0.0; }
   }
-  dirs[2 * i] = (float)dx;
-  dirs[2 * i + 1] = (float)dy;
+  dirs[2 * i] = (TO)dx;
+  dirs[2 * i + 1] = (TO)dy;
   ok[i] = good;
 }
 
@@ -262,9 +264,10 @@ int poly_prepass_grid(const Cam& c, int* iters, cudaStream_t st) {
 
 size_t traj_scratch_bytes_internal(int w, int h) { return traj_bytes(w, h); }
 
-int trajectory_field_internal(const fsb_camera* cam, const double t[3], double eps_scale,
-                              double depth, float* dirs, uint8_t* ok, void* scratch,
-                              size_t scratch_bytes, cudaStream_t st) {
+template <typename TO>
+int trajectory_field_t(const fsb_camera* cam, const double t[3], double eps_scale, double depth,
+                       TO* dirs, uint8_t* ok, void* scratch, size_t scratch_bytes,
+                       cudaStream_t st) {
   if (!cam_ok(cam) || !dirs || !ok || !scratch || !t) return FSB_EINVAL;
   if (scratch_bytes < traj_bytes(cam->width, cam->height)) return FSB_ENOSPC;
   // fields.py:63-67: t_hat = t / ||t||, zero baseline is an error.
@@ -280,8 +283,21 @@ int trajectory_field_internal(const fsb_camera* cam, const double t[3], double e
   dim3 blk(kBX, kBY), grd = grid2d(c.width, c.height, blk);
   k_traj_a<<<grd, blk, 0, st>>>(c, th, depth, s);
   k_traj_b<<<grd, blk, 0, st>>>(c, th, depth, eps_scale, s);
-  k_traj_c<<<grd, blk, 0, st>>>(c.width, c.height, s, dirs, ok);
+  k_traj_c<TO><<<grd, blk, 0, st>>>(c.width, c.height, s, dirs, ok);
   return launch_status();
+}
+
+int trajectory_field_internal(const fsb_camera* cam, const double t[3], double eps_scale,
+                              double depth, float* dirs, uint8_t* ok, void* scratch,
+                              size_t scratch_bytes, cudaStream_t st) {
+  return trajectory_field_t<float>(cam, t, eps_scale, depth, dirs, ok, scratch, scratch_bytes, st);
+}
+
+int trajectory_field64_internal(const fsb_camera* cam, const double t[3], double eps_scale,
+                                double depth, double* dirs, uint8_t* ok, void* scratch,
+                                size_t scratch_bytes, cudaStream_t st) {
+  return trajectory_field_t<double>(cam, t, eps_scale, depth, dirs, ok, scratch, scratch_bytes,
+                                    st);
 }
 
 int fov_mask_internal(const fsb_camera* cam, uint8_t* mask, int* iters, cudaStream_t st) {
@@ -295,17 +311,28 @@ int fov_mask_internal(const fsb_camera* cam, uint8_t* mask, int* iters, cudaStre
 }
 
 // i1c/ok on the cam0 grid; mask1 must be the cam1 FOV mask; iters0 scratch int.
-int calibrate_internal(const fsb_rig* rig, const float* i1, const uint8_t* mask1, float* i1c,
-                       uint8_t* ok, int* iters0, cudaStream_t st) {
+template <typename TI, typename TO>
+int calibrate_t(const fsb_rig* rig, const TI* i1, const uint8_t* mask1, TO* i1c, uint8_t* ok,
+                int* iters0, cudaStream_t st) {
   Cam c0 = make_cam(rig->cam0), c1 = make_cam(rig->cam1);
   Rot R;
   for (int k = 0; k < 9; ++k) R.r[k] = rig->rotation[k];
   int rc = poly_prepass_grid(c0, iters0, st);
   if (rc) return rc;
   dim3 blk(kBX, kBY);
-  k_calibrate_image<<<grid2d(c0.width, c0.height, blk), blk, 0, st>>>(c0, c1, R, iters0, i1,
-                                                                      mask1, i1c, ok);
+  k_calibrate_image<TI, TO><<<grid2d(c0.width, c0.height, blk), blk, 0, st>>>(c0, c1, R, iters0,
+                                                                              i1, mask1, i1c, ok);
   return launch_status();
+}
+
+int calibrate_internal(const fsb_rig* rig, const float* i1, const uint8_t* mask1, float* i1c,
+                       uint8_t* ok, int* iters0, cudaStream_t st) {
+  return calibrate_t<float, float>(rig, i1, mask1, i1c, ok, iters0, st);
+}
+
+int calibrate64_internal(const fsb_rig* rig, const double* i1, const uint8_t* mask1, double* i1c,
+                         uint8_t* ok, int* iters0, cudaStream_t st) {
+  return calibrate_t<double, double>(rig, i1, mask1, i1c, ok, iters0, st);
 }
 
 }  // namespace fsb

@@ -189,21 +189,25 @@ FSB_INLINE bool split_pos(double x, double y, int h, int w, int& ix, int& iy, Ac
   return true;
 }
 
-template <int C, bool kGlobal = true>
-FSB_INLINE void load_tap(const float* __restrict__ f, int idx, float v[C]) {
+template <int C, bool kGlobal = true, typename TF = float>
+FSB_INLINE void load_tap(const TF* __restrict__ f, int idx, TF v[C]) {
   if constexpr (C == 1) {
     v[0] = kGlobal ? __ldg(f + idx) : f[idx];
-  } else {
+  } else if constexpr (sizeof(TF) == 4) {
     float2 t = kGlobal ? __ldg(reinterpret_cast<const float2*>(f) + idx)
                        : reinterpret_cast<const float2*>(f)[idx];
+    v[0] = t.x; v[1] = t.y;
+  } else {
+    double2 t = kGlobal ? __ldg(reinterpret_cast<const double2*>(f) + idx)
+                        : reinterpret_cast<const double2*>(f)[idx];
     v[0] = t.x; v[1] = t.y;
   }
 }
 
 // Evaluation given the 16 tap validities `okb` (bit 4a+b, a = dy+1 outer, b = dx+1
 // inner); taps are read only where valid. Returns false when no tap is valid.
-template <int C, typename Acc, bool kGlobal = true>
-FSB_INLINE bool bicubic_bits(const float* __restrict__ field, unsigned okb, int w, int ix, int iy,
+template <int C, typename Acc, bool kGlobal = true, typename TF = float>
+FSB_INLINE bool bicubic_bits(const TF* __restrict__ field, unsigned okb, int w, int ix, int iy,
                              Acc fx, Acc fy, Acc out[C]) {
   if (okb == 0) return false;
   if (okb == 0xFFFFu) {
@@ -217,8 +221,8 @@ FSB_INLINE bool bicubic_bits(const float* __restrict__ field, unsigned okb, int 
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        float vf[C];
-        load_tap<C, kGlobal>(field, (iy + a - 1) * w + (ix + b - 1), vf);
+        TF vf[C];
+        load_tap<C, kGlobal, TF>(field, (iy + a - 1) * w + (ix + b - 1), vf);
         const Acc wt = wy[a] * wx[b];
 #pragma unroll
         for (int k = 0; k < C; ++k) cub[k] += wt * (Acc)vf[k];
@@ -239,8 +243,8 @@ FSB_INLINE bool bicubic_bits(const float* __restrict__ field, unsigned okb, int 
 #pragma unroll
     for (int b = 1; b <= 2; ++b)
       if (okb >> (4 * a + b) & 1u) {
-        float vf[C];
-        load_tap<C, kGlobal>(field, (iy + a - 1) * w + (ix + b - 1), vf);
+        TF vf[C];
+        load_tap<C, kGlobal, TF>(field, (iy + a - 1) * w + (ix + b - 1), vf);
         const Acc bw = by[a - 1] * bx[b - 1];
 #pragma unroll
         for (int k = 0; k < C; ++k) bil[k] += bw * (Acc)vf[k];
@@ -263,8 +267,8 @@ FSB_INLINE bool bicubic_bits(const float* __restrict__ field, unsigned okb, int 
         const Acc d2 = ddx * ddx + ddy * ddy;
         if (d2 < nd2) { nd2 = d2; best = 4 * a + b; }
       }
-  float vf[C];
-  load_tap<C, kGlobal>(field, (iy + (best >> 2) - 1) * w + (ix + (best & 3) - 1), vf);
+  TF vf[C];
+  load_tap<C, kGlobal, TF>(field, (iy + (best >> 2) - 1) * w + (ix + (best & 3) - 1), vf);
 #pragma unroll
   for (int k = 0; k < C; ++k) out[k] = (Acc)vf[k];
   return true;
@@ -274,8 +278,8 @@ FSB_INLINE bool bicubic_bits(const float* __restrict__ field, unsigned okb, int 
 // The 16 tap validities are gathered first (bit 4a+b, scan order dy outer / dx
 // inner); the all-valid case is a plain Catmull-Rom sum, the fallbacks visit only
 // valid taps — identical sums to the reference, whose invalid taps add exact zeros.
-template <int C, typename Acc, bool kGlobal = true>
-FSB_INLINE bool bicubic_at(const float* __restrict__ field, const uint8_t* __restrict__ mask, int h,
+template <int C, typename Acc, bool kGlobal = true, typename TF = float>
+FSB_INLINE bool bicubic_at(const TF* __restrict__ field, const uint8_t* __restrict__ mask, int h,
                            int w, int ix, int iy, Acc fx, Acc fy, Acc out[C]) {
   unsigned okb = 0;
   const bool inner = ix >= 1 && ix + 2 < w && iy >= 1 && iy + 2 < h;
@@ -289,18 +293,18 @@ FSB_INLINE bool bicubic_at(const float* __restrict__ field, const uint8_t* __res
       const bool v = in && (kGlobal ? __ldg(mask + idx) : mask[idx]);
       okb |= (v ? 1u : 0u) << (4 * a + b);
     }
-  return bicubic_bits<C, Acc, kGlobal>(field, okb, w, ix, iy, fx, fy, out);
+  return bicubic_bits<C, Acc, kGlobal, TF>(field, okb, w, ix, iy, fx, fy, out);
 }
 
 // Full sample at a continuous position: returns validity, out untouched when
 // invalid.
-template <int C, typename Acc>
-FSB_INLINE bool bicubic_sample(const float* __restrict__ field, const uint8_t* __restrict__ mask,
+template <int C, typename Acc, typename TF = float>
+FSB_INLINE bool bicubic_sample(const TF* __restrict__ field, const uint8_t* __restrict__ mask,
                                int h, int w, double x, double y, Acc out[C]) {
   int ix, iy;
   Acc fx, fy;
   if (!split_pos<Acc>(x, y, h, w, ix, iy, fx, fy)) return false;
-  return bicubic_at<C, Acc>(field, mask, h, w, ix, iy, fx, fy, out);
+  return bicubic_at<C, Acc, true, TF>(field, mask, h, w, ix, iy, fx, fy, out);
 }
 
 // ---------------------------------------------------------------- reductions

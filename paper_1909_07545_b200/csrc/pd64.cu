@@ -1,0 +1,466 @@
+// fp64 parity path: the whole solve_pyramid frame in float64 storage and
+// arithmetic (compiled with -fmad=false, IEEE division / sqrt, the reference's
+// operation order), one primal-dual cycle per launch.
+//
+// The fp32 path (TMA-fed temporally blocked kernels) is the production path.
+// At the reference defaults (N=50 warps) the problem is at its conditioning
+// limit: ANY fp32 rounding moves the p99 disparity by ~2e-2 px against the
+// fp64 reference (profiles/r01_precision_study.txt). This path reproduces the
+// reference to round-off at every N, so parity can be shown at N=50 too.
+//
+// Reference: solver.py:306-452 (solve_level, solve_pyramid) with the stages of
+// solver.py:279-303 and :332-365; rasters.py:57-141 (bicubic).
+
+#include <string.h>
+
+#include "pd_math.cuh"
+
+namespace fsb {
+
+// defined in the other translation units
+int trajectory_field64_internal(const fsb_camera* cam, const double t[3], double eps_scale,
+                                double depth, double* dirs, uint8_t* ok, void* scratch,
+                                size_t scratch_bytes, cudaStream_t st);
+size_t traj_scratch_bytes_internal(int w, int h);
+int fov_mask_internal(const fsb_camera* cam, uint8_t* mask, int* iters, cudaStream_t st);
+int calibrate64_internal(const fsb_rig* rig, const double* i1, const uint8_t* mask1, double* i1c,
+                         uint8_t* ok, int* iters0, cudaStream_t st);
+int pyramid_shapes_internal(int h, int w, int levels, double scale, int min_width, int* shapes,
+                            int max_levels);
+int downsample64_internal(const double* src, const uint8_t* mask, int fh, int fw, double* dst,
+                          uint8_t* dmask, int ch, int cw, cudaStream_t st);
+int upsample64_internal(const double* u, const double* wv, const uint8_t* mask, int sh, int sw,
+                        const uint8_t* dmask, int dh, int dw, double* uo, double* wo,
+                        cudaStream_t st);
+size_t level_setup_scratch_internal(int h, int w);
+int level_setup64_internal(const double* i0, const uint8_t* mask, int h, int w,
+                           const fsb_params* prm, double* tensor, double* steps, void* scratch,
+                           size_t scratch_bytes, cudaStream_t st);
+int mean_finish_internal(const double* partials, int nparts, const uint8_t* mask, size_t n,
+                         double* out, cudaStream_t st);
+
+namespace {
+
+constexpr int kBX = 32, kBY = 8;
+constexpr int kMaxLevels = 32;
+
+struct L64 {
+  int h, w;
+  size_t n;
+  const double* i0; const double* i1; const uint8_t* mask;
+  const double* traj; const uint8_t* traj_ok;
+  double* T; double* S;
+  double* u; double* ub; double* v; double* vb; double* p; double* q;
+  double* wv; double* uo; double* iu; double* rho0; double* i1w; uint8_t* i1w_ok;
+  double* dirs; uint8_t* dir_ok;
+  double* partials;
+};
+
+__device__ __forceinline__ bool ex_at(const uint8_t* __restrict__ m, int w, int x, size_t i) {
+  return x + 1 < w && m[i] && m[i + 1];
+}
+__device__ __forceinline__ bool ey_at(const uint8_t* __restrict__ m, int h, int w, int y, size_t i) {
+  return y + 1 < h && m[i] && m[i + w];
+}
+
+// solver.py:332-337
+__global__ void k64_sample(L64 L) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= L.w || y >= L.h) return;
+  const size_t i = (size_t)y * L.w + x;
+  const double px = (double)x + L.wv[2 * i], py = (double)y + L.wv[2 * i + 1];
+  double iv[1], dr[2];
+  const bool wok = bicubic_sample<1, double, double>(L.i1, L.mask, L.h, L.w, px, py, iv);
+  bool dok = bicubic_sample<2, double, double>(L.traj, L.traj_ok, L.h, L.w, px, py, dr);
+  const bool mk = L.mask[i] != 0;
+  double d0 = 0.0, d1 = 0.0;
+  if (dok) {
+    const double nrm = sqrt(dr[0] * dr[0] + dr[1] * dr[1]);
+    if (nrm > 0.5 && mk) { d0 = dr[0] / fmax(nrm, 1e-300); d1 = dr[1] / fmax(nrm, 1e-300); }
+    else dok = false;
+  }
+  L.i1w[i] = wok ? iv[0] : 0.0;
+  L.i1w_ok[i] = wok && mk;
+  L.dirs[2 * i] = d0; L.dirs[2 * i + 1] = d1;
+  L.dir_ok[i] = dok;
+}
+
+// solver.py:339-346 with image_derivative_along 192-202
+__global__ void k64_linearize(L64 L) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= L.w || y >= L.h) return;
+  const size_t i = (size_t)y * L.w + x, n = L.n;
+  double ahead[1];
+  const bool ok = bicubic_sample<1, double, double>(L.i1w, L.i1w_ok, L.h, L.w,
+                                                    (double)x + L.dirs[2 * i],
+                                                    (double)y + L.dirs[2 * i + 1], ahead);
+  const double i1w = L.i1w[i];
+  const bool iu_ok = ok && L.i1w_ok[i];
+  const bool data_ok = iu_ok && L.dir_ok[i];
+  L.iu[i] = data_ok ? ahead[0] - i1w : 0.0;
+  L.rho0[i] = data_ok ? i1w - L.i0[i] : 0.0;
+  const double u = L.u[i];
+  L.uo[i] = u;
+  L.ub[i] = u;
+  L.vb[i] = L.v[i];
+  L.vb[n + i] = L.v[n + i];
+}
+
+// solver.py:290-293
+template <bool kDiag>
+__global__ void k64_dual(L64 L, double alpha0, double alpha1, float* dp, float* dq) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+  double pn = 0.0, qn = 0.0;
+  if (x < L.w && y < L.h) {
+    const size_t i = (size_t)y * L.w + x, n = L.n;
+    const bool ex = ex_at(L.mask, L.w, x, i), ey = ey_at(L.mask, L.h, L.w, y, i);
+    const double ub = L.ub[i], vb0 = L.vb[i], vb1 = L.vb[n + i];
+    double gx = 0.0, gy = 0.0, g00 = 0.0, g01 = 0.0, g10 = 0.0, g11 = 0.0;
+    if (ex) { gx = L.ub[i + 1] - ub; g00 = L.vb[i + 1] - vb0; g10 = L.vb[n + i + 1] - vb1; }
+    if (ey) { gy = L.ub[i + L.w] - ub; g01 = L.vb[i + L.w] - vb0; g11 = L.vb[n + i + L.w] - vb1; }
+    double p0 = L.p[i], p1 = L.p[n + i];
+    double q0 = L.q[i], q1 = L.q[n + i], q2 = L.q[2 * n + i], q3 = L.q[3 * n + i];
+    dual_update_exact<double>(L.T[i], L.T[n + i], L.T[2 * n + i], L.S[i] * alpha1,
+                              (1.0 / (2.0 * alpha0)) * alpha0, gx, gy, g00, g01, g10, g11, vb0,
+                              vb1, p0, p1, q0, q1, q2, q3);
+    L.p[i] = p0; L.p[n + i] = p1;
+    L.q[i] = q0; L.q[n + i] = q1; L.q[2 * n + i] = q2; L.q[3 * n + i] = q3;
+    if (kDiag) {
+      pn = sqrt(p0 * p0 + p1 * p1);
+      qn = sqrt(((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3);
+    }
+  }
+  if (kDiag) {
+    pn = warp_max(pn); qn = warp_max(qn);
+    if ((threadIdx.x & 31) == 0) {
+      atomic_max_nonneg(dp, (float)pn);
+      atomic_max_nonneg(dq, (float)qn);
+    }
+  }
+}
+
+__device__ __forceinline__ FluxT<double> flux64(const L64& L, size_t i, int x, int y) {
+  const size_t n = L.n;
+  const bool ex = ex_at(L.mask, L.w, x, i), ey = ey_at(L.mask, L.h, L.w, y, i);
+  return make_flux_exact<double>(L.T[i], L.T[n + i], L.T[2 * n + i], ex, ey, L.p[i], L.p[n + i],
+                                 L.q[i], L.q[n + i], L.q[2 * n + i], L.q[3 * n + i]);
+}
+
+// solver.py:295-303
+__global__ void k64_primal(L64 L, double lam, double alpha0, double alpha1, double theta) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= L.w || y >= L.h) return;
+  const size_t i = (size_t)y * L.w + x, n = L.n;
+  const FluxT<double> z = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const FluxT<double> f = flux64(L, i, x, y);
+  const FluxT<double> fl = x > 0 ? flux64(L, i - 1, x - 1, y) : z;
+  const FluxT<double> fu = y > 0 ? flux64(L, i - L.w, x, y - 1) : z;
+  const double dv = ((f.px - fl.px) + f.py) - fu.py;
+  const double d0 = ((f.q0x - fl.q0x) + f.q0y) - fu.q0y;
+  const double d1 = ((f.q1x - fl.q1x) + f.q1y) - fu.q1y;
+  double u = L.u[i], v0 = L.v[i], v1 = L.v[n + i], ub, vb0, vb1;
+  primal_update_exact<double>(dv, d0, d1, L.S[n + i], L.S[2 * n + i], L.iu[i], L.rho0[i], L.uo[i],
+                              L.p[i], L.p[n + i], lam, alpha0, alpha1, theta, u, v0, v1, ub, vb0,
+                              vb1);
+  L.u[i] = u; L.v[i] = v0; L.v[n + i] = v1;
+  L.ub[i] = ub; L.vb[i] = vb0; L.vb[n + i] = vb1;
+}
+
+// solver.py:356-365
+template <bool kDiag>
+__global__ void k64_finish(L64 L, double du_max, float* dmax) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+  double adu = 0.0;
+  if (x < L.w && y < L.h) {
+    const size_t i = (size_t)y * L.w + x;
+    const double uo = L.uo[i];
+    double du = fmin(fmax(L.u[i] - uo, -du_max), du_max);
+    if (!L.mask[i]) du = 0.0;
+    const double u = uo + du;
+    L.u[i] = u;
+    L.ub[i] = u;
+    L.wv[2 * i] = L.wv[2 * i] + du * L.dirs[2 * i];
+    L.wv[2 * i + 1] = L.wv[2 * i + 1] + du * L.dirs[2 * i + 1];
+    adu = fabs(du);
+  }
+  if (kDiag) {
+    __shared__ double ssum[8];
+    __shared__ double smax[8];
+    const double mx = warp_max(adu), sm = warp_sum(adu);
+    const int lane = threadIdx.x & 31, wid = (threadIdx.y * blockDim.x + threadIdx.x) >> 5;
+    if (lane == 0) { ssum[wid] = sm; smax[wid] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+      double t = 0.0, m = 0.0;
+      const int nw = (blockDim.x * blockDim.y) >> 5;
+      for (int k = 0; k < nw; ++k) { t += ssum[k]; m = fmax(m, smax[k]); }
+      L.partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+      atomic_max_nonneg(dmax, (float)m);
+    }
+  }
+}
+
+__global__ void k64_and_mask(const uint8_t* a, const uint8_t* b, size_t n, uint8_t* o) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) o[i] = a[i] && b[i];
+}
+
+// interleave two planes of v into (H, W, 2)
+__global__ void k64_interleave(const double* v, size_t n, double* out) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) { out[2 * i] = v[i]; out[2 * i + 1] = v[n + i]; }
+}
+
+struct Carve {
+  char* base;
+  size_t off = 0;
+  template <typename X>
+  X* take(size_t count) {
+    size_t bytes = align_up(count * sizeof(X));
+    X* p = base ? reinterpret_cast<X*>(base + off) : nullptr;
+    off += bytes;
+    return p;
+  }
+};
+
+struct Plan64 {
+  int nlev, shapes[2 * kMaxLevels];
+  size_t n0;
+  uint8_t *mask0, *mask1, *i1c_ok, *solve_mask;
+  int* iters;
+  double *lvl_i0[kMaxLevels], *lvl_i1[kMaxLevels], *traj[kMaxLevels];
+  uint8_t *lvl_mask[kMaxLevels], *traj_ok[kMaxLevels];
+  void* traj_scratch; size_t traj_bytes;
+  void* setup_scratch; size_t setup_bytes;
+  double *T, *S, *u[2], *wv[2], *ub, *v, *vb, *p, *q, *uo, *iu, *rho0, *i1w, *dirs, *partials;
+  uint8_t *i1w_ok, *dir_ok;
+  size_t bytes;
+};
+
+size_t partial_count(int h, int w) {
+  return (size_t)((w + kBX - 1) / kBX) * ((h + kBY - 1) / kBY) + 64;
+}
+
+int plan64(const fsb_rig* rig, const fsb_params* prm, void* base, Plan64& P) {
+  const int H = rig->cam0.height, W = rig->cam0.width;
+  int n = pyramid_shapes_internal(H, W, prm->pyramid_levels, prm->pyramid_scale, prm->min_width,
+                                  P.shapes, kMaxLevels);
+  if (n < 1 || n > kMaxLevels) return FSB_EINVAL;
+  P.nlev = n;
+  P.n0 = (size_t)H * W;
+  const size_t n0 = P.n0, n1 = (size_t)rig->cam1.height * rig->cam1.width;
+  Carve c{static_cast<char*>(base)};
+  P.mask0 = c.take<uint8_t>(n0); P.mask1 = c.take<uint8_t>(n1);
+  P.i1c_ok = c.take<uint8_t>(n0); P.solve_mask = c.take<uint8_t>(n0);
+  P.iters = c.take<int>(64);
+  for (int l = 0; l < n; ++l) {
+    size_t np = (size_t)P.shapes[2 * l] * P.shapes[2 * l + 1];
+    P.lvl_i0[l] = l == 0 ? nullptr : c.take<double>(np);
+    P.lvl_i1[l] = l == 0 ? nullptr : c.take<double>(np);
+    P.lvl_mask[l] = l == 0 ? nullptr : c.take<uint8_t>(np);
+    P.traj[l] = c.take<double>(2 * np);
+    P.traj_ok[l] = c.take<uint8_t>(np);
+  }
+  P.traj_bytes = traj_scratch_bytes_internal(W, H);
+  P.traj_scratch = c.take<char>(P.traj_bytes);
+  P.setup_bytes = level_setup_scratch_internal(H, W);
+  P.setup_scratch = c.take<char>(P.setup_bytes);
+  P.T = c.take<double>(3 * n0); P.S = c.take<double>(3 * n0);
+  for (int k = 0; k < 2; ++k) { P.u[k] = c.take<double>(n0); P.wv[k] = c.take<double>(2 * n0); }
+  P.ub = c.take<double>(n0); P.v = c.take<double>(2 * n0); P.vb = c.take<double>(2 * n0);
+  P.p = c.take<double>(2 * n0); P.q = c.take<double>(4 * n0);
+  P.uo = c.take<double>(n0); P.iu = c.take<double>(n0); P.rho0 = c.take<double>(n0);
+  P.i1w = c.take<double>(n0); P.dirs = c.take<double>(2 * n0);
+  P.i1w_ok = c.take<uint8_t>(n0); P.dir_ok = c.take<uint8_t>(n0);
+  P.partials = c.take<double>(partial_count(H, W));
+  P.bytes = c.off;
+  return FSB_OK;
+}
+
+fsb_camera scaled(const fsb_camera& c, int h, int w) {  // camera.py:66-77
+  fsb_camera o = c;
+  double sx = (double)w / (double)c.width, sy = (double)h / (double)c.height;
+  o.width = w; o.height = h;
+  o.fx = c.fx * sx; o.fy = c.fy * sy;
+  o.cx = (c.cx + 0.5) * sx - 0.5;
+  o.cy = (c.cy + 0.5) * sy - 0.5;
+  return o;
+}
+
+int solve_level64(const L64& L, const fsb_params* prm, const fsb_diag* diag, int64_t pd_off,
+                  int64_t warp_off, void* scratch, size_t scratch_bytes, cudaStream_t st) {
+  const size_t n = L.n;
+  int rc = level_setup64_internal(L.i0, L.mask, L.h, L.w, prm, L.T, L.S, scratch, scratch_bytes,
+                                  st);
+  if (rc) return rc;
+  cudaMemsetAsync(L.v, 0, 2 * n * sizeof(double), st);
+  cudaMemsetAsync(L.vb, 0, 2 * n * sizeof(double), st);
+  cudaMemsetAsync(L.p, 0, 2 * n * sizeof(double), st);
+  cudaMemsetAsync(L.q, 0, 4 * n * sizeof(double), st);
+  cudaMemcpyAsync(L.ub, L.u, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  const int N = prm->warp_iters, K = prm->pd_iters;
+  dim3 blk(kBX, kBY), grd = grid2d(L.w, L.h, blk);
+  const bool dpq = diag && diag->max_p_norm && diag->max_q_norm;
+  const bool ddu = diag && diag->max_du && diag->mean_abs_du;
+  for (int wi = 0; wi < N; ++wi) {
+    k64_sample<<<grd, blk, 0, st>>>(L);
+    k64_linearize<<<grd, blk, 0, st>>>(L);
+    for (int k = 0; k < K; ++k) {
+      if (dpq) {
+        const int64_t slot = pd_off + (int64_t)wi * K + k;
+        k64_dual<true><<<grd, blk, 0, st>>>(L, prm->alpha0, prm->alpha1,
+                                            diag->max_p_norm + slot, diag->max_q_norm + slot);
+      } else {
+        k64_dual<false><<<grd, blk, 0, st>>>(L, prm->alpha0, prm->alpha1, nullptr, nullptr);
+      }
+      k64_primal<<<grd, blk, 0, st>>>(L, prm->lam, prm->alpha0, prm->alpha1, prm->theta);
+    }
+    if (ddu) {
+      k64_finish<true><<<grd, blk, 0, st>>>(L, prm->du_max, diag->max_du + warp_off + wi);
+      rc = mean_finish_internal(L.partials, (int)(grd.x * grd.y), L.mask, n,
+                                diag->mean_abs_du + warp_off + wi, st);
+      if (rc) return rc;
+    } else {
+      k64_finish<false><<<grd, blk, 0, st>>>(L, prm->du_max, nullptr);
+    }
+  }
+  return launch_status();
+}
+
+bool params_ok64(const fsb_params* p) {
+  if (!p) return false;
+  if (!(p->lam > 0 && p->alpha0 > 0 && p->alpha1 > 0 && p->beta > 0 && p->eta > 0)) return false;
+  if (!(p->du_max > 0) || p->warp_iters < 1 || p->pd_iters < 1) return false;
+  return p->pyramid_levels >= 1 && p->pyramid_scale > 1.0;
+}
+
+}  // namespace
+
+size_t solve_pyramid64_bytes(const fsb_rig* rig, const fsb_params* prm) {
+  if (!rig || !params_ok64(prm)) return 0;
+  Plan64 P;
+  if (plan64(rig, prm, nullptr, P)) return 0;
+  return P.bytes;
+}
+
+int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0, const double* i1,
+                    const double* const* traj_dirs, const uint8_t* const* traj_okv, void* ws,
+                    size_t ws_bytes, double* u_out, double* w_out, double* v_out,
+                    uint8_t* mask_out, double* i1c, const fsb_diag* diag, cudaStream_t st) {
+  if (!rig || !params_ok64(prm) || !i0 || !i1 || !ws || !u_out || !w_out || !v_out ||
+      !mask_out || !i1c)
+    return FSB_EINVAL;
+  if ((traj_dirs == nullptr) != (traj_okv == nullptr)) return FSB_EINVAL;
+  Plan64 P;
+  int rc = plan64(rig, prm, nullptr, P);
+  if (rc) return rc;
+  if (ws_bytes < P.bytes) return FSB_ENOSPC;
+  plan64(rig, prm, ws, P);
+  const fsb_rig& r = *rig;
+  double t_res[3];
+  for (int k = 0; k < 3; ++k)  // translation_only_rig (fields.py:159-167)
+    t_res[k] = (r.rotation[0 * 3 + k] * r.translation[0] + r.rotation[1 * 3 + k] * r.translation[1]) +
+               r.rotation[2 * 3 + k] * r.translation[2];
+  if (!traj_dirs && t_res[0] == 0.0 && t_res[1] == 0.0 && t_res[2] == 0.0) return FSB_EDOMAIN;
+  const size_t n0 = P.n0;
+  const int N = prm->warp_iters, K = prm->pd_iters;
+  if (diag) {
+    const int64_t npd = (int64_t)P.nlev * N * K, nw = (int64_t)P.nlev * N;
+    if (diag->max_p_norm) cudaMemsetAsync(diag->max_p_norm, 0, npd * sizeof(float), st);
+    if (diag->max_q_norm) cudaMemsetAsync(diag->max_q_norm, 0, npd * sizeof(float), st);
+    if (diag->max_du) cudaMemsetAsync(diag->max_du, 0, nw * sizeof(float), st);
+  }
+  rc = fov_mask_internal(&r.cam0, P.mask0, P.iters + 0, st);
+  if (rc) return rc;
+  rc = fov_mask_internal(&r.cam1, P.mask1, P.iters + 1, st);
+  if (rc) return rc;
+  rc = calibrate64_internal(rig, i1, P.mask1, i1c, P.i1c_ok, P.iters + 2, st);
+  if (rc) return rc;
+  k64_and_mask<<<(unsigned)((n0 + 255) / 256), 256, 0, st>>>(P.mask0, P.i1c_ok, n0, P.solve_mask);
+  P.lvl_i0[0] = const_cast<double*>(i0);
+  P.lvl_i1[0] = i1c;
+  P.lvl_mask[0] = P.solve_mask;
+  for (int l = 1; l < P.nlev; ++l) {
+    const int fh = P.shapes[2 * (l - 1)], fw = P.shapes[2 * (l - 1) + 1];
+    const int ch = P.shapes[2 * l], cw = P.shapes[2 * l + 1];
+    rc = downsample64_internal(P.lvl_i0[l - 1], P.lvl_mask[l - 1], fh, fw, P.lvl_i0[l],
+                               P.lvl_mask[l], ch, cw, st);
+    if (rc) return rc;
+    rc = downsample64_internal(P.lvl_i1[l - 1], P.lvl_mask[l - 1], fh, fw, P.lvl_i1[l],
+                               P.lvl_mask[l], ch, cw, st);
+    if (rc) return rc;
+  }
+  int64_t pd_off = 0, warp_off = 0;
+  int cur = 0, prev_h = 0, prev_w = 0;
+  const uint8_t* prev_mask = nullptr;
+  for (int k = 0; k < P.nlev; ++k) {
+    const int l = P.nlev - 1 - k;
+    const int h = P.shapes[2 * l], w = P.shapes[2 * l + 1];
+    const size_t np = (size_t)h * w;
+    const double* traj;
+    const uint8_t* tok;
+    if (traj_dirs) {
+      traj = traj_dirs[k];
+      tok = traj_okv[k];
+    } else {
+      fsb_camera cl = scaled(r.cam0, h, w);
+      rc = trajectory_field64_internal(&cl, t_res, prm->epsilon_scale, 1.0, P.traj[l],
+                                       P.traj_ok[l], P.traj_scratch, P.traj_bytes, st);
+      if (rc) return rc;
+      traj = P.traj[l];
+      tok = P.traj_ok[l];
+    }
+    double* u = P.u[cur];
+    double* wv = P.wv[cur];
+    if (k == 0) {
+      cudaMemsetAsync(u, 0, np * sizeof(double), st);
+      cudaMemsetAsync(wv, 0, 2 * np * sizeof(double), st);
+    } else {
+      rc = upsample64_internal(P.u[cur ^ 1], P.wv[cur ^ 1], prev_mask, prev_h, prev_w,
+                               P.lvl_mask[l], h, w, u, wv, st);
+      if (rc) return rc;
+    }
+    L64 L;
+    L.h = h; L.w = w; L.n = np;
+    L.i0 = P.lvl_i0[l]; L.i1 = P.lvl_i1[l]; L.mask = P.lvl_mask[l];
+    L.traj = traj; L.traj_ok = tok;
+    L.T = P.T; L.S = P.S;
+    L.u = u; L.ub = P.ub; L.v = P.v; L.vb = P.vb; L.p = P.p; L.q = P.q;
+    L.wv = wv; L.uo = P.uo; L.iu = P.iu; L.rho0 = P.rho0; L.i1w = P.i1w; L.i1w_ok = P.i1w_ok;
+    L.dirs = P.dirs; L.dir_ok = P.dir_ok; L.partials = P.partials;
+    rc = solve_level64(L, prm, diag, pd_off, warp_off, P.setup_scratch, P.setup_bytes, st);
+    if (rc) return rc;
+    pd_off += (int64_t)N * K;
+    warp_off += N;
+    prev_h = h; prev_w = w; prev_mask = P.lvl_mask[l];
+    if (l == 0) {
+      cudaMemcpyAsync(u_out, u, n0 * sizeof(double), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(w_out, wv, 2 * n0 * sizeof(double), cudaMemcpyDeviceToDevice, st);
+      k64_interleave<<<(unsigned)((n0 + 255) / 256), 256, 0, st>>>(P.v, n0, v_out);
+      cudaMemcpyAsync(mask_out, P.solve_mask, n0, cudaMemcpyDeviceToDevice, st);
+    }
+    cur ^= 1;
+  }
+  return launch_status();
+}
+
+}  // namespace fsb
+
+using namespace fsb;
+
+extern "C" {
+
+size_t fsb_solve_pyramid_f64_workspace_bytes(const fsb_rig* rig, const fsb_params* prm) {
+  return solve_pyramid64_bytes(rig, prm);
+}
+
+int fsb_solve_pyramid_f64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
+                          const double* i1, const double* const* traj_dirs,
+                          const uint8_t* const* traj_ok, void* workspace, size_t workspace_bytes,
+                          double* u, double* w, double* v, uint8_t* mask, double* i1c,
+                          const fsb_diag* diag, void* stream) {
+  return solve_pyramid64(rig, prm, i0, i1, traj_dirs, traj_ok, workspace, workspace_bytes, u, w,
+                         v, mask, i1c, diag, as_stream(stream));
+}
+
+}  // extern "C"

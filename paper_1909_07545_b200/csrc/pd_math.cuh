@@ -88,3 +88,66 @@ FSB_INLINE void primal_update(float div_tp, float div_q0, float div_q1, float ta
 }
 
 }  // namespace fsb
+
+namespace fsb {
+
+// ---------------------------------------------------------------- exact variants
+// The same cycle with IEEE division / square root throughout, for the fp64
+// parity path (the reference's own operation order, solver.py:290-302).
+
+template <typename T>
+FSB_INLINE void dual_update_exact(T a, T b, T c, T sp, T sq, T gx, T gy, T g00, T g01, T g10,
+                                  T g11, T vb0, T vb1, T& p0, T& p1, T& q0, T& q1, T& q2,
+                                  T& q3) {
+  p0 = p0 + sp * ((a * gx + b * gy) - vb0);
+  p1 = p1 + sp * ((b * gx + c * gy) - vb1);
+  const T pd = fmax(T(1), sqrt(p0 * p0 + p1 * p1));
+  p0 = p0 / pd;
+  p1 = p1 / pd;
+  q0 = q0 + sq * g00;
+  q1 = q1 + sq * g01;
+  q2 = q2 + sq * g10;
+  q3 = q3 + sq * g11;
+  const T qd = fmax(T(1), sqrt(((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3));
+  q0 = q0 / qd;
+  q1 = q1 / qd;
+  q2 = q2 / qd;
+  q3 = q3 / qd;
+}
+
+template <typename T>
+struct FluxT {
+  T px, py, q0x, q0y, q1x, q1y;
+};
+
+template <typename T>
+FSB_INLINE FluxT<T> make_flux_exact(T a, T b, T c, bool ex, bool ey, T p0, T p1, T q0, T q1,
+                                    T q2, T q3) {
+  FluxT<T> f;
+  f.px = ex ? a * p0 + b * p1 : T(0);
+  f.py = ey ? b * p0 + c * p1 : T(0);
+  f.q0x = ex ? q0 : T(0);
+  f.q0y = ey ? q1 : T(0);
+  f.q1x = ex ? q2 : T(0);
+  f.q1y = ey ? q3 : T(0);
+  return f;
+}
+
+template <typename T>
+FSB_INLINE void primal_update_exact(T div_tp, T div_q0, T div_q1, T tau_u, T tau_v, T iu, T rho0,
+                                    T u_omega, T p0, T p1, T lam, T alpha0, T alpha1, T theta,
+                                    T& u, T& v0, T& v1, T& u_bar, T& v_bar0, T& v_bar1) {
+  const T u_hat = u + (tau_u * alpha1) * div_tp;
+  const T rho_hat = rho0 + (u_hat - u_omega) * iu;
+  const T u_new = shrink_step<T>(u_hat, rho_hat, iu, tau_u, lam);
+  const T v0n = v0 + tau_v * (alpha0 * div_q0 + alpha1 * p0);
+  const T v1n = v1 + tau_v * (alpha0 * div_q1 + alpha1 * p1);
+  u_bar = u_new + theta * (u_new - u);
+  v_bar0 = v0n + theta * (v0n - v0);
+  v_bar1 = v1n + theta * (v1n - v1);
+  u = u_new;
+  v0 = v0n;
+  v1 = v1n;
+}
+
+}  // namespace fsb

@@ -73,8 +73,9 @@ __global__ void k_divergence(const float* __restrict__ p, const uint8_t* __restr
 
 // downsample_area (rasters.py:224-260): fine pixels binned by (i*nc)//nf,
 // summed in fine raster order (np.bincount), mask from the nearest fine sample.
-__global__ void k_downsample(const float* __restrict__ src, const uint8_t* __restrict__ mask,
-                             int fh, int fw, float* __restrict__ dst, uint8_t* __restrict__ dmask,
+template <typename T>
+__global__ void k_downsample(const T* __restrict__ src, const uint8_t* __restrict__ mask,
+                             int fh, int fw, T* __restrict__ dst, uint8_t* __restrict__ dmask,
                              int ch, int cw) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   int i = blockIdx.y * blockDim.y + threadIdx.y;
@@ -96,27 +97,28 @@ __global__ void k_downsample(const float* __restrict__ src, const uint8_t* __res
   cc = min(max(cc, 0), fw - 1);
   bool cm = mask[(size_t)rr * fw + cc] && cnt > 0.0;
   size_t o = (size_t)i * cw + j;
-  dst[o] = cm ? (float)avg : 0.f;
+  dst[o] = cm ? (T)avg : T(0);
   dmask[o] = cm;
 }
 
 // upsample_state (rasters.py:276-297), f64 taps/accumulation.
-__global__ void k_upsample(const float* __restrict__ u, const float* __restrict__ wv,
+template <typename T>
+__global__ void k_upsample(const T* __restrict__ u, const T* __restrict__ wv,
                            const uint8_t* __restrict__ mask, int sh, int sw,
                            const uint8_t* __restrict__ dmask, int dh, int dw, double sx, double sy,
-                           float* __restrict__ uo, float* __restrict__ wo) {
+                           T* __restrict__ uo, T* __restrict__ wo) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= dw || y >= dh) return;
   double px = (x + 0.5) / sx - 0.5, py = (y + 0.5) / sy - 0.5;
   double us[1], ws[2];
-  bool ok = bicubic_sample<1, double>(u, mask, sh, sw, px, py, us);
-  ok = bicubic_sample<2, double>(wv, mask, sh, sw, px, py, ws) && ok;
+  bool ok = bicubic_sample<1, double, T>(u, mask, sh, sw, px, py, us);
+  ok = bicubic_sample<2, double, T>(wv, mask, sh, sw, px, py, ws) && ok;
   size_t i = (size_t)y * dw + x;
   bool keep = ok && dmask[i];
-  uo[i] = (float)((keep ? us[0] : 0.0) * (0.5 * (sx + sy)));
-  wo[2 * i] = (float)((keep ? ws[0] : 0.0) * sx);
-  wo[2 * i + 1] = (float)((keep ? ws[1] : 0.0) * sy);
+  uo[i] = (T)((keep ? us[0] : 0.0) * (0.5 * (sx + sy)));
+  wo[2 * i] = (T)((keep ? ws[0] : 0.0) * sx);
+  wo[2 * i + 1] = (T)((keep ? ws[1] : 0.0) * sy);
 }
 
 }  // namespace
@@ -138,20 +140,40 @@ int pyramid_shapes_internal(int h, int w, int levels, double scale, int min_widt
   return n;
 }
 
-int downsample_internal(const float* src, const uint8_t* mask, int fh, int fw, float* dst,
-                        uint8_t* dmask, int ch, int cw, cudaStream_t st) {
+template <typename T>
+int downsample_t(const T* src, const uint8_t* mask, int fh, int fw, T* dst, uint8_t* dmask, int ch,
+                 int cw, cudaStream_t st) {
   dim3 blk(kBX, kBY);
-  k_downsample<<<grid2d(cw, ch, blk), blk, 0, st>>>(src, mask, fh, fw, dst, dmask, ch, cw);
+  k_downsample<T><<<grid2d(cw, ch, blk), blk, 0, st>>>(src, mask, fh, fw, dst, dmask, ch, cw);
   return launch_status();
 }
 
-int upsample_internal(const float* u, const float* wv, const uint8_t* mask, int sh, int sw,
-                      const uint8_t* dmask, int dh, int dw, float* uo, float* wo, cudaStream_t st) {
+template <typename T>
+int upsample_t(const T* u, const T* wv, const uint8_t* mask, int sh, int sw, const uint8_t* dmask,
+               int dh, int dw, T* uo, T* wo, cudaStream_t st) {
   double sx = (double)dw / (double)sw, sy = (double)dh / (double)sh;
   dim3 blk(kBX, kBY);
-  k_upsample<<<grid2d(dw, dh, blk), blk, 0, st>>>(u, wv, mask, sh, sw, dmask, dh, dw, sx, sy, uo,
-                                                  wo);
+  k_upsample<T><<<grid2d(dw, dh, blk), blk, 0, st>>>(u, wv, mask, sh, sw, dmask, dh, dw, sx, sy,
+                                                     uo, wo);
   return launch_status();
+}
+
+int downsample_internal(const float* src, const uint8_t* mask, int fh, int fw, float* dst,
+                        uint8_t* dmask, int ch, int cw, cudaStream_t st) {
+  return downsample_t<float>(src, mask, fh, fw, dst, dmask, ch, cw, st);
+}
+int downsample64_internal(const double* src, const uint8_t* mask, int fh, int fw, double* dst,
+                          uint8_t* dmask, int ch, int cw, cudaStream_t st) {
+  return downsample_t<double>(src, mask, fh, fw, dst, dmask, ch, cw, st);
+}
+int upsample_internal(const float* u, const float* wv, const uint8_t* mask, int sh, int sw,
+                      const uint8_t* dmask, int dh, int dw, float* uo, float* wo, cudaStream_t st) {
+  return upsample_t<float>(u, wv, mask, sh, sw, dmask, dh, dw, uo, wo, st);
+}
+int upsample64_internal(const double* u, const double* wv, const uint8_t* mask, int sh, int sw,
+                        const uint8_t* dmask, int dh, int dw, double* uo, double* wo,
+                        cudaStream_t st) {
+  return upsample_t<double>(u, wv, mask, sh, sw, dmask, dh, dw, uo, wo, st);
 }
 
 }  // namespace fsb

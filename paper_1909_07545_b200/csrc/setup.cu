@@ -70,7 +70,8 @@ __device__ __forceinline__ int reflect_idx(int i, int n) {
 }
 
 // axis-0 pass on (f*m, m): out[2*i] = num, out[2*i+1] = den
-__global__ void k_gauss_rows(const float* __restrict__ f, const uint8_t* __restrict__ m, int h,
+template <typename TI>
+__global__ void k_gauss_rows(const TI* __restrict__ f, const uint8_t* __restrict__ m, int h,
                              int w, Gauss g, double* __restrict__ out) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -119,9 +120,10 @@ __device__ __forceinline__ bool edge_y(const uint8_t* m, int h, int y, int w, si
 
 // compute_tensor (solver.py:122-161) on the smoothed image; tensor in f64
 // scratch (3 per pixel) and f32 planes.
+template <typename TO>
 __global__ void k_tensor(const double* __restrict__ sm, const uint8_t* __restrict__ m, int h, int w,
                          double beta, double eta, double* __restrict__ t64,
-                         float* __restrict__ t32) {
+                         TO* __restrict__ t32) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= w || y >= h) return;
@@ -151,12 +153,13 @@ __global__ void k_tensor(const double* __restrict__ sm, const uint8_t* __restric
     c = (lam_n * uy) * uy + ux * ux;
   }
   t64[3 * i] = a; t64[3 * i + 1] = b; t64[3 * i + 2] = c;
-  t32[i] = (float)a; t32[n + i] = (float)b; t32[2 * n + i] = (float)c;
+  t32[i] = (TO)a; t32[n + i] = (TO)b; t32[2 * n + i] = (TO)c;
 }
 
 // precondition_steps (solver.py:246-276)
+template <typename TO>
 __global__ void k_steps(const double* __restrict__ t64, const uint8_t* __restrict__ m, int h, int w,
-                        double alpha0, double alpha1, float* __restrict__ steps) {
+                        double alpha0, double alpha1, TO* __restrict__ steps) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= w || y >= h) return;
@@ -186,9 +189,9 @@ __global__ void k_steps(const double* __restrict__ t64, const uint8_t* __restric
   }
   double tau_u = 1.0 / fmax(alpha1 * col_u, 1e-12);
   double tau_v = 1.0 / (alpha1 + alpha0 * ecount);
-  steps[i] = (float)sigma_p;
-  steps[n + i] = (float)tau_u;
-  steps[2 * n + i] = (float)tau_v;
+  steps[i] = (TO)sigma_p;
+  steps[n + i] = (TO)tau_u;
+  steps[2 * n + i] = (TO)tau_v;
 }
 
 __global__ void k_planes_to_t64(const float* __restrict__ t32, size_t n, double* __restrict__ t64) {
@@ -220,10 +223,10 @@ size_t smooth_bytes(int h, int w) {
 
 size_t level_setup_scratch_internal(int h, int w) { return smooth_bytes(h, w); }
 
-int level_setup_internal(const fsb_level* lv, const fsb_params* prm, void* scratch,
-                         size_t scratch_bytes, cudaStream_t st) {
-  if (!lv || !prm || !scratch) return FSB_EINVAL;
-  int h = lv->h, w = lv->w;
+template <typename T>
+int level_setup_t(const T* i0, const uint8_t* mask, int h, int w, const fsb_params* prm,
+                  T* tensor, T* steps, void* scratch, size_t scratch_bytes, cudaStream_t st) {
+  if (!prm || !scratch) return FSB_EINVAL;
   if (scratch_bytes < smooth_bytes(h, w)) return FSB_ENOSPC;
   Gauss g;
   if (!make_gauss(prm->tensor_sigma, g)) return FSB_EINVAL;
@@ -233,11 +236,24 @@ int level_setup_internal(const fsb_level* lv, const fsb_params* prm, void* scrat
   double* sm = reinterpret_cast<double*>(p); p += align_up(n * sizeof(double));
   double* t64 = reinterpret_cast<double*>(p);
   dim3 blk(kBX, kBY), grd = grid2d(w, h, blk);
-  k_gauss_rows<<<grd, blk, 0, st>>>(lv->i0, lv->mask, h, w, g, nd);
-  k_gauss_cols<<<grd, blk, 0, st>>>(nd, lv->mask, h, w, g, sm);
-  k_tensor<<<grd, blk, 0, st>>>(sm, lv->mask, h, w, prm->beta, prm->eta, t64, lv->tensor);
-  k_steps<<<grd, blk, 0, st>>>(t64, lv->mask, h, w, prm->alpha0, prm->alpha1, lv->steps);
+  k_gauss_rows<T><<<grd, blk, 0, st>>>(i0, mask, h, w, g, nd);
+  k_gauss_cols<<<grd, blk, 0, st>>>(nd, mask, h, w, g, sm);
+  k_tensor<T><<<grd, blk, 0, st>>>(sm, mask, h, w, prm->beta, prm->eta, t64, tensor);
+  k_steps<T><<<grd, blk, 0, st>>>(t64, mask, h, w, prm->alpha0, prm->alpha1, steps);
   return launch_status();
+}
+
+int level_setup_internal(const fsb_level* lv, const fsb_params* prm, void* scratch,
+                         size_t scratch_bytes, cudaStream_t st) {
+  if (!lv) return FSB_EINVAL;
+  return level_setup_t<float>(lv->i0, lv->mask, lv->h, lv->w, prm, lv->tensor, lv->steps, scratch,
+                              scratch_bytes, st);
+}
+
+int level_setup64_internal(const double* i0, const uint8_t* mask, int h, int w,
+                           const fsb_params* prm, double* tensor, double* steps, void* scratch,
+                           size_t scratch_bytes, cudaStream_t st) {
+  return level_setup_t<double>(i0, mask, h, w, prm, tensor, steps, scratch, scratch_bytes, st);
 }
 
 }  // namespace fsb
@@ -260,7 +276,7 @@ int fsb_smooth_masked(const float* f, const uint8_t* mask, int32_t h, int32_t w,
   double* nd = reinterpret_cast<double*>(p); p += align_up(n * 2 * sizeof(double));
   double* sm = reinterpret_cast<double*>(p);
   dim3 blk(kBX, kBY), grd = grid2d(w, h, blk);
-  k_gauss_rows<<<grd, blk, 0, st>>>(f, mask, h, w, g, nd);
+  k_gauss_rows<float><<<grd, blk, 0, st>>>(f, mask, h, w, g, nd);
   k_gauss_cols<<<grd, blk, 0, st>>>(nd, mask, h, w, g, sm);
   k_to_f32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sm, n, out);
   return launch_status();
@@ -278,7 +294,7 @@ int fsb_compute_tensor(const float* smoothed, const uint8_t* mask, int32_t h, in
   double* t64 = reinterpret_cast<double*>(static_cast<char*>(scratch) + align_up(n * sizeof(double)));
   k_f32_to_f64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(smoothed, n, sm);
   dim3 blk(kBX, kBY), grd = grid2d(w, h, blk);
-  k_tensor<<<grd, blk, 0, st>>>(sm, mask, h, w, beta, eta, t64, tensor);
+  k_tensor<float><<<grd, blk, 0, st>>>(sm, mask, h, w, beta, eta, t64, tensor);
   return launch_status();
 }
 

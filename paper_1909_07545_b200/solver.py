@@ -340,21 +340,28 @@ class Solver:
     captured into a CUDA graph) and optional diagnostics slots.
     """
 
-    def __init__(self, rig, params: SolverParams, collect_diagnostics: bool = False):
+    def __init__(self, rig, params: SolverParams, collect_diagnostics: bool = False,
+                 precision: str = "fp32"):
+        if precision not in ("fp32", "fp64"):
+            raise ValueError("precision must be 'fp32' or 'fp64'")
         L = _ext.lib()
         self.rig = rig
         self.params = params
+        self.precision = precision
         self.rs = _ext.rig_struct(rig)
         self.ps = _ext.params_struct(params)
         self.H, self.W = self.rs.cam0.height, self.rs.cam0.width
         self.H1, self.W1 = self.rs.cam1.height, self.rs.cam1.width
-        nbytes = L.fsb_solve_pyramid_workspace_bytes(C.byref(self.rs), C.byref(self.ps))
+        sizer = (L.fsb_solve_pyramid_workspace_bytes if precision == "fp32"
+                 else L.fsb_solve_pyramid_f64_workspace_bytes)
+        nbytes = sizer(C.byref(self.rs), C.byref(self.ps))
         if nbytes == 0:
             raise ValueError("invalid rig or solver parameters")
         self.shapes = pyramid_shapes(self.H, self.W, params.pyramid_levels,
                                      params.pyramid_scale, params.min_width)
         self.workspace = _dev.scratch(nbytes)
-        E = _dev.empty
+        self.dtype = torch.float32 if precision == "fp32" else torch.float64
+        E = lambda shape, dt=None: _dev.empty(shape, dt or self.dtype)  # noqa: E731
         self.i0 = E((self.H, self.W)); self.i1 = E((self.H1, self.W1))
         self.u = E((self.H, self.W)); self.w = E((self.H, self.W, 2))
         self.v = E((self.H, self.W, 2)); self.mask = E((self.H, self.W), torch.uint8)
@@ -363,8 +370,9 @@ class Solver:
         if collect_diagnostics:
             npd, nw = C.c_int64(), C.c_int64()
             L.fsb_diag_counts(self.H, self.W, C.byref(self.ps), C.byref(npd), C.byref(nw))
-            self.d_p = E((npd.value,)); self.d_q = E((npd.value,))
-            self.d_du = E((nw.value,)); self.d_mean = E((nw.value,), torch.float64)
+            self.d_p = E((npd.value,), torch.float32); self.d_q = E((npd.value,), torch.float32)
+            self.d_du = E((nw.value,), torch.float32)
+            self.d_mean = E((nw.value,), torch.float64)
             self.diag = _ext.FsbDiag(_dev.ptr(self.d_p), _dev.ptr(self.d_q),
                                      _dev.ptr(self.d_du), _dev.ptr(self.d_mean))
         self._traj = None
@@ -384,7 +392,7 @@ class Solver:
         for (h, w) in self.shapes[::-1]:
             cam_l = self.rig.cam0.scaled_to((h, w))
             d, ok = traj_override(StereoRig(cam_l, cam_l, rig_t.pose))
-            dirs_t.append(_dev.upload(np.asarray(d, dtype=np.float64)))
+            dirs_t.append(_dev.upload(np.asarray(d, dtype=np.float64), self.dtype))
             ok_t.append(_dev.upload(np.asarray(ok, dtype=bool), torch.uint8))
         n = len(dirs_t)
         self._traj = (dirs_t, ok_t, (C.c_void_p * n)(*[_dev.ptr(t) for t in dirs_t]),
@@ -403,12 +411,15 @@ class Solver:
         """Enqueue one frame on the current stream (device inputs, device outputs)."""
         i0 = self.i0 if i0 is None else i0
         i1 = self.i1 if i1 is None else i1
-        _ext.check(_ext.lib().fsb_solve_pyramid(*self._args(i0, i1), _dev.stream_ptr()),
-                   "solve_pyramid")
+        L = _ext.lib()
+        fn = L.fsb_solve_pyramid if self.precision == "fp32" else L.fsb_solve_pyramid_f64
+        _ext.check(fn(*self._args(i0, i1), _dev.stream_ptr()), "solve_pyramid")
 
     def capture(self) -> int:
         """Capture one frame on the fixed input buffers into a CUDA graph (native,
         fsb_graph_create); returns the number of kernel launches per frame."""
+        if self.precision != "fp32":
+            raise ValueError("graph capture is provided for the fp32 production path")
         L = _ext.lib()
         self.release()
         side = torch.cuda.Stream()
@@ -470,7 +481,7 @@ class Solver:
         self._d64["i1"].copy_(h["i1"], non_blocking=True)
         self.i0.copy_(self._d64["i0"])
         self.i1.copy_(self._d64["i1"])
-        if self._traj is None:
+        if self._traj is None and self.precision == "fp32":
             self.replay()
         else:
             self.run()
@@ -508,13 +519,16 @@ def _rig_key(rig) -> tuple:
 
 
 def solve_pyramid(i0, i1, rig, params: SolverParams, collect_diagnostics: bool = False,
-                  traj_override=None) -> StereoResult:
+                  traj_override=None, *, precision: str = "fp32") -> StereoResult:
     """Full coarse-to-fine solve of a calibrated stereo pair (solver.py:401-452).
 
     Drop-in for `fisheyestereo.solve_pyramid`: same arguments, same
     `StereoResult` fields, ValueError on shape mismatch / invalid params /
     zero baseline. Engines are cached per (rig, params) so repeated frames
     reuse the workspace and CUDA graph.
+
+    precision="fp64" runs the float64 parity path (reference round-off at any
+    warp count, several times slower); "fp32" is the production path.
     """
     i0a, i1a = np.asarray(i0), np.asarray(i1)
     if i0a.shape != (rig.cam0.height, rig.cam0.width):
@@ -523,10 +537,10 @@ def solve_pyramid(i0, i1, rig, params: SolverParams, collect_diagnostics: bool =
         raise ValueError("image 1 does not match camera 1 dimensions")
     if traj_override is None and not np.any(rig.pose.rotation.T @ rig.pose.translation):
         raise ValueError("trajectory field undefined for zero baseline")
-    key = (_rig_key(rig), tuple(asdict(params).items()), bool(collect_diagnostics))
+    key = (_rig_key(rig), tuple(asdict(params).items()), bool(collect_diagnostics), precision)
     eng = None if traj_override is not None else _CACHE.get(key)
     if eng is None:
-        eng = Solver(rig, params, collect_diagnostics)
+        eng = Solver(rig, params, collect_diagnostics, precision)
         if traj_override is not None:
             eng.set_traj_override(traj_override)
         else:
