@@ -512,6 +512,23 @@ def run_b200(a) -> None:
                         "fp64<->fp32 casts on the device)"}
 
     roof = pd_roofline(eng, rig, prm, img0) if rank == 0 else None
+    # the float64 parity path (reference round-off at any N), device-resident
+    f64 = None
+    if rank == 0 and not a.no_e2e:
+        e64 = Solver(rig, prm, precision="fp64")
+        e64.i0.copy_(img0)
+        e64.i1.copy_(img1)
+        e64.run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(2):
+            e64.run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        f64 = {"value": 2 / (e0.elapsed_time(e1) / 1e3), "unit": "frames/s",
+               "path": "fsb_solve_pyramid_f64 (float64 storage + IEEE arithmetic)"}
+        del e64
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         cb = cpu_baseline(rig, prm, img0.cpu().numpy().astype(np.float64),
@@ -534,6 +551,7 @@ def run_b200(a) -> None:
             "gpu_launches": kernels * K,
             "kernels_per_frame": kernels,
             "roofline": roof,
+            "fp64_parity_path": f64,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
