@@ -33,6 +33,7 @@ UNITS = [
     ("pd_block.cu", []),
     ("pd_pair.cu", []),
     ("pd_tma.cu", []),
+    ("pd_cluster.cu", []),
     ("pd64.cu", ["-fmad=false"]),
     ("solver.cu", []),
     ("synth.cu", ["-fmad=false"]),

@@ -189,6 +189,23 @@ FSB_INLINE bool split_pos(double x, double y, int h, int w, int& ix, int& iy, Ac
   return true;
 }
 
+// Integer pixel (x, y) plus a float offset: split_pos<float>((double)x + off.x,
+// (double)y + off.y) in fp32 integer/float ops only. floor(x + o) = x + floor(o)
+// exactly, and o - floor(o) in fp32 is the correctly rounded exact fraction —
+// the same float split_pos's fp64 fraction rounds to — so the results are
+// bit-identical. Offsets beyond 1e7 px are out of range for any image.
+FSB_INLINE bool split_off(int x, int y, float ox, float oy, int h, int w, int& ix, int& iy,
+                          float& fx, float& fy) {
+  if (!(fabsf(ox) < 1e7f) || !(fabsf(oy) < 1e7f)) return false;  // also NaN / inf
+  const float flx = floorf(ox), fly = floorf(oy);
+  ix = x + (int)flx;
+  iy = y + (int)fly;
+  if (ix < -2 || ix > w || iy < -2 || iy > h) return false;
+  fx = ox - flx;
+  fy = oy - fly;
+  return true;
+}
+
 template <int C, bool kGlobal = true, typename TF = float>
 FSB_INLINE void load_tap(const TF* __restrict__ f, int idx, TF v[C]) {
   if constexpr (C == 1) {

@@ -142,8 +142,10 @@ __global__ void __launch_bounds__(256) k_warp_prologue(fsb_level L) {
   const int ox = blockIdx.x * TX, oy = blockIdx.y * TY;
   const SampleSrc S{L.i1, L.mask, L.traj, L.traj_ok, reinterpret_cast<const float4*>(L.packed),
                     L.full16, L.h, L.w};
-  for (int k = threadIdx.x; k < SH * SW; k += blockDim.x) {
-    const int r = k / SW, c = k - r * SW;
+  // flat loop over the halo tile; (r, c) advanced incrementally (no division)
+  constexpr int kStep = 256;  // == blockDim.x (launch_bounds)
+  int r = threadIdx.x / SW, c = threadIdx.x - (threadIdx.x / SW) * SW;
+  for (int k = threadIdx.x; k < SH * SW; k += kStep) {
     const int gx = ox - H + c, gy = oy - H + r;
     float iw = 0.f;
     bool iok = false, dok = false;
@@ -165,6 +167,9 @@ __global__ void __launch_bounds__(256) k_warp_prologue(fsb_level L) {
     }
     s_iw[k] = iw;
     s_okb[k] = iok;
+    r += kStep / SW;
+    c += kStep % SW;
+    if (c >= SW) { c -= SW; ++r; }
   }
   __syncthreads();
   {  // pack the validity bytes into one 64-bit word per tile row (warp ballots)
@@ -189,8 +194,7 @@ __global__ void __launch_bounds__(256) k_warp_prologue(fsb_level L) {
       const float2 d = s_dir[k];
       int ix, iy;
       float fx, fy;
-      if (split_pos<float>((double)gx + (double)d.x, (double)gy + (double)d.y, L.h, L.w, ix, iy,
-                           fx, fy)) {
+      if (split_off(gx, gy, d.x, d.y, L.h, L.w, ix, iy, fx, fy)) {
         const int lx = ix - (ox - H), ly = iy - (oy - H);  // tile-local stencil base
         unsigned okb = 0;
 #pragma unroll

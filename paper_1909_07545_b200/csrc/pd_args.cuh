@@ -7,6 +7,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "../../include/fsb200.h"
+
 namespace fsb {
 
 struct StateSet {   // plane stride n: v, vb, p hold 2 planes, q holds 4
@@ -45,5 +47,11 @@ int pd_block_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream
                     int* nblocks);
 int pd_pair_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st,
                    int* nblocks);
+
+// Whole-level warp loop on one thread-block cluster (pd_cluster.cu) for levels
+// small enough to live on <= 16 SMs.
+bool level_cluster_fits(int h, int w, int warp_iters);
+int level_cluster_solve(const fsb_level* L, const fsb_params* prm, const fsb_diag* diag,
+                        int64_t pd_off, int64_t warp_off, cudaStream_t st);
 
 }  // namespace fsb

@@ -46,12 +46,11 @@ FSB_INLINE float4 cubic_packed(const float4* __restrict__ t, int w, int ix, int 
 // i1w / warp_ok and the renormalised direction / dir_ok at x + w for one pixel.
 FSB_INLINE void warp_sample_px(const SampleSrc& S, int x, int y, float2 wv, bool mk, float& i1w,
                                bool& i1w_ok, float2& dir, bool& dir_ok) {
-  const double px = (double)x + (double)wv.x, py = (double)y + (double)wv.y;
   int ix, iy;
   float fx, fy;
   float iv = 0.f, dr0 = 0.f, dr1 = 0.f;
   bool wok = false, dok = false;
-  if (split_pos<float>(px, py, S.h, S.w, ix, iy, fx, fy)) {
+  if (split_off(x, y, wv.x, wv.y, S.h, S.w, ix, iy, fx, fy)) {
     const bool inner = ix >= 1 && ix + 2 < S.w && iy >= 1 && iy + 2 < S.h;
     const uint8_t fl = (S.full16 && inner) ? S.full16[(size_t)iy * S.w + ix] : 0;
     if ((fl & 3) == 3) {
@@ -67,8 +66,15 @@ FSB_INLINE void warp_sample_px(const SampleSrc& S, int x, int y, float2 wv, bool
   }
   float d0 = 0.f, d1 = 0.f;
   if (dok) {
-    const float nrm = sqrtf(dr0 * dr0 + dr1 * dr1);
-    if (nrm > 0.5f && mk) { d0 = dr0 / nrm; d1 = dr1 / nrm; } else dok = false;
+    // norm > 0.5 (solver.py:336) as norm^2 > 0.25; unit vector via rsqrt (<= 2 ulp)
+    const float n2 = dr0 * dr0 + dr1 * dr1;
+    if (n2 > 0.25f && mk) {
+      const float r = rsqrtf(n2);
+      d0 = dr0 * r;
+      d1 = dr1 * r;
+    } else {
+      dok = false;
+    }
   }
   i1w = wok ? iv : 0.f;
   i1w_ok = wok && mk;

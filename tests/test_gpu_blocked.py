@@ -73,3 +73,43 @@ def test_blocked_level_solve_matches_one_iteration_kernels():
         np.testing.assert_allclose(da.max_q_norm, db.max_q_norm, atol=1e-6)
         np.testing.assert_allclose(da.max_du, db.max_du, atol=1e-6)
         np.testing.assert_allclose(da.mean_abs_du, db.mean_abs_du, atol=1e-6)
+
+
+def _random_pair(h, w, seed):
+    rng = np.random.default_rng(seed)
+    mask = np.ones((h, w), bool)
+    yy, xx = np.mgrid[0:h, 0:w]
+    mask &= (xx - w / 2) ** 2 / (0.48 * w) ** 2 + (yy - h / 2) ** 2 / (0.48 * h) ** 2 < 1.0
+    base = O.smooth_in_mask(rng.random((h, w + 8)), np.ones((h, w + 8), bool), 1.2)
+    i0 = f32(base[:, 4:w + 4])
+    i1 = f32(base[:, 2:w + 2] + 0.01 * rng.normal(size=(h, w)))  # ~2 px shift
+    ang = 0.2 * np.sin(yy / max(h, 1) * 3.0)
+    dirs = f32(np.stack([np.cos(ang), np.sin(ang)], -1))
+    tok = mask.copy()
+    tok[:, :2] = False
+    return i0, i1, dirs, tok, mask
+
+
+# Level shapes on the whole-level cluster path (<= 16 rows per CTA, <= 16 warps),
+# including ragged bands and widths that are not multiples of 64.
+@pytest.mark.parametrize("shape", [(64, 64), (128, 128), (37, 50), (17, 130), (250, 40),
+                                   (96, 160)])
+def test_cluster_level_solve_matches_v1_and_oracle(shape):
+    from paper_1909_07545_b200.solver import Diagnostics, SolverParams, WarpState, solve_level
+    h, w = shape
+    i0, i1, dirs, tok, mask = _random_pair(h, w, seed=h * w)
+    prm = SolverParams(warp_iters=3, pd_iters=6, pyramid_levels=1)
+    rng = np.random.default_rng(1)
+    init = WarpState(u=f32(rng.normal(size=(h, w)) * 0.3), w=f32(rng.normal(size=(h, w, 2)) * 0.3))
+    da, db = Diagnostics(), Diagnostics()
+    a, sa = solve_level(i0, i1, dirs, tok, prm, mask, init, da, blocked=True)
+    b, sb = solve_level(i0, i1, dirs, tok, prm, mask, init, db, blocked=False)
+    for k in ("u", "w"):
+        np.testing.assert_allclose(getattr(a, k), getattr(b, k), atol=1e-5, err_msg=k)
+    for k in ("u", "v", "p", "q", "u_bar", "v_bar"):
+        np.testing.assert_allclose(getattr(sa, k), getattr(sb, k), atol=1e-5, err_msg=k)
+    for k in ("max_p_norm", "max_q_norm", "max_du", "mean_abs_du"):
+        np.testing.assert_allclose(getattr(da, k), getattr(db, k), atol=1e-6, err_msg=k)
+    ref = O.level_solve(i0, i1, dirs, tok, prm, mask, init.u, init.w)
+    err = np.abs(a.u - ref[0])[mask]
+    assert np.median(err) < 1e-5 and np.percentile(err, 99) < 1e-3, (np.median(err), err.max())
