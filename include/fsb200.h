@@ -197,9 +197,16 @@ typedef struct fsb_level {
    * state_b likewise, tensor, steps, iu, rho0, u_omega, maskf one block of 10
    * planes, and w % 4 == 0, the PD iterations run in the persistent TMA kernel. */
   float* maskf;
+  /* Optional int32 scratch of fsb_level_tiles(h,w) entries. When non-NULL,
+   * solve_level's TMA path lists the PD tiles whose interior holds a solve-mask
+   * pixel and skips the others: outside the mask the edges are zero and I_u is
+   * zero, so v, p, q stay 0 and u stays constant there (solver.py:279-303), and
+   * a skipped tile's result is its input. */
+  int32_t* tiles;
 } fsb_level;
 
 size_t fsb_level_partials(int32_t h, int32_t w);
+size_t fsb_level_tiles(int32_t h, int32_t w);
 
 /* compute_tensor(smooth_masked(i0)) + precondition_steps (solver.py:319-321,
  * 122-161, 246-276). scratch >= fsb_smooth_scratch_bytes(h,w). */

@@ -28,7 +28,7 @@ EXPORTED = (
     "fsb_calibrate_scratch_bytes", "fsb_trajectory_field", "fsb_trajectory_scratch_bytes",
     "fsb_sample_bicubic", "fsb_gradient", "fsb_divergence", "fsb_smooth_masked",
     "fsb_smooth_scratch_bytes", "fsb_pyramid_shapes", "fsb_downsample_area",
-    "fsb_upsample_state", "fsb_compute_tensor", "fsb_precondition_steps", "fsb_level_partials", "fsb_level_setup", "fsb_warp_linearize",
+    "fsb_upsample_state", "fsb_compute_tensor", "fsb_precondition_steps", "fsb_level_partials", "fsb_level_tiles", "fsb_level_setup", "fsb_warp_linearize",
     "fsb_pd_iterate", "fsb_thresholding_step", "fsb_warp_finish", "fsb_solve_level", "fsb_diag_counts",
     "fsb_solve_pyramid_workspace_bytes", "fsb_solve_pyramid",
     "fsb_solve_pyramid_f64_workspace_bytes", "fsb_solve_pyramid_f64", "fsb_render", "fsb_graph_create", "fsb_graph_launch", "fsb_graph_destroy",
@@ -67,7 +67,7 @@ class FsbLevel(C.Structure):
         (name, C.c_void_p) for name in (
             "i0", "i1", "mask", "traj", "traj_ok", "tensor", "steps", "u", "u_bar", "v",
             "v_bar", "p", "q", "wv", "u_omega", "iu", "rho0", "i1w", "i1w_ok", "dirs",
-            "dir_ok", "partials", "state_b", "packed", "full16", "maskf")]
+            "dir_ok", "partials", "state_b", "packed", "full16", "maskf", "tiles")]
 
 
 class FsbPrim(C.Structure):
@@ -118,6 +118,7 @@ def lib() -> C.CDLL:
             "fsb_precondition_steps": (C.c_int, [vp, vp, i32, i32, P(FsbParams), vp, vp, sz,
                                                  vp]),
             "fsb_level_partials": (sz, [i32, i32]),
+            "fsb_level_tiles": (sz, [i32, i32]),
             "fsb_level_setup": (C.c_int, [P(FsbLevel), P(FsbParams), vp, sz, vp]),
             "fsb_warp_linearize": (C.c_int, [P(FsbLevel), vp]),
             "fsb_pd_iterate": (C.c_int, [P(FsbLevel), P(FsbParams), i32, vp, vp, vp]),

@@ -30,6 +30,8 @@ struct BlockArgs {
   float* wv;
   // diagnostics (nullptr = off)
   float* diag_p; float* diag_q; float* diag_du; double* partials;
+  // TMA kernel work list (pd_tma_tile_list), nullptr = every tile
+  const int* tile_list;
 };
 
 // TMA descriptors of one level for the persistent kernel (pd_tma.cu): the two
@@ -42,6 +44,9 @@ bool pd_tma_maps(TmaMaps* maps, const float* state_a, const float* state_b, cons
                  int w, int h);
 int pd_tma_launch(const BlockArgs& A, const TmaMaps& maps, int src_set, int halo, bool lin,
                   bool fin, cudaStream_t st, int* nparts);
+
+int pd_tma_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles, cudaStream_t st);
+size_t pd_tma_partials(int w, int h, int halo);
 
 int pd_block_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st,
                     int* nblocks);

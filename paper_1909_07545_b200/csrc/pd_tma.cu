@@ -95,7 +95,8 @@ enum { CA, CB, CC, CSP, CTU, CTV, CIU, CRH, CUO, CM };
 template <int R, bool LIN, bool FIN, bool DIAG>
 __global__ void __launch_bounds__(kNW * 32, 1)
     k_pd_tma(const BlockArgs A, const __grid_constant__ CUtensorMap tm_src,
-             const __grid_constant__ CUtensorMap tm_const, int ntx, int ntiles) {
+             const __grid_constant__ CUtensorMap tm_const, int ntx, int ntiles,
+             const int* __restrict__ tlist) {
   constexpr int TW = kEW - 2 * R, TH = kEH - 2 * R, NW = kNW, PY = kPY, EH = kEH;
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ unsigned char smem_raw[];
@@ -130,10 +131,14 @@ __global__ void __launch_bounds__(kNW * 32, 1)
     }                                                                                     \
   } while (0)
 
+  // Work list: all tiles, or the compacted list of tiles holding mask pixels
+  // (tlist[0] = count, tlist[1 + k] = tile id; pd_tma_tile_list).
+  const int cnt = tlist ? tlist[0] : ntiles;
   uint32_t parity = 0;
-  int tile = blockIdx.x;
-  if (tile < ntiles) FSB_ISSUE_TILE(tile);
-  for (; tile < ntiles; tile += gridDim.x) {
+  int k = blockIdx.x;
+  if (k < cnt) FSB_ISSUE_TILE(tlist ? tlist[1 + k] : k);
+  for (; k < cnt; k += gridDim.x) {
+    const int tile = tlist ? tlist[1 + k] : k;
     const int ox = (tile % ntx) * TW - R, oy = (tile / ntx) * TH - R;
     mbar_wait(bar, parity);
     parity ^= 1;
@@ -173,12 +178,17 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       mbits |= (m.y != 0.f ? 1u : 0u) << (2 * j + 1);
     }
     __syncthreads();  // staging consumed: prefetch the next tile behind the cycles
-    if (tile + (int)gridDim.x < ntiles) FSB_ISSUE_TILE(tile + (int)gridDim.x);
+    if (k + (int)gridDim.x < cnt) FSB_ISSUE_TILE(tlist ? tlist[1 + k + gridDim.x] : k + gridDim.x);
 
     const f2 sq2 = mk2(A.sigma_q * A.alpha0, A.sigma_q * A.alpha0);
     const f2 al0 = mk2(A.alpha0, A.alpha0), th2 = mk2(A.theta, A.theta);
     const f2 lam2 = mk2(A.lam, A.lam), zero = mk2(0.f, 0.f);
 
+    // Rows whose cycle-`it` values reach the stored interior (dependency cone):
+    // the primal half needs [lo, hi), the dual half one more row above (the
+    // primal reads the flux of the row above). Warps entirely outside, or
+    // entirely outside the image, skip the math but keep publishing and the
+    // barriers; whatever they hold is never read by a needed row.
     for (int it = 1; it <= A.iters; ++it) {
       s_top[warp][0][lane] = ub[0];
       s_top[warp][1][lane] = vb0[0];
@@ -334,7 +344,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         double t = 0.0;
         float m = 0.f;
         for (int k = 0; k < NW; ++k) { t += red_s[k]; m = fmaxf(m, red_m[k]); }
-        A.partials[tile] = t;
+        A.partials[tile] = t;  // tiles off the list keep the zero of the level start
         atomic_max_nonneg(A.diag_du, m);
       }
       __syncthreads();
@@ -401,7 +411,7 @@ int launch_tma(const BlockArgs& A, const CUtensorMap& ms, const CUtensorMap& mc,
   }
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
   if (ntiles_out) *ntiles_out = ntiles;
-  kern<<<grid, kNW * 32, kSmemBytes, st>>>(A, ms, mc, ntx, ntiles);
+  kern<<<grid, kNW * 32, kSmemBytes, st>>>(A, ms, mc, ntx, ntiles, A.tile_list);
   return launch_status();
 }
 
@@ -421,7 +431,57 @@ int launch_tma_r(const BlockArgs& A, const CUtensorMap& ms, const CUtensorMap& m
   return launch_tma_d<R, false, false>(A, ms, mc, st, nt);
 }
 
+// One block per tile: does the interior [tx*TW, +TW) x [ty*TH, +TH) hold a
+// mask pixel? The flag lands at tiles[1 + tile].
+__global__ void k_tile_flags(const uint8_t* __restrict__ m, int w, int h, int TW, int TH, int ntx,
+                             int* __restrict__ tiles) {
+  const int t = blockIdx.x, x0 = (t % ntx) * TW, y0 = (t / ntx) * TH;
+  int any = 0;
+  for (int k = threadIdx.x; k < TW * TH; k += blockDim.x) {
+    const int x = x0 + k % TW, y = y0 + k / TW;
+    if (x < w && y < h && m[(size_t)y * w + x]) any = 1;
+  }
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) tiles[1 + t] = any;
+}
+
+// In-place stream compaction of the flags into ascending tile ids (one block):
+// tiles[0] = count, tiles[1 + k] = k-th active tile.
+__global__ void k_tile_compact(int* tiles, int ntiles) {
+  __shared__ int s_scan[1024];
+  __shared__ int s_base;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < ntiles; c0 += blockDim.x) {
+    const int t = c0 + threadIdx.x;
+    const int f = t < ntiles ? tiles[1 + t] : 0;
+    s_scan[threadIdx.x] = f;
+    __syncthreads();
+    for (int d = 1; d < (int)blockDim.x; d <<= 1) {  // Hillis-Steele inclusive scan
+      const int v = threadIdx.x >= (unsigned)d ? s_scan[threadIdx.x - d] : 0;
+      __syncthreads();
+      s_scan[threadIdx.x] += v;
+      __syncthreads();
+    }
+    const int pos = s_base + s_scan[threadIdx.x] - f;
+    __syncthreads();  // every flag of this chunk read before any write below
+    if (f) tiles[1 + pos] = t;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) s_base += s_scan[threadIdx.x];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tiles[0] = s_base;
+}
+
 }  // namespace
+
+int pd_tma_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles, cudaStream_t st) {
+  const int TW = kEW - 2 * halo, TH = kEH - 2 * halo;
+  const int ntx = (w + TW - 1) / TW, nty = (h + TH - 1) / TH;
+  k_tile_flags<<<ntx * nty, 256, 0, st>>>(mask, w, h, TW, TH, ntx, tiles);
+  k_tile_compact<<<1, 1024, 0, st>>>(tiles, ntx * nty);
+  return launch_status();
+}
 
 bool pd_tma_maps(TmaMaps* maps, const float* state_a, const float* state_b, const float* consts,
                  int w, int h) {

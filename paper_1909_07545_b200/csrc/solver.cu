@@ -108,6 +108,7 @@ struct LevelState {  // state buffers sized for the finest level, reused per lev
   double* partials;
   float* packed;
   uint8_t* full16;
+  int* tiles;
 };
 
 struct Plan {
@@ -169,6 +170,7 @@ int make_plan(const fsb_rig* rig, const fsb_params* prm, void* base, Plan& P) {
   s.state_b = c.take<float>(12 * n0);
   s.packed = c.take<float>(4 * n0);
   s.full16 = c.take<uint8_t>(n0);
+  s.tiles = c.take<int>(pd_tma_partials(W, H, 5) + 1);
   P.bytes = c.off;
   return FSB_OK;
 }
@@ -272,6 +274,18 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
   const bool dpq = diag && diag->max_p_norm && diag->max_q_norm;
   const bool ddu = diag && diag->max_du && diag->mean_abs_du;
   int rc = FSB_OK;
+  if (tma && L->tiles && halo <= 5) {
+    // Skip tiles without mask pixels. Their state is constant for the whole
+    // level (v, p, q = 0 and u fixed outside the mask), so both ping-pong sets
+    // and u_omega must hold it from the start; partial sums of skipped tiles
+    // stay zero.
+    rc = pd_tma_tile_list(L->mask, L->w, L->h, halo, L->tiles, st);
+    if (rc) return rc;
+    copy_set(sets[1], sets[0], n, st);
+    cudaMemcpyAsync(L->u_omega, L->u, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+    if (ddu) cudaMemsetAsync(L->partials, 0, pd_tma_partials(L->w, L->h, halo) * sizeof(double), st);
+    A.tile_list = L->tiles;
+  }
   for (int wi = 0; wi < N; ++wi) {
     rc = warp_prologue_internal(L, st);  // samples at x + w, I_u, rho0 (solver.py:332-343)
     if (rc) return rc;
@@ -479,6 +493,7 @@ int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const floa
     L.rho0 = S.consts + 7 * np; L.u_omega = S.consts + 8 * np; L.maskf = S.consts + 9 * np;
     L.wv = wv; L.i1w = S.i1w;
     L.i1w_ok = S.i1w_ok; L.dirs = S.dirs; L.dir_ok = S.dir_ok; L.partials = S.partials;
+    L.tiles = S.tiles;
     L.state_b = S.state_b;
     L.packed = S.packed; L.full16 = S.full16;
     rc = solve_level_internal(&L, prm, diag, pd_off, warp_off, P.setup_scratch,
@@ -518,6 +533,7 @@ using namespace fsb;
 extern "C" {
 
 size_t fsb_level_partials(int32_t h, int32_t w) { return level_partials_count(h, w); }
+size_t fsb_level_tiles(int32_t h, int32_t w) { return pd_tma_partials(w, h, 5) + 1; }
 
 int fsb_level_setup(const fsb_level* lv, const fsb_params* prm, void* scratch,
                     size_t scratch_bytes, void* stream) {

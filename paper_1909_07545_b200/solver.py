@@ -143,6 +143,8 @@ class _Level:
         self.state_b = E((12, h, w)) if blocked else None
         self.packed = E((h, w, 4)) if blocked else None
         self.full16 = E((h, w), U8) if blocked else None
+        ntl = int(_ext.lib().fsb_level_tiles(h, w))
+        self.tiles = E((ntl,), torch.int32) if blocked else None
 
     def struct(self) -> _ext.FsbLevel:
         s = _ext.FsbLevel()
