@@ -47,6 +47,7 @@ int pd_tma_launch(const BlockArgs& A, const TmaMaps& maps, int src_set, int halo
 
 int pd_tma_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles, cudaStream_t st);
 size_t pd_tma_partials(int w, int h, int halo);
+int pd_num_sms();
 
 int pd_block_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st,
                     int* nblocks);

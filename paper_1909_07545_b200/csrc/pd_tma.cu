@@ -493,6 +493,8 @@ bool pd_tma_maps(TmaMaps* maps, const float* state_a, const float* state_b, cons
          make_map(&maps->consts, consts, w, h, kConstPlanes, n);
 }
 
+int pd_num_sms() { return num_sms(); }
+
 size_t pd_tma_partials(int w, int h, int halo) {
   const int TW = kEW - 2 * halo, TH = kEH - 2 * halo;
   return (size_t)((w + TW - 1) / TW) * ((h + TH - 1) / TH);
@@ -506,7 +508,9 @@ int pd_tma_launch(const BlockArgs& A, const TmaMaps& maps, int src_set, int halo
     case 1: return launch_tma_r<1>(A, ms, maps.consts, lin, fin, st, nparts);
     case 2: return launch_tma_r<2>(A, ms, maps.consts, lin, fin, st, nparts);
     case 3: return launch_tma_r<3>(A, ms, maps.consts, lin, fin, st, nparts);
+    case 4: return launch_tma_r<4>(A, ms, maps.consts, lin, fin, st, nparts);
     case 5: return launch_tma_r<5>(A, ms, maps.consts, lin, fin, st, nparts);
+    case 10: return launch_tma_r<10>(A, ms, maps.consts, lin, fin, st, nparts);
     default: return FSB_EINVAL;
   }
 }

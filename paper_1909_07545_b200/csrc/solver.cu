@@ -7,6 +7,7 @@
 
 #include <math.h>
 #include <stdlib.h>
+#include <stdio.h>
 #include <string.h>
 
 #include <vector>
@@ -170,7 +171,7 @@ int make_plan(const fsb_rig* rig, const fsb_params* prm, void* base, Plan& P) {
   s.state_b = c.take<float>(12 * n0);
   s.packed = c.take<float>(4 * n0);
   s.full16 = c.take<uint8_t>(n0);
-  s.tiles = c.take<int>(pd_tma_partials(W, H, 5) + 1);
+  s.tiles = c.take<int>(pd_tma_partials(W, H, 10) + 1);
   P.bytes = c.off;
   return FSB_OK;
 }
@@ -188,15 +189,31 @@ size_t level_partials_count(int h, int w) { return level_partials_internal(h, w)
 namespace {
 
 // PD iterations per launch of the blocked kernel (= its halo). FSB_PD_HALO
-// overrides for tuning experiments (1, 2, 3 or 5).
-int pd_halo(int K) {
+// overrides for tuning experiments (1, 2, 3, 4, 5 or 10); FSB_PD_HALO_L =
+// "w:R,w:R,..." overrides it per level width.
+int pd_halo(int K, int w = 0, int hgt = 0) {
   static int env = -1;
+  static int lw[16], lr[16], nl = 0;
   if (env < 0) {
     const char* e = getenv("FSB_PD_HALO");
     env = e ? atoi(e) : 0;
+    const char* l = getenv("FSB_PD_HALO_L");
+    while (l && *l && nl < 16) {
+      int a, b, c = 0;
+      if (sscanf(l, "%d:%d%n", &a, &b, &c) != 2) break;
+      lw[nl] = a; lr[nl] = b; ++nl;
+      l += c;
+      if (*l == ',') ++l;
+    }
   }
   int h = env > 0 ? env : 5;
-  if (K < h) h = K <= 1 ? 1 : (K == 2 ? 2 : (K == 3 ? 3 : 5));
+  // A level whose 10-cycle tiles (44 x 12 interiors) fit in one wave runs each
+  // warp's K = 10 cycles in one launch: at these sizes the per-launch cost
+  // (exposed tile load, launch gap) outweighs the extra halo (C3 256^2: -10 %).
+  if (env <= 0 && K >= 10 && w > 0 && (int)pd_tma_partials(w, hgt, 10) <= pd_num_sms()) h = 10;
+  for (int i = 0; i < nl; ++i)
+    if (lw[i] == w) h = lr[i];
+  if (K < h) h = K <= 1 ? 1 : (K == 2 ? 2 : (K == 3 ? 3 : (K == 4 ? 4 : 5)));
   return h;
 }
 
@@ -256,10 +273,11 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
                       int64_t pd_off, int64_t warp_off, cudaStream_t st) {
   const size_t n = (size_t)L->h * L->w;
   const int N = prm->warp_iters, K = prm->pd_iters;
-  const int halo = pd_halo(K);
   StateSet sets[2] = {set_a(L), set_b(L)};
   TmaMaps maps;
   const bool tma = tma_layout(L) && pd_tma_maps(&maps, L->u, L->state_b, L->tensor, L->w, L->h);
+  int halo = pd_halo(K, L->w, L->h);
+  if (!tma && halo > 5) halo = 5;  // the fallback kernels stop at R = 5
   int cur = 0;
   BlockArgs A;
   memset(&A, 0, sizeof(A));
@@ -274,7 +292,7 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
   const bool dpq = diag && diag->max_p_norm && diag->max_q_norm;
   const bool ddu = diag && diag->max_du && diag->mean_abs_du;
   int rc = FSB_OK;
-  if (tma && L->tiles && halo <= 5) {
+  if (tma && L->tiles) {
     // Skip tiles without mask pixels. Their state is constant for the whole
     // level (v, p, q = 0 and u fixed outside the mask), so both ping-pong sets
     // and u_omega must hold it from the start; partial sums of skipped tiles
@@ -533,7 +551,7 @@ using namespace fsb;
 extern "C" {
 
 size_t fsb_level_partials(int32_t h, int32_t w) { return level_partials_count(h, w); }
-size_t fsb_level_tiles(int32_t h, int32_t w) { return pd_tma_partials(w, h, 5) + 1; }
+size_t fsb_level_tiles(int32_t h, int32_t w) { return pd_tma_partials(w, h, 10) + 1; }
 
 int fsb_level_setup(const fsb_level* lv, const fsb_params* prm, void* scratch,
                     size_t scratch_bytes, void* stream) {
