@@ -114,6 +114,31 @@ int fsb_calibrate_second_image(const fsb_rig* rig, const float* i1, const uint8_
                                void* stream);
 size_t fsb_calibrate_scratch_bytes(const fsb_rig* rig);
 
+/* ------------------------------------------------------- post-solve depth */
+
+/* compose_with_calibration (fields.py:170-182): full = w + cal(x + w) where the
+ * f64 bicubic of the calibration field under cal_ok is valid, else 0.
+ * wv, cal, full: (h,w,2) f64; cal_ok, ok: (h,w) u8. */
+int fsb_compose_calibration(const double* wv, const double* cal, const uint8_t* cal_ok, int32_t h,
+                            int32_t w, double* full, uint8_t* ok, void* stream);
+
+/* triangulate_midpoint (camera.py:317-343) on n pixel pairs x0 (cam0), x1
+ * (cam1), (n,2) f64: distance along the camera-0 ray of the midpoint of the
+ * shortest segment between the rays; invalid (NaN, ok = 0) for invalid rays,
+ * rays closer to parallel than min_angle, or a midpoint behind camera 0. */
+int fsb_triangulate_midpoint(const fsb_rig* rig, const double* x0, const double* x1, int64_t n,
+                             double min_angle, double* depth, uint8_t* ok, void* scratch,
+                             size_t scratch_bytes, void* stream);
+size_t fsb_triangulate_scratch_bytes(void);
+
+/* depth_from_correspondence (evaluate.py:101-114): x1 = x + corr on the cam0
+ * grid, triangulated (min_angle 1e-6), ok &= valid, depth = min(depth, cap)
+ * where ok else 0. corr: (h,w,2) f64; valid, ok: (h,w) u8; depth (h,w) f64.
+ * Scratch: fsb_triangulate_scratch_bytes(). */
+int fsb_depth_from_correspondence(const fsb_rig* rig, const double* corr, const uint8_t* valid,
+                                  int32_t h, int32_t w, double depth_cap, double* depth,
+                                  uint8_t* ok, void* scratch, size_t scratch_bytes, void* stream);
+
 /* generate_trajectory_field (fields.py:48-108) for the translation-only rig
  * (cam, cam, (I, t)); fp64 throughout, dirs stored f32 (H,W,2), ok u8 (H,W).
  * Returns FSB_EDOMAIN for a zero baseline (fields.py:63-66). */
@@ -322,6 +347,15 @@ typedef struct fsb_prim {
 int fsb_render(const fsb_camera* cam, const double rotation[9], const double origin[3],
                const fsb_prim* prims, int32_t nprims, int32_t supersample, float* image,
                float* depth, uint8_t* hit, void* stream);
+
+/* make_ground_truth (synth.py:271-303): exact depth0 (cam0 ray distance, 0 off
+ * the scene / FOV), correspondence x1 - x0 (0 where cam0 misses or cam1 cannot
+ * project) and covisibility (unoccluded from camera 1 within occlusion_tol,
+ * inside camera 1's FOV and image). depth0 (H,W) f64, corr (H,W,2) f64, covis
+ * (H,W) u8 on the cam0 grid; scratch >= 256 bytes. */
+int fsb_ground_truth(const fsb_rig* rig, const fsb_prim* prims, int32_t nprims,
+                     double occlusion_tol, double* depth0, double* corr, uint8_t* covis,
+                     void* scratch, size_t scratch_bytes, void* stream);
 
 /* Library build identification, e.g. "fsb200 sm_100a". */
 const char* fsb_version(void);

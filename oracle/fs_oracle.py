@@ -687,3 +687,56 @@ def pyramid_solve(i0, i1, rig, prm, traj_override=None, trace: bool = False) -> 
         u, w, s = level_solve(f0[lvl], f1[lvl], dirs, tok, prm, lm, u0, w0, tr)
         prev = lm
     return Solution(u=u, w=w, v=s.v, mask=prev, i1c=i1c, trace=tr)
+
+
+# ---------------------------------------------------------------- post-solve depth
+# the solver's warp -> camera-1 correspondence -> depth.
+
+def compose_calibration(w, cal, cal_ok):
+    """compose_with_calibration (fields.py:170-182): the camera-1 pixel of x is
+    (x + w) + cal(x + w); cal is sampled bicubically under cal_ok."""
+    h, wd = cal_ok.shape
+    gx, gy = grid_xy(h, wd)
+    probe = np.stack([gx, gy], axis=-1) + w
+    cal_at, ok = bicubic(cal, probe, cal_ok)
+    full = np.where(ok[..., None], w + np.where(ok[..., None], cal_at, 0.0), 0.0)
+    return full, ok
+
+
+def camera1_center(pose):
+    """RelativePose.camera1_center (camera.py:267-270): -R^T t."""
+    return -np.asarray(pose.rotation).T @ np.asarray(pose.translation)
+
+
+def triangulate(rig, x0, x1, min_angle=1e-6):
+    """triangulate_midpoint (camera.py:317-343): distance along the camera-0 ray
+    of the midpoint of the shortest segment between the two rays."""
+    x0 = np.asarray(x0, dtype=np.float64)
+    x1 = np.asarray(x1, dtype=np.float64)
+    r0x, r0y, r0z, v0 = unproject(rig.cam0, x0[..., 0], x0[..., 1])
+    r1x, r1y, r1z, v1 = unproject(rig.cam1, x1[..., 0], x1[..., 1])
+    R = np.asarray(rig.pose.rotation, dtype=np.float64)
+    c1 = camera1_center(rig.pose)
+    r0 = np.stack([r0x, r0y, r0z], axis=-1)
+    d1 = np.stack([r1x, r1y, r1z], axis=-1) @ R  # R^T r1
+    r0 = np.where(v0[..., None], r0, 0.0)
+    d1 = np.where(v1[..., None], d1, 0.0)
+    b = np.sum(r0 * d1, axis=-1)
+    sin_angle = np.linalg.norm(np.cross(r0, d1), axis=-1)
+    p = r0 @ c1
+    q = d1 @ c1
+    ok = v0 & v1 & (sin_angle >= min_angle)
+    denom = np.where(ok, 1.0 - b * b, 1.0)
+    s0 = (p - b * q) / denom
+    ok = ok & (s0 > 0)
+    return np.where(ok, s0, np.nan), ok
+
+
+def depth_from_corr(rig, corr, valid, depth_cap=1e6):
+    """depth_from_correspondence (evaluate.py:101-114)."""
+    h, wd = valid.shape
+    gx, gy = grid_xy(h, wd)
+    grid = np.stack([gx, gy], axis=-1)
+    depth, ok = triangulate(rig, grid, grid + corr)
+    ok = ok & valid
+    return np.where(ok, np.minimum(depth, depth_cap), 0.0), ok

@@ -243,6 +243,63 @@ def main() -> int:
         k += 1
     np.savez_compressed(OUT / "render.npz", **rec)
 
+    # ---- post-solve depth: compose_with_calibration, depth_from_correspondence,
+    # triangulate_midpoint (own rng: the fixtures above keep their streams)
+    from fisheyestereo import evaluate
+    rd = np.random.default_rng(1909)
+    for name, (c0, c1, pose) in {
+        "unified": (cams["unified"],
+                    camera.UnifiedCamera(width=48, height=40, fx=20.0, fy=20.5, cx=24.0, cy=19.9,
+                                         fov=np.pi, xi=0.9),
+                    camera.RelativePose.from_displacement((0.1, 0.0, 0.0),
+                                                          rotvec=(0.0, 0.03, 0.01))),
+        "kb": (cams["kb"], cams["kb"],
+               camera.RelativePose.from_displacement((0.064, 0.01, 0.0),
+                                                     rotvec=(0.002, 0.004, 0.001))),
+    }.items():
+        rig = camera.StereoRig(c0, c1, pose)
+        cal, cok = fields.generate_calibration_field(rig)
+        wv = rd.uniform(-4.0, 1.0, size=(c0.height, c0.width, 2))
+        wv[..., 1] *= 0.2
+        full, fok = fields.compose_with_calibration(wv, cal, cok)
+        valid = fok & c0.fov_mask()
+        depth, dok = evaluate.depth_from_correspondence(rig, full, valid)
+        depth_c, dok_c = evaluate.depth_from_correspondence(rig, full, valid, depth_cap=2.0)
+        pts = rd.uniform(-1.5, 1.5, size=(400, 3))
+        pts[:, 2] = rd.uniform(0.3, 5.0, size=400)
+        x0, ok0 = rig.cam0.project(pts)
+        x1, ok1 = rig.cam1.project(pose.transform(pts))
+        sel = ok0 & ok1
+        x0, x1 = x0[sel], x1[sel]
+        x1[:5] = x0[:5]  # zero-disparity / parallel-ray cases
+        x1[5:10] += rd.normal(size=(5, 2)) * 3.0  # inconsistent pairs
+        tri, tok = camera.triangulate_midpoint(rig, x0, x1)
+        np.savez_compressed(OUT / f"depth_{name}.npz", cam0=cam_record(c0), cam1=cam_record(c1),
+                            R=pose.rotation, t=pose.translation, cal=cal, cal_ok=cok, wv=wv,
+                            full=full, full_ok=fok, valid=valid, depth=depth, depth_ok=dok,
+                            depth_cap2=depth_c, depth_cap2_ok=dok_c, x0=x0, x1=x1, tri=tri,
+                            tri_ok=tok)
+
+    # ---- ground truth of a rendered pair (synth.make_ground_truth)
+    rec = {}
+    for k, (scene, c0, c1, pose) in enumerate([
+            (synth.default_scene(), cams["unified"],
+             camera.UnifiedCamera(width=48, height=40, fx=20.0, fy=20.5, cx=24.0, cy=19.9,
+                                  fov=np.pi, xi=0.9),
+             camera.RelativePose.from_displacement((0.1, 0.02, 0.0), rotvec=(0.0, 0.03, 0.01))),
+            (extra, cams["kb"], cams["kb"],
+             camera.RelativePose.from_displacement((0.3, 0.0, 0.05), rotvec=(0.01, 0.0, 0.02)))]):
+        rig = camera.StereoRig(c0, c1, pose)
+        gt = synth.make_ground_truth(scene, rig)
+        rec[f"cam0_{k}"] = cam_record(c0)
+        rec[f"cam1_{k}"] = cam_record(c1)
+        rec[f"R_{k}"] = pose.rotation
+        rec[f"t_{k}"] = pose.translation
+        rec[f"depth0_{k}"] = gt.depth0
+        rec[f"corr_{k}"] = gt.correspondence
+        rec[f"covis_{k}"] = gt.covisibility
+    np.savez_compressed(OUT / "ground_truth.npz", **rec)
+
     total = sum(f.stat().st_size for f in OUT.glob("*.npz"))
     print(f"wrote {len(list(OUT.glob('*.npz')))} fixtures, {total / 1024:.0f} KiB -> {OUT}")
     return 0

@@ -37,6 +37,7 @@ UNITS = [
     ("pd64.cu", ["-fmad=false"]),
     ("solver.cu", []),
     ("synth.cu", ["-fmad=false"]),
+    ("depth.cu", ["-fmad=false"]),
 ]
 HEADERS = [*sorted(CSRC.glob("*.cuh")), ROOT / "include" / "fsb200.h"]
 

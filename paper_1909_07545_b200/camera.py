@@ -222,3 +222,30 @@ def project(cam, points):
     _ext.check(L.fsb_project(C.byref(cs), _dev.ptr(dX), n, _dev.ptr(pix), _dev.ptr(ok),
                              _dev.stream_ptr()), "project")
     return _dev.download(pix).reshape(shape + (2,)), _dev.download(ok, bool).reshape(shape)
+
+
+def triangulate_midpoint(rig, x0, x1, min_angle: float = 1e-6):
+    """Depth along the camera-0 ray from pixel correspondences (camera.py:317-343):
+    the midpoint of the shortest segment between the two unprojection rays;
+    NaN / invalid for invalid rays, near-parallel rays (< min_angle) or a
+    midpoint behind camera 0. x0, x1: (..., 2)."""
+    L = _ext.lib()
+    a = np.asarray(x0, dtype=np.float64)
+    b = np.asarray(x1, dtype=np.float64)
+    if a.shape != b.shape or a.shape[-1:] != (2,):
+        raise ValueError("x0 and x1 must both be (..., 2)")
+    shape = a.shape[:-1]
+    n = int(np.prod(shape))
+    rs = _ext.rig_struct(rig)
+    da = _dev.upload(a.reshape(n, 2), _dev.torch.float64)
+    db = _dev.upload(b.reshape(n, 2), _dev.torch.float64)
+    depth = _dev.empty((max(n, 1),), _dev.torch.float64)
+    ok = _dev.empty((max(n, 1),), _dev.torch.uint8)
+    s = _dev.scratch(L.fsb_triangulate_scratch_bytes())
+    _ext.check(L.fsb_triangulate_midpoint(C.byref(rs), _dev.ptr(da), _dev.ptr(db), n,
+                                          float(min_angle), _dev.ptr(depth), _dev.ptr(ok),
+                                          _dev.ptr(s), s.numel(), _dev.stream_ptr()),
+               "triangulate_midpoint")
+    d = _dev.download(depth)[:n].reshape(shape)
+    v = _dev.download(ok, bool)[:n].reshape(shape)
+    return d, v

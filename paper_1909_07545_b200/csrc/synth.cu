@@ -179,10 +179,111 @@ __global__ void k_render(RenderArgs a, float* __restrict__ image, float* __restr
   if (hitmask) hitmask[o] = hit;
 }
 
+// Nearest hit distance of a ray from `o` along `d` over the scene (Scene.cast
+// without the shading, synth.py:193-205).
+__device__ double first_hit(const fsb_prim* prims, int nprims, const double o[3],
+                            const double d[3]) {
+  double best = INFINITY;
+  for (int k = 0; k < nprims; ++k) {
+    const double t = intersect(prims[k], o, d);
+    if (t < best) best = t;
+  }
+  return best;
+}
+
+struct TruthArgs {
+  Cam c0, c1;
+  double R[9], t[3], c1w[3];  // pose (world = camera 0) and camera-1 centre
+  const fsb_prim* prims;
+  int nprims;
+  double tol;
+};
+
+// make_ground_truth (synth.py:271-303) for one camera-0 pixel: depth0 from a
+// point-sampled camera-0 render, the exact correspondence through camera 1,
+// and covisibility (unoccluded from camera 1, inside its FOV and image).
+__global__ void k_ground_truth(TruthArgs a, const int* iters, double* __restrict__ depth0,
+                               double* __restrict__ corr, uint8_t* __restrict__ covis) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= a.c0.width || y >= a.c0.height) return;
+  const size_t i = (size_t)y * a.c0.width + x;
+  double r[3];
+  const bool valid = cam_unproject(a.c0, (double)x, (double)y,
+                                   a.c0.model == FSB_CAM_POLYNOMIAL ? *iters : 0, r[0], r[1],
+                                   r[2]);
+  if (!valid) r[0] = r[1] = r[2] = 0.0;
+  const double o0[3] = {0.0, 0.0, 0.0};
+  const double t0 = first_hit(a.prims, a.nprims, o0, r);
+  const bool hit = isfinite(t0) && valid;  // render()'s valid0
+  const double dep = hit ? t0 : 0.0;
+  depth0[i] = dep;
+  double pt[3];
+  for (int k = 0; k < 3; ++k) pt[k] = (hit ? r[k] : 0.0) * dep;
+  // pose.transform: pts @ R.T + t
+  double q[3];
+  for (int k = 0; k < 3; ++k)
+    q[k] = ((pt[0] * a.R[3 * k] + pt[1] * a.R[3 * k + 1]) + pt[2] * a.R[3 * k + 2]) + a.t[k];
+  double px, py;
+  const bool v1 = cam_project(a.c1, q[0], q[1], q[2], px, py);
+  const bool both = hit && v1;
+  corr[2 * i] = both ? px - (double)x : 0.0;
+  corr[2 * i + 1] = both ? py - (double)y : 0.0;
+  // occlusion: re-cast from camera 1 toward the surface point
+  double seg[3];
+  for (int k = 0; k < 3; ++k) seg[k] = pt[k] - a.c1w[k];
+  const double dist1 = sqrt((seg[0] * seg[0] + seg[1] * seg[1]) + seg[2] * seg[2]);
+  const double inv = fmax(dist1, 1e-300);
+  double d1[3];
+  for (int k = 0; k < 3; ++k) d1[k] = seg[k] / inv;
+  const double th = first_hit(a.prims, a.nprims, a.c1w, d1);
+  const bool unocc = fabs(th - dist1) <= a.tol * fmax(dist1, 1.0);
+  const bool inb = px >= 0.0 && px <= (double)(a.c1.width - 1) && py >= 0.0 &&
+                   py <= (double)(a.c1.height - 1) && isfinite(px) && isfinite(py);
+  covis[i] = both && unocc && inb;
+}
+
+// Polynomial camera 0: call-wide Newton count of the grid (camera.py:177-185).
+__global__ void k_grid_iters(Cam c, int* iters) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  int n = 0;
+  if (x < c.width && y < c.height) n = poly_conv_iters(c, (double)x, (double)y);
+  for (int o = 16; o > 0; o >>= 1) n = max(n, __shfl_xor_sync(0xffffffffu, n, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(iters, n);
+}
+
 }  // namespace
 }  // namespace fsb
 
 using namespace fsb;
+
+extern "C" int fsb_ground_truth(const fsb_rig* rig, const fsb_prim* prims, int32_t nprims,
+                                double occlusion_tol, double* depth0, double* corr,
+                                uint8_t* covis, void* scratch, size_t scratch_bytes,
+                                void* stream) {
+  if (!rig || rig->cam0.width < 1 || rig->cam0.height < 1 || nprims < 0 ||
+      (nprims > 0 && !prims) || !depth0 || !corr || !covis || !scratch ||
+      scratch_bytes < sizeof(int))
+    return FSB_EINVAL;
+  cudaStream_t st = as_stream(stream);
+  TruthArgs a;
+  a.c0 = make_cam(rig->cam0);
+  a.c1 = make_cam(rig->cam1);
+  for (int k = 0; k < 9; ++k) a.R[k] = rig->rotation[k];
+  for (int k = 0; k < 3; ++k) a.t[k] = rig->translation[k];
+  for (int j = 0; j < 3; ++j)  // camera1_center = -R^T t
+    a.c1w[j] = -((a.R[j] * a.t[0] + a.R[3 + j] * a.t[1]) + a.R[6 + j] * a.t[2]);
+  a.prims = prims;
+  a.nprims = nprims;
+  a.tol = occlusion_tol;
+  int* iters = static_cast<int*>(scratch);
+  const dim3 blk(16, 16), grd = grid2d(a.c0.width, a.c0.height, blk);
+  cudaMemsetAsync(iters, 0, sizeof(int), st);
+  if (a.c0.model == FSB_CAM_POLYNOMIAL) k_grid_iters<<<grd, blk, 0, st>>>(a.c0, iters);
+  k_ground_truth<<<grd, blk, 0, st>>>(a, iters, depth0, corr, covis);
+  return launch_status();
+}
 
 extern "C" int fsb_render(const fsb_camera* cam, const double rotation[9], const double origin[3],
                           const fsb_prim* prims, int32_t nprims, int32_t supersample,

@@ -83,3 +83,24 @@ def calibrate_second_image(i1, rig, mask1=None):
                                             _dev.stream_ptr()), "calibrate_second_image")
     cal, cal_ok = generate_calibration_field(rig)
     return _dev.download(i1c), _dev.download(ok, bool), cal, cal_ok
+
+
+def compose_with_calibration(w, cal_field, cal_valid):
+    """Solver warp (calibrated frame) -> full camera-1 correspondence
+    (fields.py:170-182): (x + w) + calibration(x + w), f64 bicubic of the
+    calibration field under `cal_valid`; 0 where that sample is invalid."""
+    L = _ext.lib()
+    ok_in = np.asarray(cal_valid, dtype=bool)
+    h, wd = ok_in.shape
+    wv = np.asarray(w, dtype=np.float64)
+    cal = np.asarray(cal_field, dtype=np.float64)
+    if wv.shape != (h, wd, 2) or cal.shape != (h, wd, 2):
+        raise ValueError("w and cal_field must be (H, W, 2) on the cal_valid grid")
+    dw, dc = _dev.upload(wv, torch.float64), _dev.upload(cal, torch.float64)
+    dm = _dev.upload(ok_in, torch.uint8)
+    full = _dev.empty((h, wd, 2), torch.float64)
+    ok = _dev.empty((h, wd), torch.uint8)
+    _ext.check(L.fsb_compose_calibration(_dev.ptr(dw), _dev.ptr(dc), _dev.ptr(dm), h, wd,
+                                         _dev.ptr(full), _dev.ptr(ok), _dev.stream_ptr()),
+               "compose_with_calibration")
+    return _dev.download(full), _dev.download(ok, bool)

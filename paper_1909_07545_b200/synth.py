@@ -161,6 +161,34 @@ def render(scene, cam, pose: RelativePose | None = None, noise_sigma: float = 0.
     return _dev.download(img), _dev.download(depth), _dev.download(hit, bool)
 
 
+@dataclass(frozen=True)
+class GroundTruth:
+    """Exact per-pixel geometry of a rendered stereo pair (camera-0 grid)."""
+
+    depth0: np.ndarray          # meters along the camera-0 ray
+    correspondence: np.ndarray  # exact x1 - x0, pixels, zero where invalid
+    covisibility: np.ndarray    # boolean: unoccluded and inside both views
+
+
+def make_ground_truth(scene, rig: StereoRig, occlusion_tol: float = 1e-6) -> GroundTruth:
+    """Exact depth, correspondence and covisibility (synth.py:271-303), ray-cast
+    on the GPU in fp64 (fsb_ground_truth)."""
+    L = _ext.lib()
+    rs = _ext.rig_struct(rig)
+    h, w = rs.cam0.height, rs.cam0.width
+    prims = _scene_device(scene)
+    depth = _dev.empty((h, w), torch.float64)
+    corr = _dev.empty((h, w, 2), torch.float64)
+    covis = _dev.empty((h, w), torch.uint8)
+    s = _dev.scratch(256)
+    _ext.check(L.fsb_ground_truth(C.byref(rs), _dev.ptr(prims), len(scene.primitives),
+                                  float(occlusion_tol), _dev.ptr(depth), _dev.ptr(corr),
+                                  _dev.ptr(covis), _dev.ptr(s), s.numel(), _dev.stream_ptr()),
+               "make_ground_truth")
+    return GroundTruth(depth0=_dev.download(depth), correspondence=_dev.download(corr),
+                       covisibility=_dev.download(covis, bool))
+
+
 # ---------------------------------------------------------------- stock configurations
 
 def default_rig() -> StereoRig:

@@ -153,3 +153,24 @@ def test_pyramid_solve():
     same(sol.trace.max_p_norm, g["max_p"])
     same(sol.trace.max_du, g["max_du"])
     same(sol.trace.mean_abs_du, g["mean_du"])
+
+
+@pytest.mark.parametrize("name", ["unified", "kb"])
+def test_depth_chain(name):
+    """compose_with_calibration, depth_from_correspondence (with and without a
+    cap) and triangulate_midpoint against the reference."""
+    g = load_golden(f"depth_{name}")
+    rig = _rig(g)
+    full, fok = O.compose_calibration(g["wv"], g["cal"], g["cal_ok"])
+    same(fok, g["full_ok"])
+    same(full, g["full"])
+    d, dok = O.depth_from_corr(rig, g["full"], g["valid"])
+    same(dok, g["depth_ok"])
+    np.testing.assert_allclose(d, g["depth"], rtol=1e-12, atol=0)
+    d2, dok2 = O.depth_from_corr(rig, g["full"], g["valid"], depth_cap=2.0)
+    same(dok2, g["depth_cap2_ok"])
+    np.testing.assert_allclose(d2, g["depth_cap2"], rtol=1e-12, atol=0)
+    t, tok = O.triangulate(rig, g["x0"], g["x1"])
+    same(tok, g["tri_ok"])
+    np.testing.assert_allclose(t, g["tri"], rtol=1e-12, atol=0)
+    assert np.isnan(t[~tok]).all()
