@@ -68,13 +68,17 @@ def workload(name: str, frame: int = 0):
         return (c4_rig(0), SolverParams(),
                 "C4: 256-frame sequence of C3-geometry frames (per-frame pose, reseeded scene), "
                 "partitioned in contiguous blocks across ranks; N=50 x K=10, 5 levels", 1)
-    if name == "c5":
+    if name in ("c5", "c5-tgv"):
         cam = UnifiedCamera(width=2048, height=2048, fx=910.0, fy=910.0, cx=1023.5, cy=1023.5,
                             fov=math.pi, xi=0.9)
+        reg = "huber" if name == "c5" else "tgv"
         return (StereoRig(cam, cam, RelativePose.from_displacement((0.1, 0, 0),
                                                                    rotvec=(0, 0.02, 0.005))),
-                SolverParams(warp_iters=20, pd_iters=10, pyramid_levels=7, min_width=32),
-                "C5: 2048x2048 unified, N=20 x K=10, 7 levels (min_width 32), TGV", 1)
+                SolverParams(warp_iters=20, pd_iters=10, pyramid_levels=7, min_width=32,
+                             regularizer=reg),
+                "C5: 2048x2048 unified, N=20 x K=10 (200 iters/level), 7 levels (min_width 32), "
+                + ("Huber-TV regulariser (eps 0.05; parity unpinned, no reference Huber)"
+                   if reg == "huber" else "TGV (parity variant)"), 1)
     raise ValueError(name)
 
 
@@ -566,7 +570,7 @@ def main(argv=None) -> int:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=["c3", "c1", "c2", "c4", "c5"], default="c3")
+    ap.add_argument("--workload", choices=["c3", "c1", "c2", "c4", "c5", "c5-tgv"], default="c3")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the public-API e2e leg")
     ap.add_argument("--profile-pd", action="store_true",

@@ -74,7 +74,17 @@ typedef struct fsb_params {
   double epsilon_scale;
   double tensor_sigma;
   double theta;
+  /* Regulariser (extension, parity-unpinned against the TGV-only reference):
+   * FSB_REG_TGV alpha1|T grad u - v| + alpha0|grad v| (solver.py:279-303),
+   * FSB_REG_TV alpha1|T grad u| (v, q held at 0: tau_v = sigma_q = 0),
+   * FSB_REG_HUBER alpha1 Huber_eps(T grad u) (TV with the Huber dual step
+   * p <- proj((p + sigma_p alpha1 T grad u_bar) / (1 + sigma_p alpha1 eps))). */
+  int32_t regularizer;
+  int32_t reserved;
+  double huber_eps;
 } fsb_params;
+
+enum { FSB_REG_TGV = 0, FSB_REG_TV = 1, FSB_REG_HUBER = 2 };
 
 /* Per-iteration invariants (Diagnostics, solver.py:104-119). Device arrays the
  * caller sizes with fsb_diag_counts(); any pointer may be NULL. */

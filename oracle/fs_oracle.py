@@ -503,8 +503,10 @@ class Steps:
     tau_v: np.ndarray
 
 
-def step_sizes(T, mask, alpha0, alpha1):
-    """Diagonal preconditioning (solver.py:246-276)."""
+def step_sizes(T, mask, alpha0, alpha1, regularizer="tgv"):
+    """Diagonal preconditioning (solver.py:246-276). For the TV / Huber-TV
+    extension (no reference; parity unpinned) v and q are held at zero by
+    tau_v = sigma_q = 0."""
     a, b, c = np.abs(T[..., 0]), np.abs(T[..., 1]), np.abs(T[..., 2])
     ex, ey = edges(mask)
     exf, eyf = ex.astype(np.float64), ey.astype(np.float64)
@@ -518,9 +520,10 @@ def step_sizes(T, mask, alpha0, alpha1):
     cnt = exf + eyf
     cnt[:, 1:] += exf[:, :-1]
     cnt[1:, :] += eyf[:-1, :]
-    return Steps(sigma_p=sp, sigma_q=1.0 / (2.0 * alpha0),
+    tgv = regularizer == "tgv"
+    return Steps(sigma_p=sp, sigma_q=1.0 / (2.0 * alpha0) if tgv else 0.0,
                  tau_u=1.0 / np.maximum(alpha1 * col, 1e-12),
-                 tau_v=1.0 / (alpha1 + alpha0 * cnt))
+                 tau_v=1.0 / (alpha1 + alpha0 * cnt) if tgv else np.zeros_like(cnt))
 
 
 def apply_T(T, v):
@@ -555,8 +558,10 @@ class PDState:
 
 def pd_cycle(s: PDState, T, iu, rho0, u_omega, prm, mask, st: Steps) -> PDState:
     """primal_dual_iterate (solver.py:279-303)."""
-    p = _unit_ball(s.p + st.sigma_p[..., None] * prm.alpha1
-                   * (apply_T(T, grad_fwd(s.u_bar, mask)) - s.v_bar))
+    p = s.p + st.sigma_p[..., None] * prm.alpha1 * (apply_T(T, grad_fwd(s.u_bar, mask)) - s.v_bar)
+    if getattr(prm, "regularizer", "tgv") == "huber":  # prox of the Huber conjugate
+        p = p / (1.0 + st.sigma_p[..., None] * prm.alpha1 * prm.huber_eps)
+    p = _unit_ball(p)
     jac = np.concatenate([grad_fwd(s.v_bar[..., 0], mask), grad_fwd(s.v_bar[..., 1], mask)],
                          axis=-1)
     q = _unit_ball(s.q + st.sigma_q * prm.alpha0 * jac)
@@ -612,7 +617,7 @@ def level_solve(i0, i1, traj, traj_ok, prm, mask, u0, w0, trace: Trace | None = 
     mask = np.asarray(mask, dtype=bool)
     h, wd = mask.shape
     T = edge_tensor(smooth_in_mask(i0, mask, prm.tensor_sigma), mask, prm.beta, prm.eta)
-    st = step_sizes(T, mask, prm.alpha0, prm.alpha1)
+    st = step_sizes(T, mask, prm.alpha0, prm.alpha1, getattr(prm, "regularizer", "tgv"))
     z2 = np.zeros((h, wd, 2))
     s = PDState(u=np.array(u0, dtype=np.float64), v=z2.copy(), p=z2.copy(),
                 q=np.zeros((h, wd, 4)), u_bar=np.array(u0, dtype=np.float64), v_bar=z2.copy())

@@ -55,7 +55,8 @@ class FsbParams(C.Structure):
                 ("pd_iters", C.c_int32), ("du_max", C.c_double),
                 ("pyramid_levels", C.c_int32), ("min_width", C.c_int32),
                 ("pyramid_scale", C.c_double), ("epsilon_scale", C.c_double),
-                ("tensor_sigma", C.c_double), ("theta", C.c_double)]
+                ("tensor_sigma", C.c_double), ("theta", C.c_double),
+                ("regularizer", C.c_int32), ("reserved", C.c_int32), ("huber_eps", C.c_double)]
 
 
 class FsbDiag(C.Structure):
@@ -216,4 +217,6 @@ def params_struct(p) -> FsbParams:
     s.epsilon_scale = float(p.epsilon_scale)
     s.tensor_sigma = float(p.tensor_sigma)
     s.theta = float(p.theta)
+    s.regularizer = {"tgv": 0, "tv": 1, "huber": 2}[getattr(p, "regularizer", "tgv")]
+    s.huber_eps = float(getattr(p, "huber_eps", 0.05))
     return s

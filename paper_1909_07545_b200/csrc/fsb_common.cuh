@@ -25,6 +25,16 @@ inline int launch_status() {
   return e == cudaSuccess ? FSB_OK : static_cast<int>(e);
 }
 
+// Regulariser (fsb_params.regularizer): TV / Huber-TV hold v and q at zero
+// through sigma_q = tau_v = 0; Huber adds the conjugate's 1 / (1 + sp eps)
+// shrink of the dual step (eps = 0 disables it).
+inline double sigma_q_of(const fsb_params* p) {
+  return p->regularizer == FSB_REG_TGV ? 1.0 / (2.0 * p->alpha0) : 0.0;  // solver.py:265
+}
+inline double huber_eps_of(const fsb_params* p) {
+  return p->regularizer == FSB_REG_HUBER ? p->huber_eps : 0.0;
+}
+
 inline dim3 grid2d(int w, int h, dim3 blk) {
   return dim3((unsigned)((w + blk.x - 1) / blk.x), (unsigned)((h + blk.y - 1) / blk.y), 1);
 }

@@ -26,7 +26,7 @@ struct PD {
   const float* __restrict__ rho0;
   const float* __restrict__ u_omega;
   float* u; float* u_bar; float* v; float* v_bar; float* p; float* q;
-  float lam, alpha0, alpha1, theta, sigma_q;
+  float lam, alpha0, alpha1, theta, sigma_q, heps;
 };
 
 __device__ __forceinline__ bool ex_at(const uint8_t* __restrict__ m, int w, int x, size_t i) {
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(256) k_pd_dual(PD s, float* __restrict__ dp, f
     float p0 = s.p[i], p1 = s.p[n + i];
     float q0 = s.q[i], q1 = s.q[n + i], q2 = s.q[2 * n + i], q3 = s.q[3 * n + i];
     dual_update(s.T[i], s.T[n + i], s.T[2 * n + i], s.S[i] * s.alpha1, s.sigma_q * s.alpha0, gx,
-                gy, g00, g01, g10, g11, vb0, vb1, p0, p1, q0, q1, q2, q3);
+                gy, g00, g01, g10, g11, vb0, vb1, p0, p1, q0, q1, q2, q3, s.heps);
     s.p[i] = p0; s.p[n + i] = p1;
     s.q[i] = q0; s.q[n + i] = q1; s.q[2 * n + i] = q2; s.q[3 * n + i] = q3;
     if (kDiag) {
@@ -328,7 +328,8 @@ PD make_pd(const fsb_level* L, const fsb_params* prm) {
   s.p = L->p; s.q = L->q;
   s.lam = (float)prm->lam; s.alpha0 = (float)prm->alpha0; s.alpha1 = (float)prm->alpha1;
   s.theta = (float)prm->theta;
-  s.sigma_q = (float)(1.0 / (2.0 * prm->alpha0));  // solver.py:265
+  s.sigma_q = (float)sigma_q_of(prm);  // solver.py:265
+  s.heps = (float)huber_eps_of(prm);
   return s;
 }
 

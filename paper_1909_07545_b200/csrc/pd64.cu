@@ -108,7 +108,8 @@ __global__ void k64_linearize(L64 L) {
 
 // solver.py:290-293
 template <bool kDiag>
-__global__ void k64_dual(L64 L, double alpha0, double alpha1, float* dp, float* dq) {
+__global__ void k64_dual(L64 L, double alpha0, double alpha1, double sigma_q, double heps,
+                         float* dp, float* dq) {
   int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
   double pn = 0.0, qn = 0.0;
   if (x < L.w && y < L.h) {
@@ -121,8 +122,8 @@ __global__ void k64_dual(L64 L, double alpha0, double alpha1, float* dp, float* 
     double p0 = L.p[i], p1 = L.p[n + i];
     double q0 = L.q[i], q1 = L.q[n + i], q2 = L.q[2 * n + i], q3 = L.q[3 * n + i];
     dual_update_exact<double>(L.T[i], L.T[n + i], L.T[2 * n + i], L.S[i] * alpha1,
-                              (1.0 / (2.0 * alpha0)) * alpha0, gx, gy, g00, g01, g10, g11, vb0,
-                              vb1, p0, p1, q0, q1, q2, q3);
+                              sigma_q * alpha0, gx, gy, g00, g01, g10, g11, vb0, vb1, p0, p1, q0,
+                              q1, q2, q3, heps);
     L.p[i] = p0; L.p[n + i] = p1;
     L.q[i] = q0; L.q[n + i] = q1; L.q[2 * n + i] = q2; L.q[3 * n + i] = q3;
     if (kDiag) {
@@ -308,10 +309,12 @@ int solve_level64(const L64& L, const fsb_params* prm, const fsb_diag* diag, int
     for (int k = 0; k < K; ++k) {
       if (dpq) {
         const int64_t slot = pd_off + (int64_t)wi * K + k;
-        k64_dual<true><<<grd, blk, 0, st>>>(L, prm->alpha0, prm->alpha1,
-                                            diag->max_p_norm + slot, diag->max_q_norm + slot);
+        k64_dual<true><<<grd, blk, 0, st>>>(L, prm->alpha0, prm->alpha1, sigma_q_of(prm),
+                                            huber_eps_of(prm), diag->max_p_norm + slot,
+                                            diag->max_q_norm + slot);
       } else {
-        k64_dual<false><<<grd, blk, 0, st>>>(L, prm->alpha0, prm->alpha1, nullptr, nullptr);
+        k64_dual<false><<<grd, blk, 0, st>>>(L, prm->alpha0, prm->alpha1, sigma_q_of(prm),
+                                             huber_eps_of(prm), nullptr, nullptr);
       }
       k64_primal<<<grd, blk, 0, st>>>(L, prm->lam, prm->alpha0, prm->alpha1, prm->theta);
     }
@@ -331,6 +334,8 @@ bool params_ok64(const fsb_params* p) {
   if (!p) return false;
   if (!(p->lam > 0 && p->alpha0 > 0 && p->alpha1 > 0 && p->beta > 0 && p->eta > 0)) return false;
   if (!(p->du_max > 0) || p->warp_iters < 1 || p->pd_iters < 1) return false;
+  if (p->regularizer < FSB_REG_TGV || p->regularizer > FSB_REG_HUBER) return false;
+  if (p->regularizer == FSB_REG_HUBER && !(p->huber_eps > 0)) return false;
   return p->pyramid_levels >= 1 && p->pyramid_scale > 1.0;
 }
 

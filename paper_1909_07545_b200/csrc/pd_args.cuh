@@ -24,6 +24,7 @@ struct BlockArgs {
   const float* S;   // sigma_p, tau_u, tau_v planes
   float* iu; float* rho0; float* u_omega;
   float lam, alpha0, alpha1, theta, sigma_q, du_max;
+  float huber_eps;  // > 0: Huber-TV dual step (fsb_params.regularizer)
   int iters;
   // FIN: w += du * dirs with this warp's directions (from k_warp_prologue)
   const float* dirs;

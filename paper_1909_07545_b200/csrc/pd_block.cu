@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_block(const BlockArgs A) {
         const float g10 = ex ? s_vb1[i + 1] - vb1 : 0.f;
         const float g11 = ey ? s_vb1[i + SW] - vb1 : 0.f;
         dual_update(ta[k], tb[k], tc[k], sp[k], sq, gx, gy, g00, g01, g10, g11, vb0, vb1, p0[k],
-                    p1[k], q0[k], q1[k], q2[k], q3[k]);
+                    p1[k], q0[k], q1[k], q2[k], q3[k], A.huber_eps);
         const Flux f = make_flux(ta[k], tb[k], tc[k], ex, ey, p0[k], p1[k], q0[k], q1[k], q2[k],
                                  q3[k]);
         s_px[i] = f.px; s_py[i] = f.py;

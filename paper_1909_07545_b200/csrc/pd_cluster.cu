@@ -38,6 +38,7 @@ struct ClusterArgs {
   float* i1w; uint8_t* i1w_ok;     // scratch planes (global, cluster-visible)
   SampleSrc src;                   // i1 / traj gather tables of the level
   float lam, alpha0, alpha1, theta, sigma_q, du_max;
+  float huber_eps;  // > 0: Huber-TV dual step
   int N, K;
   float* diag_p; float* diag_q; float* diag_du; double* diag_mean;  // nullptr = off
 };
@@ -214,7 +215,13 @@ __global__ void __launch_bounds__(512, 1) k_level_cluster(const ClusterArgs A) {
         const f2 g10 = mul2(exf, sub2(R2, VB1)), g11 = mul2(eyf, sub2(D2, VB1));
         const f2 t0 = sub2(fma2(ta2, gx, mul2(tb2, gy)), VB0);
         const f2 t1 = sub2(fma2(tb2, gx, mul2(tc2, gy)), VB1);
-        const f2 pp0 = fma2(sp2, t0, P0), pp1 = fma2(sp2, t1, P1);
+        f2 pp0 = fma2(sp2, t0, P0), pp1 = fma2(sp2, t1, P1);
+        if (A.huber_eps > 0.f) {  // Huber-TV: p / (1 + sp eps) before the projection
+          const f2 kk = mk2(__frcp_rn(fmaf(sp2.x, A.huber_eps, 1.f)),
+                            __frcp_rn(fmaf(sp2.y, A.huber_eps, 1.f)));
+          pp0 = mul2(pp0, kk);
+          pp1 = mul2(pp1, kk);
+        }
         const f2 rp = unit_scale2(fma2(pp0, pp0, mul2(pp1, pp1)));
         P0 = mul2(pp0, rp);
         P1 = mul2(pp1, rp);
@@ -400,7 +407,8 @@ int level_cluster_solve(const fsb_level* L, const fsb_params* prm, const fsb_dia
   A.src = SampleSrc{L->i1, L->mask, L->traj, L->traj_ok,
                     reinterpret_cast<const float4*>(L->packed), L->full16, L->h, L->w};
   A.lam = (float)prm->lam; A.alpha0 = (float)prm->alpha0; A.alpha1 = (float)prm->alpha1;
-  A.theta = (float)prm->theta; A.sigma_q = (float)(1.0 / (2.0 * prm->alpha0));
+  A.theta = (float)prm->theta; A.sigma_q = (float)sigma_q_of(prm);
+  A.huber_eps = (float)huber_eps_of(prm);
   A.du_max = (float)prm->du_max;
   A.N = prm->warp_iters; A.K = prm->pd_iters;
   if (diag && diag->max_p_norm && diag->max_q_norm) {

@@ -29,9 +29,15 @@ FSB_INLINE T shrink_step(T u_hat, T rho_hat, T g, T tau_u, T lam) {
 //   sp = sigma_p * alpha1, sq = sigma_q * alpha0.
 FSB_INLINE void dual_update(float a, float b, float c, float sp, float sq, float gx, float gy,
                             float g00, float g01, float g10, float g11, float vb0, float vb1,
-                            float& p0, float& p1, float& q0, float& q1, float& q2, float& q3) {
+                            float& p0, float& p1, float& q0, float& q1, float& q2, float& q3,
+                            float heps = 0.f) {
   p0 = p0 + sp * ((a * gx + b * gy) - vb0);
   p1 = p1 + sp * ((b * gx + c * gy) - vb1);
+  if (heps > 0.f) {  // Huber-TV: prox of the conjugate, p / (1 + sp eps)
+    const float k = __frcp_rn(1.f + sp * heps);
+    p0 = p0 * k;
+    p1 = p1 * k;
+  }
   // x / max(1, |x|) (solver.py:221-223): identity inside the unit ball (exactly
   // as the reference, divisor 1), x * rsqrt(|x|^2) outside (<= 2 ulp, fp32 path).
   const float pn2 = p0 * p0 + p1 * p1;
@@ -98,9 +104,14 @@ namespace fsb {
 template <typename T>
 FSB_INLINE void dual_update_exact(T a, T b, T c, T sp, T sq, T gx, T gy, T g00, T g01, T g10,
                                   T g11, T vb0, T vb1, T& p0, T& p1, T& q0, T& q1, T& q2,
-                                  T& q3) {
+                                  T& q3, T heps = T(0)) {
   p0 = p0 + sp * ((a * gx + b * gy) - vb0);
   p1 = p1 + sp * ((b * gx + c * gy) - vb1);
+  if (heps > T(0)) {
+    const T dd = T(1) + sp * heps;
+    p0 = p0 / dd;
+    p1 = p1 / dd;
+  }
   const T pd = fmax(T(1), sqrt(p0 * p0 + p1 * p1));
   p0 = p0 / pd;
   p1 = p1 / pd;

@@ -218,8 +218,14 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         const f2 g11 = mul2(eyf[j], sub2(dvb1, vb1[j]));
         const f2 t0 = sub2(fma2(ta[j], gx, mul2(tb[j], gy)), vb0[j]);
         const f2 t1 = sub2(fma2(tb[j], gx, mul2(tc[j], gy)), vb1[j]);
-        const f2 pp0 = fma2(sp[j], t0, p0[j]);
-        const f2 pp1 = fma2(sp[j], t1, p1[j]);
+        f2 pp0 = fma2(sp[j], t0, p0[j]);
+        f2 pp1 = fma2(sp[j], t1, p1[j]);
+        if (A.huber_eps > 0.f) {  // Huber-TV: p / (1 + sp eps) before the projection
+          const f2 kk = mk2(__frcp_rn(fmaf(sp[j].x, A.huber_eps, 1.f)),
+                            __frcp_rn(fmaf(sp[j].y, A.huber_eps, 1.f)));
+          pp0 = mul2(pp0, kk);
+          pp1 = mul2(pp1, kk);
+        }
         const f2 rp = unit_scale2(fma2(pp0, pp0, mul2(pp1, pp1)));
         p0[j] = mul2(pp0, rp);
         p1[j] = mul2(pp1, rp);

@@ -159,7 +159,7 @@ __global__ void k_tensor(const double* __restrict__ sm, const uint8_t* __restric
 // precondition_steps (solver.py:246-276)
 template <typename TO>
 __global__ void k_steps(const double* __restrict__ t64, const uint8_t* __restrict__ m, int h, int w,
-                        double alpha0, double alpha1, TO* __restrict__ steps) {
+                        double alpha0, double alpha1, bool tgv, TO* __restrict__ steps) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= w || y >= h) return;
@@ -188,7 +188,7 @@ __global__ void k_steps(const double* __restrict__ t64, const uint8_t* __restric
     ecount = ecount + eyu;
   }
   double tau_u = 1.0 / fmax(alpha1 * col_u, 1e-12);
-  double tau_v = 1.0 / (alpha1 + alpha0 * ecount);
+  double tau_v = tgv ? 1.0 / (alpha1 + alpha0 * ecount) : 0.0;  // TV / Huber: v held at 0
   steps[i] = (TO)sigma_p;
   steps[n + i] = (TO)tau_u;
   steps[2 * n + i] = (TO)tau_v;
@@ -239,7 +239,8 @@ int level_setup_t(const T* i0, const uint8_t* mask, int h, int w, const fsb_para
   k_gauss_rows<T><<<grd, blk, 0, st>>>(i0, mask, h, w, g, nd);
   k_gauss_cols<<<grd, blk, 0, st>>>(nd, mask, h, w, g, sm);
   k_tensor<T><<<grd, blk, 0, st>>>(sm, mask, h, w, prm->beta, prm->eta, t64, tensor);
-  k_steps<T><<<grd, blk, 0, st>>>(t64, mask, h, w, prm->alpha0, prm->alpha1, steps);
+  k_steps<T><<<grd, blk, 0, st>>>(t64, mask, h, w, prm->alpha0, prm->alpha1,
+                                  prm->regularizer == FSB_REG_TGV, steps);
   return launch_status();
 }
 
@@ -308,7 +309,8 @@ int fsb_precondition_steps(const float* tensor, const uint8_t* mask, int32_t h, 
   double* t64 = static_cast<double*>(scratch);
   k_planes_to_t64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(tensor, n, t64);
   dim3 blk(kBX, kBY), grd = grid2d(w, h, blk);
-  k_steps<<<grd, blk, 0, st>>>(t64, mask, h, w, prm->alpha0, prm->alpha1, steps);
+  k_steps<<<grd, blk, 0, st>>>(t64, mask, h, w, prm->alpha0, prm->alpha1,
+                               prm->regularizer == FSB_REG_TGV, steps);
   return launch_status();
 }
 

@@ -60,6 +60,8 @@ bool params_ok(const fsb_params* p) {
   if (!(p->du_max > 0)) return false;
   if (p->warp_iters < 1 || p->pd_iters < 1) return false;
   if (p->pyramid_levels < 1 || !(p->pyramid_scale > 1.0)) return false;
+  if (p->regularizer < FSB_REG_TGV || p->regularizer > FSB_REG_HUBER) return false;
+  if (p->regularizer == FSB_REG_HUBER && !(p->huber_eps > 0)) return false;
   return true;
 }
 
@@ -285,7 +287,8 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
   A.mask = L->mask; A.T = L->tensor; A.S = L->steps;
   A.iu = L->iu; A.rho0 = L->rho0; A.u_omega = L->u_omega;
   A.lam = (float)prm->lam; A.alpha0 = (float)prm->alpha0; A.alpha1 = (float)prm->alpha1;
-  A.theta = (float)prm->theta; A.sigma_q = (float)(1.0 / (2.0 * prm->alpha0));
+  A.theta = (float)prm->theta; A.sigma_q = (float)sigma_q_of(prm);
+  A.huber_eps = (float)huber_eps_of(prm);
   A.du_max = (float)prm->du_max;
   A.wv = L->wv; A.dirs = L->dirs;
   A.partials = L->partials;
@@ -356,7 +359,8 @@ int pd_iterate_blocked(const fsb_level* L, const fsb_params* prm, int iters, flo
   A.mask = L->mask; A.T = L->tensor; A.S = L->steps;
   A.iu = L->iu; A.rho0 = L->rho0; A.u_omega = L->u_omega;
   A.lam = (float)prm->lam; A.alpha0 = (float)prm->alpha0; A.alpha1 = (float)prm->alpha1;
-  A.theta = (float)prm->theta; A.sigma_q = (float)(1.0 / (2.0 * prm->alpha0));
+  A.theta = (float)prm->theta; A.sigma_q = (float)sigma_q_of(prm);
+  A.huber_eps = (float)huber_eps_of(prm);
   A.du_max = (float)prm->du_max;
   if (tma) {  // per-stage entry: the level setup has not filled maskf
     int rc = mask_to_float_internal(L->mask, n, L->maskf, st);

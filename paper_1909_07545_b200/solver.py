@@ -28,6 +28,9 @@ from .fields import calibrate_second_image  # noqa: F401  (re-export, solver.py:
 from .rasters import pixel_grid, pyramid_shapes, sample_bicubic
 
 
+REGULARIZERS = {"tgv": 0, "tv": 1, "huber": 2}
+
+
 @dataclass
 class SolverParams:
     """Optimisation weights and schedule (solver.py:36-80), same defaults."""
@@ -46,10 +49,20 @@ class SolverParams:
     epsilon_scale: float = 0.1
     tensor_sigma: float = 1.0
     theta: float = 1.0
+    # Regulariser (extension; the reference is TGV only, so "tv" / "huber" are
+    # parity-unpinned): "tgv" = alpha1|T grad u - v| + alpha0|grad v| (reference),
+    # "tv" = alpha1|T grad u| (TV-L1: v and q held at 0), "huber" = alpha1 *
+    # Huber_eps(T grad u) (Huber-TV, BASELINE config C5).
+    regularizer: str = "tgv"
+    huber_eps: float = 0.05
 
     def __post_init__(self):
         if min(self.lam, self.alpha0, self.alpha1, self.beta, self.eta) <= 0:
             raise ValueError("all weights must be positive")
+        if self.regularizer not in REGULARIZERS:
+            raise ValueError(f"regularizer must be one of {sorted(REGULARIZERS)}")
+        if self.huber_eps <= 0:
+            raise ValueError("huber_eps must be positive")
         if self.du_max <= 0:
             raise ValueError("du_max must be positive")
         if self.warp_iters < 1 or self.pd_iters < 1:
@@ -203,7 +216,8 @@ def precondition_steps(t, mask, params: SolverParams) -> _StepSizes:
                                         _dev.ptr(steps), _dev.ptr(s), s.numel(),
                                         _dev.stream_ptr()), "precondition_steps")
     st = _dev.download(steps)
-    return _StepSizes(sigma_p=st[0], sigma_q=1.0 / (2.0 * params.alpha0), tau_u=st[1],
+    sq = 1.0 / (2.0 * params.alpha0) if getattr(params, "regularizer", "tgv") == "tgv" else 0.0
+    return _StepSizes(sigma_p=st[0], sigma_q=sq, tau_u=st[1],
                       tau_v=st[2])
 
 
@@ -254,6 +268,52 @@ def primal_dual_iterate(state: SolverState, t, iu, rho0, u_omega, params: Solver
     return SolverState(u=_dev.download(lv.u), v=_from_planes(lv.v), p=_from_planes(lv.p),
                        q=_from_planes(lv.q), u_bar=_dev.download(lv.u_bar),
                        v_bar=_from_planes(lv.v_bar))
+
+
+def apply_tensor(t, vec) -> np.ndarray:
+    """Packed symmetric tensors (a, b, c) times 2-vectors (solver.py:164-168)."""
+    t = np.asarray(t)
+    vec = np.asarray(vec)
+    a, b, c = t[..., 0], t[..., 1], t[..., 2]
+    return np.stack([a * vec[..., 0] + b * vec[..., 1], b * vec[..., 0] + c * vec[..., 1]],
+                    axis=-1)
+
+
+def sqrt_tensor(t) -> np.ndarray:
+    """Symmetric PSD square root of packed tensors (solver.py:171-178)."""
+    t = np.asarray(t, dtype=np.float64)
+    a, b, c = t[..., 0], t[..., 1], t[..., 2]
+    s = np.sqrt(np.maximum(a * c - b * b, 0.0))
+    tau = np.sqrt(np.maximum((a + c) + 2.0 * s, 1e-300))
+    return np.stack([(a + s) / tau, b / tau, (c + s) / tau], axis=-1)
+
+
+def energy(i0, i1c, mask, u, v, w, params: SolverParams) -> float:
+    """Variational energy of a candidate (u, v, w) on the calibrated pair
+    (solver.py:455-473): lam |rho| + alpha1 |T^1/2 grad u - v| + alpha0 |grad v|
+    over the pixels where the warp resolves. For the TV / Huber-TV extension
+    v is zero and the first-order term is alpha1 |T^1/2 grad u| (TV) or
+    alpha1 Huber_eps(|T^1/2 grad u|) (quadratic below eps)."""
+    from .rasters import gradient, smooth_masked
+    mask = np.asarray(mask, dtype=bool)
+    i0 = np.asarray(i0, dtype=np.float64)
+    i1w, ok = warp_image(i1c, w, mask)
+    sel = mask & ok
+    t_half = sqrt_tensor(compute_tensor(smooth_masked(i0, mask, params.tensor_sigma),
+                                        params.beta, params.eta, mask))
+    rho = np.where(sel, i1w - i0, 0.0)
+    reg = getattr(params, "regularizer", "tgv")
+    v = np.asarray(v, dtype=np.float64) if reg == "tgv" else np.zeros(i0.shape + (2,))
+    gu = apply_tensor(t_half, gradient(u, mask)) - v
+    gv = np.concatenate([gradient(v[..., 0], mask), gradient(v[..., 1], mask)], axis=-1)
+    e_data = params.lam * float(np.sum(np.abs(rho[sel])))
+    ng = np.linalg.norm(gu, axis=-1)[sel]
+    if reg == "huber":
+        eps = params.huber_eps
+        ng = np.where(ng <= eps, ng * ng / (2.0 * eps), ng - 0.5 * eps)
+    e_g1 = params.alpha1 * float(np.sum(ng))
+    e_g0 = params.alpha0 * float(np.sum(np.linalg.norm(gv, axis=-1)[sel]))
+    return e_data + e_g1 + e_g0
 
 
 def warp_image(image, w, mask):
