@@ -358,6 +358,19 @@ int fsb_render(const fsb_camera* cam, const double rotation[9], const double ori
                const fsb_prim* prims, int32_t nprims, int32_t supersample, float* image,
                float* depth, uint8_t* hit, void* stream);
 
+/* evaluate.make_report (evaluate.py:62-98) reductions over n pixels:
+ * err = |w_est - w_gt| (0 outside valid; written to err_map when non-NULL),
+ * out[0] = #valid, out[1] = mean err, out[2] = median err (exact radix select),
+ * out[3] = mean |depth_est - depth_gt| over valid & finite & > 0 (NaN if none;
+ * depth pointers both NULL to skip), out[4] = that count, out[5 + k] =
+ * 100 * #(err > taus[k]) / #valid. w_*: (n,2) f64, taus/out: device f64,
+ * ntaus <= 16. Scratch: fsb_error_report_scratch_bytes(n). */
+int fsb_error_report(const double* w_est, const double* w_gt, const uint8_t* valid, int64_t n,
+                     const double* taus, int32_t ntaus, const double* depth_est,
+                     const double* depth_gt, double* err_map, double* out, void* scratch,
+                     size_t scratch_bytes, void* stream);
+size_t fsb_error_report_scratch_bytes(int64_t n);
+
 /* make_ground_truth (synth.py:271-303): exact depth0 (cam0 ray distance, 0 off
  * the scene / FOV), correspondence x1 - x0 (0 where cam0 misses or cam1 cannot
  * project) and covisibility (unoccluded from camera 1 within occlusion_tol,

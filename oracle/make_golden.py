@@ -300,6 +300,31 @@ def main() -> int:
         rec[f"covis_{k}"] = gt.covisibility
     np.savez_compressed(OUT / "ground_truth.npz", **rec)
 
+    # ---- evaluate.make_report and the PFM writer
+    from fisheyestereo import formats
+    import tempfile
+    re_ = np.random.default_rng(98)
+    h, w = 37, 53
+    w_gt = re_.normal(size=(h, w, 2)) * 5.0
+    w_est = w_gt + re_.normal(size=(h, w, 2)) * re_.choice([0.3, 2.0, 8.0], size=(h, w, 1))
+    valid = re_.random((h, w)) > 0.2
+    d_gt = re_.uniform(0.5, 6.0, size=(h, w))
+    d_est = d_gt + re_.normal(size=(h, w)) * 0.1
+    d_est[::7, ::5] = np.nan
+    d_est[1::9, ::4] = -1.0
+    taus = (0.5, 1.0, 3.0, 5.0)
+    rep = evaluate.make_report(w_est, w_gt, valid, taus, d_est, d_gt)
+    rep0 = evaluate.make_report(w_est, w_gt, valid & False, taus)
+    err = evaluate.correspondence_error(w_est, w_gt, valid)
+    with tempfile.TemporaryDirectory() as td:
+        formats.write_pfm(f"{td}/a.pfm", d_gt)
+        formats.write_vector_pfm(f"{td}/b.pfm", w_gt, third=valid)
+        pfm1 = np.frombuffer(open(f"{td}/a.pfm", "rb").read(), dtype=np.uint8)
+        pfm3 = np.frombuffer(open(f"{td}/b.pfm", "rb").read(), dtype=np.uint8)
+    np.savez_compressed(OUT / "report.npz", w_est=w_est, w_gt=w_gt, valid=valid, d_est=d_est,
+                        d_gt=d_gt, taus=np.array(taus), err=err, report=rep.to_json(),
+                        report_empty=rep0.to_json(), pfm1=pfm1, pfm3=pfm3)
+
     total = sum(f.stat().st_size for f in OUT.glob("*.npz"))
     print(f"wrote {len(list(OUT.glob('*.npz')))} fixtures, {total / 1024:.0f} KiB -> {OUT}")
     return 0

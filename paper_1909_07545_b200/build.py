@@ -38,6 +38,7 @@ UNITS = [
     ("solver.cu", []),
     ("synth.cu", ["-fmad=false"]),
     ("depth.cu", ["-fmad=false"]),
+    ("evaluate.cu", ["-fmad=false"]),
 ]
 HEADERS = [*sorted(CSRC.glob("*.cuh")), ROOT / "include" / "fsb200.h"]
 

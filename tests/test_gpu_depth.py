@@ -135,3 +135,30 @@ def test_stereo_depth_pipeline_recovers_scene_depth():
     assert sel.mean() > 0.4
     rel = np.abs(depth[sel] - gt.depth0[sel]) / gt.depth0[sel]
     assert np.median(rel) < 0.05, np.median(rel)
+
+
+def test_make_report_matches_reference():
+    """evaluate.make_report (evaluate.py:81-98) reductions on the GPU vs the
+    reference's own report: exact counts, exact (radix-select) median."""
+    import json
+    from paper_1909_07545_b200.evaluate import correspondence_error, make_report
+    g = load_golden("report")
+    taus = tuple(g["taus"])
+    rep = make_report(g["w_est"], g["w_gt"], g["valid"], taus, g["d_est"], g["d_gt"])
+    ref = json.loads(str(g["report"]))
+    assert rep.valid_count == ref["valid_count"]
+    assert rep.median_error_px == ref["median_error_px"]
+    assert abs(rep.mean_error_px - ref["mean_error_px"]) <= 1e-12 * ref["mean_error_px"]
+    assert abs(rep.mean_abs_depth_error_m - ref["mean_abs_depth_error_m"]) <= 1e-12
+    assert rep.to_dict()["pct_bad"] == ref["pct_bad"]
+    np.testing.assert_allclose(correspondence_error(g["w_est"], g["w_gt"], g["valid"]), g["err"],
+                               rtol=1e-15, atol=0)
+    empty = make_report(g["w_est"], g["w_gt"], g["valid"] & False, taus)
+    assert empty.valid_count == 0 and np.isnan(empty.median_error_px)
+    assert empty.mean_abs_depth_error_m is None
+    # odd count: the median is the middle element itself
+    v = g["valid"].copy()
+    if v.sum() % 2 == 0:
+        v[np.argwhere(v)[0][0], np.argwhere(v)[0][1]] = False
+    e = np.linalg.norm(g["w_est"] - g["w_gt"], axis=-1)[v]
+    assert make_report(g["w_est"], g["w_gt"], v, taus).median_error_px == float(np.median(e))
