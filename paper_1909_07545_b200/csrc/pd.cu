@@ -9,12 +9,15 @@
 // multi-channel state (v, v_bar, p, q, tensor, steps) is stored as consecutive
 // planes so every load of a warp is a coalesced 128-byte line.
 
+#include <stdlib.h>
+
 #include "pd_math.cuh"
 #include "warp_math.cuh"
 
 namespace fsb {
 
 constexpr int kBX = 32, kBY = 8;
+constexpr bool kSplitDefault = true;  // measured faster at 1024^2, 512^2 and 256^2 (C3)
 
 struct PD {
   int h, w;
@@ -360,9 +363,64 @@ int warp_sample_internal(const fsb_level* L, cudaStream_t st) {
   return launch_status();
 }
 
+// Split prologue for large levels: the samples at x + w once per pixel (no
+// halo re-sampling), then I_u from the sampled image in global memory (L1/L2
+// resident) in a second kernel. Same arithmetic as k_warp_prologue.
+__global__ void __launch_bounds__(256) k_sample_px(fsb_level L) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= L.w || y >= L.h) return;
+  const size_t i = (size_t)y * L.w + x;
+  float iw = 0.f;
+  bool iok = false, dok = false;
+  float2 d = make_float2(0.f, 0.f);
+  if (L.mask[i]) {
+    const SampleSrc S{L.i1, L.mask, L.traj, L.traj_ok, reinterpret_cast<const float4*>(L.packed),
+                      L.full16, L.h, L.w};
+    warp_sample_px(S, x, y, reinterpret_cast<const float2*>(L.wv)[i], true, iw, iok, d, dok);
+  }
+  L.i1w[i] = iw;
+  L.i1w_ok[i] = iok;
+  reinterpret_cast<float2*>(L.dirs)[i] = d;
+  L.dir_ok[i] = dok;
+}
+
+__global__ void __launch_bounds__(256) k_iu_px(fsb_level L) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= L.w || y >= L.h) return;
+  const size_t i = (size_t)y * L.w + x;
+  float iu = 0.f, rho0 = 0.f;
+  if (L.i1w_ok[i] && L.dir_ok[i]) {
+    const float2 d = reinterpret_cast<const float2*>(L.dirs)[i];
+    int ix, iy;
+    float fx, fy, ahead;
+    if (split_off(x, y, d.x, d.y, L.h, L.w, ix, iy, fx, fy) &&
+        bicubic_at<1, float, true>(L.i1w, L.i1w_ok, L.h, L.w, ix, iy, fx, fy, &ahead)) {
+      const float iw = L.i1w[i];
+      iu = ahead - iw;
+      rho0 = iw - L.i0[i];
+    }
+  }
+  L.iu[i] = iu;
+  L.rho0[i] = rho0;
+}
+
 int warp_prologue_internal(const fsb_level* L, cudaStream_t st) {
+  static int mode = -1;  // FSB_PROLOGUE=fused|split (tuning); default by level size
+  if (mode < 0) {
+    const char* e = getenv("FSB_PROLOGUE");
+    mode = e ? (e[0] == 's' ? 1 : (e[0] == 'f' ? 2 : 0)) : 0;
+  }
+  const bool big = (size_t)L->w * L->h >= (size_t)512 * 512;
+  if (mode == 1 || (mode == 0 && kSplitDefault)) {
+    dim3 blk(kBX, kBY), grd = grid2d(L->w, L->h, blk);
+    k_sample_px<<<grd, blk, 0, st>>>(*L);
+    k_iu_px<<<grd, blk, 0, st>>>(*L);
+    return launch_status();
+  }
   // small levels: 16 x 16 tiles so the grid still spreads over the SMs
-  if ((size_t)L->w * L->h >= (size_t)512 * 512) {
+  if (big) {
     dim3 grd((L->w + 31) / 32, (L->h + 31) / 32);
     k_warp_prologue<32, 32><<<grd, 256, 0, st>>>(*L);
   } else {
