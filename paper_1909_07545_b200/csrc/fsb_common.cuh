@@ -301,6 +301,57 @@ FSB_INLINE bool bicubic_bits(const TF* __restrict__ field, unsigned okb, int w, 
   return true;
 }
 
+// bicubic_bits on 16 tap values already in registers (t[4a+b], a = dy+1, b =
+// dx+1; invalid taps may hold anything): same branches and the same operation
+// order as bicubic_bits, hence the same result.
+FSB_INLINE bool bicubic_regs(const float t[16], unsigned okb, float fx, float fy, float& out) {
+  if (okb == 0) return false;
+  if (okb == 0xFFFFu) {
+    float wx[4], wy[4];
+    cubic_weights(fx, wx);
+    cubic_weights(fy, wy);
+    float cub = 0.f;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) cub += (wy[a] * wx[b]) * t[4 * a + b];
+    out = cub;
+    return true;
+  }
+  const float bx[2] = {1.f - fx, fx};
+  const float by[2] = {1.f - fy, fy};
+  float bil = 0.f, bws = 0.f;
+#pragma unroll
+  for (int a = 1; a <= 2; ++a)
+#pragma unroll
+    for (int b = 1; b <= 2; ++b)
+      if (okb >> (4 * a + b) & 1u) {
+        const float bw = by[a - 1] * bx[b - 1];
+        bil += bw * t[4 * a + b];
+        bws += bw;
+      }
+  if (bws > 1e-12f) {
+    out = bil / bws;
+    return true;
+  }
+  float nd2 = INFINITY;
+  int best = 0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (okb >> (4 * a + b) & 1u) {
+        const float ddx = float(b - 1) - fx, ddy = float(a - 1) - fy;
+        const float d2 = ddx * ddx + ddy * ddy;
+        if (d2 < nd2) { nd2 = d2; best = 4 * a + b; }
+      }
+  float v = t[0];
+#pragma unroll
+  for (int k = 1; k < 16; ++k) v = best == k ? t[k] : v;
+  out = v;
+  return true;
+}
+
 // kGlobal = false reads field and mask through generic loads (shared-memory tiles).
 // The 16 tap validities are gathered first (bit 4a+b, scan order dy outer / dx
 // inner); the all-valid case is a plain Catmull-Rom sum, the fallbacks visit only

@@ -379,7 +379,9 @@ __global__ void __launch_bounds__(256) k_sample_px(fsb_level L) {
                       L.full16, L.h, L.w};
     warp_sample_px(S, x, y, reinterpret_cast<const float2*>(L.wv)[i], true, iw, iok, d, dok);
   }
-  L.i1w[i] = iw;
+  // i1w is stored NaN where invalid (warp_ok & mask false): k_iu_px reads the
+  // tap validity from the values themselves, one load per tap
+  L.i1w[i] = iok ? iw : __int_as_float(0x7fc00000);
   L.i1w_ok[i] = iok;
   reinterpret_cast<float2*>(L.dirs)[i] = d;
   L.dir_ok[i] = dok;
@@ -391,15 +393,31 @@ __global__ void __launch_bounds__(256) k_iu_px(fsb_level L) {
   if (x >= L.w || y >= L.h) return;
   const size_t i = (size_t)y * L.w + x;
   float iu = 0.f, rho0 = 0.f;
-  if (L.i1w_ok[i] && L.dir_ok[i]) {
+  const float iw = L.i1w[i];
+  if (!isnan(iw) && L.dir_ok[i]) {
     const float2 d = reinterpret_cast<const float2*>(L.dirs)[i];
     int ix, iy;
-    float fx, fy, ahead;
-    if (split_off(x, y, d.x, d.y, L.h, L.w, ix, iy, fx, fy) &&
-        bicubic_at<1, float, true>(L.i1w, L.i1w_ok, L.h, L.w, ix, iy, fx, fy, &ahead)) {
-      const float iw = L.i1w[i];
-      iu = ahead - iw;
-      rho0 = iw - L.i0[i];
+    float fx, fy;
+    if (split_off(x, y, d.x, d.y, L.h, L.w, ix, iy, fx, fy)) {
+      // 16 taps (out-of-image taps invalid), validity = not NaN
+      float t[16];
+      unsigned okb = 0;
+      const bool inner = ix >= 1 && ix + 2 < L.w && iy >= 1 && iy + 2 < L.h;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int r = iy + a - 1, c = ix + b - 1;
+          const bool in = inner || ((unsigned)r < (unsigned)L.h && (unsigned)c < (unsigned)L.w);
+          const float v = in ? __ldg(L.i1w + (size_t)r * L.w + c) : __int_as_float(0x7fc00000);
+          t[4 * a + b] = v;
+          okb |= (isnan(v) ? 0u : 1u) << (4 * a + b);
+        }
+      float ahead;
+      if (bicubic_regs(t, okb, fx, fy, ahead)) {
+        iu = ahead - iw;
+        rho0 = iw - L.i0[i];
+      }
     }
   }
   L.iu[i] = iu;
