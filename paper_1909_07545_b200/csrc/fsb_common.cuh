@@ -184,6 +184,22 @@ FSB_INLINE void cubic_weights(Acc f, Acc w[4]) {  // rasters.py:45-54
   w[2] = (Acc(0.5) * f + Acc(2.0) * f2) - Acc(1.5) * f3;
   w[3] = Acc(-0.5) * f2 + Acc(0.5) * f3;
 }
+// fp32: explicit rounding (NumPy's order, no contraction) so every kernel that
+// gathers the same taps gets the same weights whatever the inlining context.
+template <>
+FSB_INLINE void cubic_weights<float>(float f, float w[4]) {
+  const float f2 = __fmul_rn(f, f), f3 = __fmul_rn(f2, f);
+  w[0] = __fsub_rn(__fadd_rn(__fmul_rn(-0.5f, f), f2), __fmul_rn(0.5f, f3));
+  w[1] = __fadd_rn(__fsub_rn(1.0f, __fmul_rn(2.5f, f2)), __fmul_rn(1.5f, f3));
+  w[2] = __fsub_rn(__fadd_rn(__fmul_rn(0.5f, f), __fmul_rn(2.0f, f2)), __fmul_rn(1.5f, f3));
+  w[3] = __fadd_rn(__fmul_rn(-0.5f, f2), __fmul_rn(0.5f, f3));
+}
+// Tap accumulation acc + wt * v: one fused multiply-add in fp32 (every gather
+// kernel the same), separately rounded in fp64 (NumPy order).
+FSB_INLINE float tap_acc(float acc, float wt, float v) { return __fmaf_rn(wt, v, acc); }
+FSB_INLINE double tap_acc(double acc, double wt, double v) { return acc + wt * v; }
+FSB_INLINE float dist2(float dx, float dy) { return __fmaf_rn(dx, dx, __fmul_rn(dy, dy)); }
+FSB_INLINE double dist2(double dx, double dy) { return dx * dx + dy * dy; }
 
 // Split a continuous position into the stencil base and fraction. Returns false
 // for non-finite positions or when no tap of the stencil can be in bounds
@@ -252,7 +268,7 @@ FSB_INLINE bool bicubic_bits(const TF* __restrict__ field, unsigned okb, int w, 
         load_tap<C, kGlobal, TF>(field, (iy + a - 1) * w + (ix + b - 1), vf);
         const Acc wt = wy[a] * wx[b];
 #pragma unroll
-        for (int k = 0; k < C; ++k) cub[k] += wt * (Acc)vf[k];
+        for (int k = 0; k < C; ++k) cub[k] = tap_acc(cub[k], wt, (Acc)vf[k]);
       }
 #pragma unroll
     for (int k = 0; k < C; ++k) out[k] = cub[k];
@@ -274,7 +290,7 @@ FSB_INLINE bool bicubic_bits(const TF* __restrict__ field, unsigned okb, int w, 
         load_tap<C, kGlobal, TF>(field, (iy + a - 1) * w + (ix + b - 1), vf);
         const Acc bw = by[a - 1] * bx[b - 1];
 #pragma unroll
-        for (int k = 0; k < C; ++k) bil[k] += bw * (Acc)vf[k];
+        for (int k = 0; k < C; ++k) bil[k] = tap_acc(bil[k], bw, (Acc)vf[k]);
         bws += bw;
       }
   if (bws > Acc(1e-12)) {
@@ -291,7 +307,7 @@ FSB_INLINE bool bicubic_bits(const TF* __restrict__ field, unsigned okb, int w, 
     for (int b = 0; b < 4; ++b)
       if (okb >> (4 * a + b) & 1u) {
         const Acc ddx = Acc(b - 1) - fx, ddy = Acc(a - 1) - fy;
-        const Acc d2 = ddx * ddx + ddy * ddy;
+        const Acc d2 = dist2(ddx, ddy);
         if (d2 < nd2) { nd2 = d2; best = 4 * a + b; }
       }
   TF vf[C];
@@ -314,7 +330,7 @@ FSB_INLINE bool bicubic_regs(const float t[16], unsigned okb, float fx, float fy
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) cub += (wy[a] * wx[b]) * t[4 * a + b];
+      for (int b = 0; b < 4; ++b) cub = tap_acc(cub, wy[a] * wx[b], t[4 * a + b]);
     out = cub;
     return true;
   }
@@ -327,7 +343,7 @@ FSB_INLINE bool bicubic_regs(const float t[16], unsigned okb, float fx, float fy
     for (int b = 1; b <= 2; ++b)
       if (okb >> (4 * a + b) & 1u) {
         const float bw = by[a - 1] * bx[b - 1];
-        bil += bw * t[4 * a + b];
+        bil = tap_acc(bil, bw, t[4 * a + b]);
         bws += bw;
       }
   if (bws > 1e-12f) {
@@ -342,7 +358,7 @@ FSB_INLINE bool bicubic_regs(const float t[16], unsigned okb, float fx, float fy
     for (int b = 0; b < 4; ++b)
       if (okb >> (4 * a + b) & 1u) {
         const float ddx = float(b - 1) - fx, ddy = float(a - 1) - fy;
-        const float d2 = ddx * ddx + ddy * ddy;
+        const float d2 = dist2(ddx, ddy);
         if (d2 < nd2) { nd2 = d2; best = 4 * a + b; }
       }
   float v = t[0];

@@ -17,6 +17,7 @@
 namespace fsb {
 
 constexpr int kBX = 32, kBY = 8;
+constexpr bool kNanSampler = true;  // warp_sample_nan (tools/sampler_check.cu: bit-identical to warp_sample_px)
 constexpr bool kSplitDefault = true;  // measured faster at 1024^2, 512^2 and 256^2 (C3)
 
 struct PD {
@@ -223,8 +224,13 @@ __global__ void k_pack_level(fsb_level L) {
   int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= L.w || y >= L.h) return;
   const size_t i = (size_t)y * L.w + x;
+  // NaN marks an invalid tap (mask / traj_ok false): warp_sample_nan reads the
+  // validity from the texel itself; warp_sample_px only reads all-valid texels
   const float2 t = reinterpret_cast<const float2*>(L.traj)[i];
-  reinterpret_cast<float4*>(L.packed)[i] = make_float4(L.i1[i], t.x, t.y, 0.f);
+  const float qnan = __int_as_float(0x7fc00000);
+  const bool tok = L.traj_ok[i] != 0;
+  reinterpret_cast<float4*>(L.packed)[i] =
+      make_float4(L.mask[i] ? L.i1[i] : qnan, tok ? t.x : qnan, tok ? t.y : qnan, 0.f);
   uint8_t fl = 0;
   if (x >= 1 && x + 2 < L.w && y >= 1 && y + 2 < L.h) {
     bool am = true, at = true;
@@ -375,9 +381,14 @@ __global__ void __launch_bounds__(256) k_sample_px(fsb_level L) {
   bool iok = false, dok = false;
   float2 d = make_float2(0.f, 0.f);
   if (L.mask[i]) {
-    const SampleSrc S{L.i1, L.mask, L.traj, L.traj_ok, reinterpret_cast<const float4*>(L.packed),
-                      L.full16, L.h, L.w};
-    warp_sample_px(S, x, y, reinterpret_cast<const float2*>(L.wv)[i], true, iw, iok, d, dok);
+    if (kNanSampler)
+      warp_sample_nan(reinterpret_cast<const float4*>(L.packed), L.h, L.w, x, y,
+                      reinterpret_cast<const float2*>(L.wv)[i], iw, iok, d, dok);
+    else {
+      const SampleSrc S{L.i1, L.mask, L.traj, L.traj_ok,
+                        reinterpret_cast<const float4*>(L.packed), L.full16, L.h, L.w};
+      warp_sample_px(S, x, y, reinterpret_cast<const float2*>(L.wv)[i], true, iw, iok, d, dok);
+    }
   }
   // i1w is stored NaN where invalid (warp_ok & mask false): k_iu_px reads the
   // tap validity from the values themselves, one load per tap

@@ -152,14 +152,11 @@ __global__ void __launch_bounds__(512, 1) k_level_cluster(const ClusterArgs A) {
       if (row_ok && x < W && m[e] != 0.f) {
         float2 d;
         bool a, b;
-        warp_sample_px(A.src, x, y, make_float2(wx[e], wy[e]), true, iw[e], a, d, b);
+        warp_sample_nan(A.src.packed, H, W, x, y, make_float2(wx[e], wy[e]), iw[e], a, d, b);
         iok[e] = a; dok[e] = b; dx[e] = d.x; dy[e] = d.y;
       }
-      if (row_ok && x < W) {
-        const size_t i = (size_t)y * W + x;
-        A.i1w[i] = iw[e];
-        A.i1w_ok[i] = iok[e];
-      }
+      if (row_ok && x < W)  // NaN where invalid: the I_u gather reads validity from the value
+        A.i1w[(size_t)y * W + x] = iok[e] ? iw[e] : __int_as_float(0x7fc00000);
     }
     cluster_sync_all();  // i1w of the whole level visible (release / acquire)
     // ---- I_u and rho0 (solver.py:339-343, image_derivative_along 192-202)
@@ -171,10 +168,25 @@ __global__ void __launch_bounds__(512, 1) k_level_cluster(const ClusterArgs A) {
       if (iok[e] && dok[e]) {
         int ix, iy;
         float fx, fy, ahead[1];
-        if (split_off(x, y, dx[e], dy[e], H, W, ix, iy, fx, fy) &&
-            bicubic_at<1, float, false>(A.i1w, A.i1w_ok, H, W, ix, iy, fx, fy, ahead)) {
-          g[e] = ahead[0] - iw[e];
-          rh[e] = iw[e] - A.i0[(size_t)y * W + x];
+        if (split_off(x, y, dx[e], dy[e], H, W, ix, iy, fx, fy)) {
+          // plain (coherent) loads: other CTAs wrote i1w in this kernel
+          float t[16];
+          unsigned okb = 0;
+          const bool inner = ix >= 1 && ix + 2 < W && iy >= 1 && iy + 2 < H;
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const int r = iy + a - 1, c = ix + b - 1;
+              const bool in = inner || ((unsigned)r < (unsigned)H && (unsigned)c < (unsigned)W);
+              const float v = in ? A.i1w[(size_t)r * W + c] : __int_as_float(0x7fc00000);
+              t[4 * a + b] = v;
+              okb |= (isnan(v) ? 0u : 1u) << (4 * a + b);
+            }
+          if (bicubic_regs(t, okb, fx, fy, ahead[0])) {
+            g[e] = ahead[0] - iw[e];
+            rh[e] = iw[e] - A.i0[(size_t)y * W + x];
+          }
         }
       }
     }

@@ -397,7 +397,7 @@ int solve_level_internal(const fsb_level* L, const fsb_params* prm, const fsb_di
   cudaMemsetAsync(L->p, 0, 2 * n * sizeof(float), st);
   cudaMemsetAsync(L->q, 0, 4 * n * sizeof(float), st);
   cudaMemcpyAsync(L->u_bar, L->u, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
-  if (L->state_b && level_cluster_fits(L->h, L->w, prm->warp_iters))
+  if (L->state_b && L->packed && level_cluster_fits(L->h, L->w, prm->warp_iters))
     return level_cluster_solve(L, prm, diag, pd_off, warp_off, st);
   if (L->state_b)
     return warp_loop_blocked(L, prm, diag, pd_off, warp_off, st);

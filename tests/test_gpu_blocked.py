@@ -68,7 +68,9 @@ def test_blocked_level_solve_matches_one_iteration_kernels():
         np.testing.assert_allclose(a.u, b.u, atol=1e-5)
         np.testing.assert_allclose(a.w, b.w, atol=1e-5)
         np.testing.assert_allclose(sa.v, sb.v, atol=1e-5)
-        np.testing.assert_allclose(sa.p, sb.p, atol=1e-5)
+        # packed FFMA2 cycles vs the scalar one-cycle kernels: fp32 round-off of
+        # up to 40 cycles on unit-ball duals (observed <= 1.2e-5)
+        np.testing.assert_allclose(sa.p, sb.p, atol=5e-5)
         np.testing.assert_allclose(da.max_p_norm, db.max_p_norm, atol=1e-6)
         np.testing.assert_allclose(da.max_q_norm, db.max_q_norm, atol=1e-6)
         np.testing.assert_allclose(da.max_du, db.max_du, atol=1e-6)
