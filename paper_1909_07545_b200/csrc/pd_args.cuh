@@ -33,6 +33,8 @@ struct BlockArgs {
   float* diag_p; float* diag_q; float* diag_du; double* partials;
   // TMA kernel work list (pd_tma_tile_list), nullptr = every tile
   const int* tile_list;
+  // FIN launches: also store u_bar / v_bar (only the level's last warp needs them)
+  int store_bars;
 };
 
 // TMA descriptors of one level for the persistent kernel (pd_tma.cu): the two

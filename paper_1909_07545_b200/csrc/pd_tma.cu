@@ -76,6 +76,12 @@ FSB_INLINE void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int
       : "memory");
 }
 
+#ifndef FSB_ALIGNED_LOAD
+#define FSB_ALIGNED_LOAD 0  // measured slower: the unpack shuffles cost more than the 2-way bank conflicts
+#endif
+#ifndef FSB_ALIGNED_STORE
+#define FSB_ALIGNED_STORE 1
+#endif
 constexpr int kNW = 16, kPY = 2, kEW = 64, kEH = kNW * kPY;
 constexpr int kStatePlanes = 12, kConstPlanes = 10;
 // TMA needs the box's innermost start coordinate 16-byte aligned (measured on
@@ -149,13 +155,29 @@ __global__ void __launch_bounds__(kNW * 32, 1)
     f2 exf[PY], eyf[PY];
     unsigned mbits = 0;  // mask of the two pixels of row j at bits 2j, 2j+1
     const f2 a1 = mk2(A.alpha1, A.alpha1);
-    const int shift = ox - (ox & ~3);  // staging column of tile column 0
+    const int shift = ox - (ox & ~3);  // staging column of tile column 0 (parity of R)
 #pragma unroll
     for (int j = 0; j < PY; ++j) {
       const int r = r0 + j;
       const int o = r * kBoxW + c0 + shift;
-      auto S2 = [&](int plane) { return mk2(st[plane * kPlane + o], st[plane * kPlane + o + 1]); };
-      auto C2 = [&](int plane) { return mk2(cs[plane * kPlane + o], cs[plane * kPlane + o + 1]); };
+      // Pixel pair (c0, c0+1) of a staged plane. Even R: 8-B aligned, one LDS.64.
+      // Odd R: the aligned pair is (c0+1, c0+2); c0 comes from the lane below
+      // by shuffle (lane 0 reads it directly) — conflict-free 64-bit loads
+      // instead of two stride-2 scalar loads.
+      auto pair = [&](const float* pl) -> f2 {
+        if constexpr (!FSB_ALIGNED_LOAD) {
+          return mk2(pl[o], pl[o + 1]);
+        } else if constexpr ((R & 1) == 0) {
+          return *reinterpret_cast<const f2*>(pl + o);
+        } else {
+          const f2 q = *reinterpret_cast<const f2*>(pl + o + 1);
+          float left = __shfl_up_sync(FULL, q.y, 1);
+          if (lane == 0) left = pl[o];
+          return mk2(left, q.x);
+        }
+      };
+      auto S2 = [&](int plane) { return pair(st + plane * kPlane); };
+      auto C2 = [&](int plane) { return pair(cs + plane * kPlane); };
       u[j] = S2(SU); v0[j] = S2(SV0); v1[j] = S2(SV1);
       p0[j] = S2(SP0); p1[j] = S2(SP1);
       q0[j] = S2(SQ0); q1[j] = S2(SQ1); q2[j] = S2(SQ2); q3[j] = S2(SQ3);
@@ -296,26 +318,28 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       }
     }
 
-    // ---- epilogue + store of the interior
+    // ---- epilogue + store of the interior. Per-pixel work (clip, w update,
+    // diagnostics) in the lane's own pair; the stores go out as 8-B aligned
+    // pairs: even R owns them, odd R pairs its .y with the next lane's .x.
     float dmax = 0.f;
     double dsum = 0.0;
 #pragma unroll
     for (int j = 0; j < PY; ++j) {
       const int r = r0 + j, gy = oy + r;
-      if (r < R || r >= EH - R || (unsigned)gy >= (unsigned)A.h) continue;
+      const bool row_in = r >= R && r < EH - R && (unsigned)gy < (unsigned)A.h;
+      f2 U2 = u[j], UB2 = ub[j];
+      if (FIN) {  // solver.py:356-360
+        float uu[2] = {u[j].x, u[j].y};
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = c0 + e, gx = ox + c;
-        if (c < R || c >= kEW - R || (unsigned)gx >= (unsigned)A.w) continue;
-        const size_t gi = (size_t)gy * A.w + gx;
-        float uu = e ? u[j].y : u[j].x, ubb = e ? ub[j].y : ub[j].x;
-        if (FIN) {  // solver.py:356-360
+        for (int e = 0; e < 2; ++e) {
+          const int c = c0 + e, gx = ox + c;
+          if (!row_in || c < R || c >= kEW - R || (unsigned)gx >= (unsigned)A.w) continue;
+          const size_t gi = (size_t)gy * A.w + gx;
           const float uom = e ? uo[j].y : uo[j].x;
           const bool mk = (mbits >> (2 * j + e)) & 1u;
-          float du = fminf(fmaxf(uu - uom, -A.du_max), A.du_max);
+          float du = fminf(fmaxf(uu[e] - uom, -A.du_max), A.du_max);
           if (!mk) du = 0.f;
-          uu = uom + du;
-          ubb = uu;
+          uu[e] = uom + du;
           const float2 d = reinterpret_cast<const float2*>(A.dirs)[gi];
           float2 wv = reinterpret_cast<float2*>(A.wv)[gi];
           wv.x = wv.x + du * d.x;
@@ -324,20 +348,47 @@ __global__ void __launch_bounds__(kNW * 32, 1)
           dmax = fmaxf(dmax, fabsf(du));
           dsum += (double)fabsf(du);
         }
-        if (LIN) A.u_omega[gi] = e ? uo[j].y : uo[j].x;
-        A.dst.u[gi] = uu;
-        A.dst.ub[gi] = ubb;
-        A.dst.v[gi] = e ? v0[j].y : v0[j].x;
-        A.dst.v[n + gi] = e ? v1[j].y : v1[j].x;
-        A.dst.vb[gi] = e ? vb0[j].y : vb0[j].x;
-        A.dst.vb[n + gi] = e ? vb1[j].y : vb1[j].x;
-        A.dst.p[gi] = e ? p0[j].y : p0[j].x;
-        A.dst.p[n + gi] = e ? p1[j].y : p1[j].x;
-        A.dst.q[gi] = e ? q0[j].y : q0[j].x;
-        A.dst.q[n + gi] = e ? q1[j].y : q1[j].x;
-        A.dst.q[2 * n + gi] = e ? q2[j].y : q2[j].x;
-        A.dst.q[3 * n + gi] = e ? q3[j].y : q3[j].x;
+        U2 = mk2(uu[0], uu[1]);
+        UB2 = U2;  // u_bar = u after the clip
       }
+      // aligned pair start (tile column) of this lane and its store predicate
+      constexpr bool kOddPairs = FSB_ALIGNED_STORE && (R & 1);
+      const int cs0 = kOddPairs ? c0 + 1 : c0;
+      const int gxs = ox + cs0;
+      // interior columns [R, kEW - R) split exactly into aligned pairs (gxs even,
+      // w % 4 == 0, so gxs + 1 < w whenever gxs < w)
+      const bool st_ok = row_in && cs0 >= R && cs0 + 1 < kEW - R && gxs < A.w;
+      const size_t gs = (size_t)gy * A.w + gxs;
+      auto put = [&](float* plane, f2 v) {
+        if constexpr (kOddPairs) {
+          const f2 o2 = mk2(v.y, __shfl_down_sync(FULL, v.x, 1));
+          if (st_ok) *reinterpret_cast<f2*>(plane + gs) = o2;
+        } else if constexpr (FSB_ALIGNED_STORE) {
+          if (st_ok) *reinterpret_cast<f2*>(plane + gs) = v;
+        } else {
+          const size_t g0 = (size_t)gy * A.w + (ox + c0);
+          if (row_in && c0 >= R && c0 < kEW - R && ox + c0 < A.w) plane[g0] = v.x;
+          if (row_in && c0 + 1 >= R && c0 + 1 < kEW - R && ox + c0 + 1 < A.w) plane[g0 + 1] = v.y;
+        }
+      };
+      if (LIN) put(A.u_omega, uo[j]);
+      put(A.dst.u, U2);
+      // after a warp's last cycle u_bar / v_bar are dead (the next warp start
+      // resets them, solver.py:344-346) unless this is the level's last warp
+      const bool bars = !FIN || A.store_bars;
+      if (bars) put(A.dst.ub, UB2);
+      put(A.dst.v, v0[j]);
+      put(A.dst.v + n, v1[j]);
+      if (bars) {
+        put(A.dst.vb, vb0[j]);
+        put(A.dst.vb + n, vb1[j]);
+      }
+      put(A.dst.p, p0[j]);
+      put(A.dst.p + n, p1[j]);
+      put(A.dst.q, q0[j]);
+      put(A.dst.q + n, q1[j]);
+      put(A.dst.q + 2 * n, q2[j]);
+      put(A.dst.q + 3 * n, q3[j]);
     }
     if (FIN && DIAG && A.diag_du) {
       __shared__ double red_s[NW];

@@ -319,6 +319,7 @@ int warp_loop_blocked(const fsb_level* L, const fsb_params* prm, const fsb_diag*
       A.diag_p = dpq ? diag->max_p_norm + pd_off + (int64_t)wi * K + done : nullptr;
       A.diag_q = dpq ? diag->max_q_norm + pd_off + (int64_t)wi * K + done : nullptr;
       A.diag_du = (fin && ddu) ? diag->max_du + warp_off + wi : nullptr;
+      A.store_bars = wi == N - 1;
       rc = tma ? pd_tma_launch(A, maps, cur, halo, lin, fin, st, &nblocks)
                : pd_launch(A, halo, lin, fin, st, &nblocks);
       if (rc) return rc;
