@@ -410,9 +410,9 @@ __global__ void __launch_bounds__(256) k_iu_px(fsb_level L) {
     int ix, iy;
     float fx, fy;
     if (split_off(x, y, d.x, d.y, L.h, L.w, ix, iy, fx, fy)) {
-      // 16 taps (out-of-image taps invalid), validity = not NaN
+      // 16 taps (out-of-image taps invalid), validity = not NaN; the validity
+      // bits are only formed when the Catmull-Rom sum says a tap is invalid
       float t[16];
-      unsigned okb = 0;
       const bool inner = ix >= 1 && ix + 2 < L.w && iy >= 1 && iy + 2 < L.h;
 #pragma unroll
       for (int a = 0; a < 4; ++a)
@@ -420,12 +420,23 @@ __global__ void __launch_bounds__(256) k_iu_px(fsb_level L) {
         for (int b = 0; b < 4; ++b) {
           const int r = iy + a - 1, c = ix + b - 1;
           const bool in = inner || ((unsigned)r < (unsigned)L.h && (unsigned)c < (unsigned)L.w);
-          const float v = in ? __ldg(L.i1w + (size_t)r * L.w + c) : __int_as_float(0x7fc00000);
-          t[4 * a + b] = v;
-          okb |= (isnan(v) ? 0u : 1u) << (4 * a + b);
+          t[4 * a + b] = in ? __ldg(L.i1w + (size_t)r * L.w + c) : __int_as_float(0x7fc00000);
         }
-      float ahead;
-      if (bicubic_regs(t, okb, fx, fy, ahead)) {
+      float wx[4], wy[4], cub = 0.f;
+      cubic_weights(fx, wx);
+      cubic_weights(fy, wy);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) cub = tap_acc(cub, wy[a] * wx[b], t[4 * a + b]);
+      unsigned okb = 0xFFFFu;
+      if (isnan(cub)) {
+        okb = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) okb |= (isnan(t[k]) ? 0u : 1u) << k;
+      }
+      float ahead = cub;
+      if (okb == 0xFFFFu || bicubic_regs(t, okb, fx, fy, ahead)) {
         iu = ahead - iw;
         rho0 = iw - L.i0[i];
       }

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(512, 1) k_level_cluster(const ClusterArgs A) {
       if (row_ok && x < W && m[e] != 0.f) {
         float2 d;
         bool a, b;
-        warp_sample_nan(A.src.packed, H, W, x, y, make_float2(wx[e], wy[e]), iw[e], a, d, b);
+        warp_sample_nan_bits(A.src.packed, H, W, x, y, make_float2(wx[e], wy[e]), iw[e], a, d, b);
         iok[e] = a; dok[e] = b; dx[e] = d.x; dy[e] = d.y;
       }
       if (row_ok && x < W)  // NaN where invalid: the I_u gather reads validity from the value

@@ -134,12 +134,113 @@ FSB_INLINE void packed_fallback(const float4* __restrict__ P, int w, int ix, int
   for (int k = 0; k < C; ++k) out[k] = __ldg(t + k);
 }
 
+// Validity bits (bit 4a+b) of channel `ch` of the 16 taps around (ix, iy):
+// in the image and not NaN.
+FSB_INLINE unsigned packed_bits(const float4* __restrict__ P, int h, int w, int ix, int iy,
+                                int ch) {
+  const float* base = reinterpret_cast<const float*>(P) + ch;
+  unsigned okb = 0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int r = iy + a - 1, c = ix + b - 1;
+      const bool in = (unsigned)r < (unsigned)h && (unsigned)c < (unsigned)w;
+      const bool v = in && !isnan(__ldg(base + 4 * ((size_t)r * w + c)));
+      okb |= (v ? 1u : 0u) << (4 * a + b);
+    }
+  return okb;
+}
+
+// warp_sample_px (mk = true) on NaN-encoded packed texels {mask ? i1 : NaN,
+// traj_ok ? traj : NaN, 0} (k_pack_level): one 16-B load per tap serves both
+// gathers. The Catmull-Rom sums are formed unconditionally; an invalid tap
+// makes its channel's sum NaN (w * NaN = NaN, also for w = 0), so the common
+// all-valid case needs no per-tap validity work, and only stencils touching
+// an invalid tap re-read their validity and take the bicubic_bits fallback
+// (L1 hits). Same results as warp_sample_px (tools/sampler_check.cu).
+// kInnerFast: separate unchecked tap loop for stencils inside the image (the
+// common case; larger code, used by the standalone sampling kernel).
+template <bool kInnerFast = true>
+FSB_INLINE void warp_sample_nan(const float4* __restrict__ P, int h, int w, int x, int y,
+                                float2 wv, float& i1w, bool& i1w_ok, float2& dir, bool& dir_ok) {
+  i1w = 0.f;
+  i1w_ok = false;
+  dir = make_float2(0.f, 0.f);
+  dir_ok = false;
+  int ix, iy;
+  float fx, fy;
+  if (!split_off(x, y, wv.x, wv.y, h, w, ix, iy, fx, fy)) return;
+  float wx[4], wy[4];
+  cubic_weights(fx, wx);
+  cubic_weights(fy, wy);
+  const float qnan = __int_as_float(0x7fc00000);
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+  if (kInnerFast && ix >= 1 && ix + 2 < w && iy >= 1 && iy + 2 < h) {
+    const float4* t0 = P + (size_t)(iy - 1) * w + (ix - 1);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const float4 t = __ldg(t0 + (size_t)a * w + b);
+        const float wt = wy[a] * wx[b];
+        a0 = tap_acc(a0, wt, t.x);
+        a1 = tap_acc(a1, wt, t.y);
+        a2 = tap_acc(a2, wt, t.z);
+      }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int r = iy + a - 1, c = ix + b - 1;
+        const bool in = (unsigned)r < (unsigned)h && (unsigned)c < (unsigned)w;
+        const float4 t = in ? __ldg(P + (size_t)r * w + c) : make_float4(qnan, qnan, qnan, 0.f);
+        const float wt = wy[a] * wx[b];
+        a0 = tap_acc(a0, wt, t.x);
+        a1 = tap_acc(a1, wt, t.y);
+        a2 = tap_acc(a2, wt, t.z);
+      }
+  }
+  if (!isnan(a0)) {
+    i1w = a0;
+    i1w_ok = true;
+  } else {
+    const unsigned okb = packed_bits(P, h, w, ix, iy, 0);
+    if (okb) {
+      float v[1];
+      packed_fallback<1>(P, w, ix, iy, fx, fy, okb, 0, v);
+      i1w = v[0];
+      i1w_ok = true;
+    }
+  }
+  bool tok = true;
+  float d0 = a1, d1 = a2;
+  if (isnan(a1)) {
+    const unsigned okb = packed_bits(P, h, w, ix, iy, 1);
+    tok = okb != 0;
+    if (tok) {
+      float v[2];
+      packed_fallback<2>(P, w, ix, iy, fx, fy, okb, 1, v);
+      d0 = v[0];
+      d1 = v[1];
+    }
+  }
+  float e0, e1;
+  if (tok && unit_dir(d0, d1, e0, e1)) {
+    dir = make_float2(e0, e1);
+    dir_ok = true;
+  }
+}
+
+// Per-tap-validity variant of warp_sample_nan (validity bits gathered with the
+// loads; preferred on small levels where many stencils touch the mask edge).
 // warp_sample_px (mk = true) on NaN-encoded packed texels {mask ? i1 : NaN,
 // traj_ok ? traj : NaN, 0} (k_pack_level): one 16-B load per tap serves both
 // gathers and carries their validity, so there is no separate mask / flag
 // gather and no divergent slow path; the rare partial stencils re-read their
 // valid taps (L1 hits) in the fallback. Same results as warp_sample_px.
-FSB_INLINE void warp_sample_nan(const float4* __restrict__ P, int h, int w, int x, int y,
+FSB_INLINE void warp_sample_nan_bits(const float4* __restrict__ P, int h, int w, int x, int y,
                                 float2 wv, float& i1w, bool& i1w_ok, float2& dir, bool& dir_ok) {
   i1w = 0.f;
   i1w_ok = false;
