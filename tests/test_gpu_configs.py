@@ -217,3 +217,47 @@ def test_fp64_path_reproduces_oracle_to_roundoff():
     r1 = solve_pyramid(i0, i1, rig1, prm1, precision="fp64")
     s1 = O.pyramid_solve(i0, i1, rig1, prm1)
     assert np.max(np.abs(r1.u - s1.u)[s1.mask]) <= 1e-8
+
+
+def test_odd_size_pipeline_parity():
+    """A 322x241 unified pair: width % 4 != 0 selects the non-TMA pair kernel
+    fallback, ragged pyramid shapes and partial tiles at every level."""
+    from paper_1909_07545_b200.camera import RelativePose, StereoRig, UnifiedCamera
+    from paper_1909_07545_b200.solver import SolverParams
+    cam0 = UnifiedCamera(width=322, height=241, fx=140.0, fy=141.0, cx=160.3, cy=120.2,
+                         fov=np.pi, xi=0.9)
+    cam1 = UnifiedCamera(width=322, height=241, fx=140.0, fy=141.0, cx=161.0, cy=119.8,
+                         fov=np.pi, xi=0.9)
+    rig = StereoRig(cam0, cam1, RelativePose.from_displacement((0.1, 0.01, 0.0),
+                                                               rotvec=(0.0, 0.02, 0.005)))
+    prm = SolverParams(warp_iters=8, pd_iters=10, pyramid_levels=3, min_width=40)
+    i0, i1 = _render_pair(rig)
+    _parity(rig, prm, i0, i1)
+
+
+def test_c5_headline_invariants():
+    """C5 (2048^2 unified, 7 levels, N=20 x K=10, Huber-TV): the size-independent
+    invariants (determinism, feasible duals, v = 0 for the TV-type regulariser,
+    clipped increments, finite output)."""
+    from paper_1909_07545_b200 import synth as S
+    from paper_1909_07545_b200.camera import RelativePose, StereoRig, UnifiedCamera
+    from paper_1909_07545_b200.solver import Solver, SolverParams
+    cam = UnifiedCamera(width=2048, height=2048, fx=910.0, fy=910.0, cx=1023.5, cy=1023.5,
+                        fov=np.pi, xi=0.9)
+    rig = StereoRig(cam, cam, RelativePose.from_displacement((0.1, 0, 0), rotvec=(0, 0.02, 0.005)))
+    sc = S.default_scene()
+    i0 = S.render_device(sc, rig.cam0)[0].double().cpu().numpy()
+    i1 = S.render_device(sc, rig.cam1, pose=rig.pose)[0].double().cpu().numpy()
+    prm = SolverParams(warp_iters=20, pd_iters=10, pyramid_levels=7, min_width=32,
+                       regularizer="huber")
+    eng = Solver(rig, prm, collect_diagnostics=True)
+    r1 = eng.solve(i0, i1)
+    r2 = eng.solve(i0, i1)
+    assert np.array_equal(r1.u, r2.u) and np.array_equal(r1.w, r2.w)
+    d = r1.diagnostics
+    assert len(d.max_p_norm) == 7 * 20 * 10
+    assert max(d.max_p_norm) <= 1 + 1e-6 and max(d.max_q_norm) == 0.0
+    assert max(d.max_du) <= prm.du_max * (1 + 1e-6)
+    assert not r1.v.any()
+    assert np.isfinite(r1.u).all() and np.isfinite(r1.w).all()
+    assert 0.6 < r1.mask.mean() < 0.9
