@@ -538,16 +538,18 @@ def run_b200(a) -> None:
         e64 = Solver(rig, prm, precision="fp64")
         e64.i0.copy_(img0)
         e64.i1.copy_(img1)
-        e64.run()
+        e64.capture()  # one CUDA graph per frame, as the fp32 path
+        for _ in range(2):
+            e64.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(2):
-            e64.run()
+        for _ in range(3):
+            e64.replay()
         e1.record(stream)
         torch.cuda.synchronize()
-        f64 = {"value": 2 / (e0.elapsed_time(e1) / 1e3), "unit": "frames/s",
-               "path": "fsb_solve_pyramid_f64 (float64 storage + IEEE arithmetic)"}
+        f64 = {"value": 3 / (e0.elapsed_time(e1) / 1e3), "unit": "frames/s",
+               "path": "fsb_solve_pyramid_f64 (float64 storage + IEEE arithmetic), graph replay"}
         del e64
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:

@@ -32,7 +32,7 @@ EXPORTED = (
     "fsb_upsample_state", "fsb_compute_tensor", "fsb_precondition_steps", "fsb_level_partials", "fsb_level_tiles", "fsb_level_setup", "fsb_warp_linearize",
     "fsb_pd_iterate", "fsb_thresholding_step", "fsb_warp_finish", "fsb_solve_level", "fsb_diag_counts",
     "fsb_solve_pyramid_workspace_bytes", "fsb_solve_pyramid",
-    "fsb_solve_pyramid_f64_workspace_bytes", "fsb_solve_pyramid_f64", "fsb_render", "fsb_graph_create", "fsb_graph_launch", "fsb_graph_destroy",
+    "fsb_solve_pyramid_f64_workspace_bytes", "fsb_solve_pyramid_f64", "fsb_render", "fsb_graph_create", "fsb_graph_create_f64", "fsb_graph_launch", "fsb_graph_destroy",
     "fsb_ground_truth", "fsb_error_report", "fsb_error_report_scratch_bytes", "fsb_version",
 )
 
@@ -149,6 +149,9 @@ def lib() -> C.CDLL:
             "fsb_ground_truth": (C.c_int, [P(FsbRig), vp, i32, dbl, vp, vp, vp, vp, sz, vp]),
             "fsb_error_report": (C.c_int, [vp, vp, vp, i64, vp, i32, vp, vp, vp, vp, vp, sz, vp]),
             "fsb_error_report_scratch_bytes": (sz, [i64]),
+            "fsb_graph_create_f64": (C.c_int, [P(FsbRig), P(FsbParams), vp, vp, vp, vp, vp, sz,
+                                               vp, vp, vp, vp, vp, P(FsbDiag), vp,
+                                               P(C.c_void_p), P(C.c_int64)]),
             "fsb_graph_launch": (C.c_int, [vp, vp]),
             "fsb_graph_destroy": (C.c_int, [vp]),
             "fsb_version": (C.c_char_p, []),

@@ -618,18 +618,17 @@ struct fsb_graph {
   cudaGraphExec_t exec;
 };
 
-int fsb_graph_create(const fsb_rig* rig, const fsb_params* prm, const float* i0, const float* i1,
-                     const float* const* traj_dirs, const uint8_t* const* traj_ok,
-                     void* workspace, size_t workspace_bytes, float* u, float* w, float* v,
-                     uint8_t* mask, float* i1c, const fsb_diag* diag, void* stream,
-                     fsb_graph** out, int64_t* n_kernels) {
+}  // extern "C"
+
+namespace {
+template <typename Enqueue>
+int capture_graph(void* stream, fsb_graph** out, int64_t* n_kernels, Enqueue enqueue) {
   if (!out || !stream) return FSB_EINVAL;  // capture needs a non-default stream
   *out = nullptr;
   cudaStream_t st = as_stream(stream);
   cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return (int)e;
-  int rc = solve_pyramid_internal(rig, prm, i0, i1, traj_dirs, traj_ok, workspace,
-                                  workspace_bytes, u, w, v, mask, i1c, diag, st);
+  int rc = enqueue(st);
   cudaGraph_t g = nullptr;
   e = cudaStreamEndCapture(st, &g);
   if (rc) { if (g) cudaGraphDestroy(g); return rc; }
@@ -651,6 +650,32 @@ int fsb_graph_create(const fsb_rig* rig, const fsb_params* prm, const float* i0,
   *out = G;
   if (n_kernels) *n_kernels = k;
   return FSB_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int fsb_graph_create(const fsb_rig* rig, const fsb_params* prm, const float* i0, const float* i1,
+                     const float* const* traj_dirs, const uint8_t* const* traj_ok,
+                     void* workspace, size_t workspace_bytes, float* u, float* w, float* v,
+                     uint8_t* mask, float* i1c, const fsb_diag* diag, void* stream,
+                     fsb_graph** out, int64_t* n_kernels) {
+  return capture_graph(stream, out, n_kernels, [&](cudaStream_t st) {
+    return solve_pyramid_internal(rig, prm, i0, i1, traj_dirs, traj_ok, workspace,
+                                  workspace_bytes, u, w, v, mask, i1c, diag, st);
+  });
+}
+
+int fsb_graph_create_f64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
+                         const double* i1, const double* const* traj_dirs,
+                         const uint8_t* const* traj_ok, void* workspace, size_t workspace_bytes,
+                         double* u, double* w, double* v, uint8_t* mask, double* i1c,
+                         const fsb_diag* diag, void* stream, fsb_graph** out,
+                         int64_t* n_kernels) {
+  return capture_graph(stream, out, n_kernels, [&](cudaStream_t st) {
+    return fsb_solve_pyramid_f64(rig, prm, i0, i1, traj_dirs, traj_ok, workspace,
+                                 workspace_bytes, u, w, v, mask, i1c, diag, st);
+  });
 }
 
 int fsb_graph_launch(fsb_graph* G, void* stream) {

@@ -480,16 +480,15 @@ class Solver:
     def capture(self) -> int:
         """Capture one frame on the fixed input buffers into a CUDA graph (native,
         fsb_graph_create); returns the number of kernel launches per frame."""
-        if self.precision != "fp32":
-            raise ValueError("graph capture is provided for the fp32 production path")
         L = _ext.lib()
         self.release()
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         g = C.c_void_p()
         nk = C.c_int64()
-        _ext.check(L.fsb_graph_create(*self._args(self.i0, self.i1), side.cuda_stream,
-                                      C.byref(g), C.byref(nk)), "graph_create")
+        fn = L.fsb_graph_create if self.precision == "fp32" else L.fsb_graph_create_f64
+        _ext.check(fn(*self._args(self.i0, self.i1), side.cuda_stream, C.byref(g), C.byref(nk)),
+                   "graph_create")
         self.graph = g
         self.kernels_per_frame = int(nk.value)
         return self.kernels_per_frame
@@ -543,7 +542,7 @@ class Solver:
         self._d64["i1"].copy_(h["i1"], non_blocking=True)
         self.i0.copy_(self._d64["i0"])
         self.i1.copy_(self._d64["i1"])
-        if self._traj is None and self.precision == "fp32":
+        if self._traj is None:
             self.replay()
         else:
             self.run()

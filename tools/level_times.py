@@ -14,11 +14,16 @@ sc = S.default_scene()
 i0 = S.render_device(sc, rig.cam0, supersample=ss)[0]
 i1 = S.render_device(sc, rig.cam1, pose=rig.pose, supersample=ss)[0]
 T = {}
+import os
+prec = os.environ.get("PREC", "fp32")
 for L in range(1, prm.pyramid_levels + 1):
     p = replace(prm, pyramid_levels=L)
-    eng = Solver(rig, p)
+    eng = Solver(rig, p, precision=prec)
     eng.i0.copy_(i0); eng.i1.copy_(i1)
-    eng.capture()
+    if os.environ.get("NOGRAPH"):
+        eng.replay = eng.run
+    else:
+        eng.capture()
     for _ in range(3):
         eng.replay()
     torch.cuda.synchronize()
