@@ -35,6 +35,7 @@ UNITS = [
     ("pd_tma.cu", []),
     ("pd_cluster.cu", []),
     ("pd64.cu", ["-fmad=false"]),
+    ("pd64_block.cu", ["-fmad=false"]),
     ("solver.cu", []),
     ("synth.cu", ["-fmad=false"]),
     ("depth.cu", ["-fmad=false"]),

@@ -11,9 +11,11 @@
 // Reference: solver.py:306-452 (solve_level, solve_pyramid) with the stages of
 // solver.py:279-303 and :332-365; rasters.py:57-141 (bicubic).
 
+#include <stdlib.h>
 #include <string.h>
 
 #include "pd_math.cuh"
+#include "pd64_block.cuh"
 
 namespace fsb {
 
@@ -54,6 +56,8 @@ struct L64 {
   double* wv; double* uo; double* iu; double* rho0; double* i1w; uint8_t* i1w_ok;
   double* dirs; uint8_t* dir_ok;
   double* partials;
+  // second state set for the blocked cycles (pd64_block.cu); nullptr = one-cycle kernels
+  double *u2, *ub2, *v2, *vb2, *p2, *q2;
 };
 
 __device__ __forceinline__ bool ex_at(const uint8_t* __restrict__ m, int w, int x, size_t i) {
@@ -234,6 +238,7 @@ struct Plan64 {
   void* traj_scratch; size_t traj_bytes;
   void* setup_scratch; size_t setup_bytes;
   double *T, *S, *u[2], *wv[2], *ub, *v, *vb, *p, *q, *uo, *iu, *rho0, *i1w, *dirs, *partials;
+  double *u2, *ub2, *v2, *vb2, *p2, *q2;
   uint8_t *i1w_ok, *dir_ok;
   size_t bytes;
 };
@@ -274,6 +279,9 @@ int plan64(const fsb_rig* rig, const fsb_params* prm, void* base, Plan64& P) {
   P.i1w = c.take<double>(n0); P.dirs = c.take<double>(2 * n0);
   P.i1w_ok = c.take<uint8_t>(n0); P.dir_ok = c.take<uint8_t>(n0);
   P.partials = c.take<double>(partial_count(H, W));
+  P.u2 = c.take<double>(n0); P.ub2 = c.take<double>(n0);
+  P.v2 = c.take<double>(2 * n0); P.vb2 = c.take<double>(2 * n0);
+  P.p2 = c.take<double>(2 * n0); P.q2 = c.take<double>(4 * n0);
   P.bytes = c.off;
   return FSB_OK;
 }
@@ -288,8 +296,27 @@ fsb_camera scaled(const fsb_camera& c, int h, int w) {  // camera.py:66-77
   return o;
 }
 
-int solve_level64(const L64& L, const fsb_params* prm, const fsb_diag* diag, int64_t pd_off,
+// FSB_PD64=plain runs the one-cycle-per-launch kernels (reference for the
+// blocked kernel in tests/tools); default: blocked, halo 2.
+int pd64_halo() {
+  static int h = -1;
+  if (h < 0) {
+    const char* e = getenv("FSB_PD64");
+    h = e && e[0] == 'p' ? 0 : (e && e[0] >= '1' && e[0] <= '3' ? e[0] - '0' : 2);
+  }
+  return h;
+}
+
+L64 swapped(const L64& L) {
+  L64 o = L;
+  o.u = L.u2; o.ub = L.ub2; o.v = L.v2; o.vb = L.vb2; o.p = L.p2; o.q = L.q2;
+  o.u2 = L.u; o.ub2 = L.ub; o.v2 = L.v; o.vb2 = L.vb; o.p2 = L.p; o.q2 = L.q;
+  return o;
+}
+
+int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, int64_t pd_off,
                   int64_t warp_off, void* scratch, size_t scratch_bytes, cudaStream_t st) {
+  L64 L = L0;  // L's state pointers follow the ping-pong of the blocked cycles
   const size_t n = L.n;
   int rc = level_setup64_internal(L.i0, L.mask, L.h, L.w, prm, L.T, L.S, scratch, scratch_bytes,
                                   st);
@@ -306,7 +333,26 @@ int solve_level64(const L64& L, const fsb_params* prm, const fsb_diag* diag, int
   for (int wi = 0; wi < N; ++wi) {
     k64_sample<<<grd, blk, 0, st>>>(L);
     k64_linearize<<<grd, blk, 0, st>>>(L);
-    for (int k = 0; k < K; ++k) {
+    const int halo = L.u2 ? pd64_halo() : 0;
+    for (int k = 0; halo > 0 && k < K;) {  // blocked: `it` cycles per launch, src -> dst
+      const int it = K - k < halo ? K - k : halo;
+      B64 A;
+      A.h = L.h; A.w = L.w; A.n = n; A.mask = L.mask; A.T = L.T; A.S = L.S;
+      A.iu = L.iu; A.rho0 = L.rho0; A.uo = L.uo;
+      A.su = L.u; A.sub = L.ub; A.sv = L.v; A.svb = L.vb; A.sp = L.p; A.sq = L.q;
+      A.du = L.u2; A.dub = L.ub2; A.dv = L.v2; A.dvb = L.vb2; A.dp = L.p2; A.dq = L.q2;
+      A.lam = prm->lam; A.alpha0 = prm->alpha0; A.alpha1 = prm->alpha1; A.theta = prm->theta;
+      A.sigma_q = sigma_q_of(prm); A.heps = huber_eps_of(prm);
+      A.iters = it;
+      const int64_t slot = pd_off + (int64_t)wi * K + k;
+      A.diag_p = dpq ? diag->max_p_norm + slot : nullptr;
+      A.diag_q = dpq ? diag->max_q_norm + slot : nullptr;
+      rc = pd64_block_launch(A, halo, st);
+      if (rc) return rc;
+      L = swapped(L);
+      k += it;
+    }
+    for (int k = 0; halo == 0 && k < K; ++k) {
       if (dpq) {
         const int64_t slot = pd_off + (int64_t)wi * K + k;
         k64_dual<true><<<grd, blk, 0, st>>>(L, prm->alpha0, prm->alpha1, sigma_q_of(prm),
@@ -326,6 +372,10 @@ int solve_level64(const L64& L, const fsb_params* prm, const fsb_diag* diag, int
     } else {
       k64_finish<false><<<grd, blk, 0, st>>>(L, prm->du_max, nullptr);
     }
+  }
+  if (L.u != L0.u) {  // the level result back into the primary set (u carries on, v is output)
+    cudaMemcpyAsync(L0.u, L.u, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(L0.v, L.v, 2 * n * sizeof(double), cudaMemcpyDeviceToDevice, st);
   }
   return launch_status();
 }
@@ -431,6 +481,7 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
     L.traj = traj; L.traj_ok = tok;
     L.T = P.T; L.S = P.S;
     L.u = u; L.ub = P.ub; L.v = P.v; L.vb = P.vb; L.p = P.p; L.q = P.q;
+    L.u2 = P.u2; L.ub2 = P.ub2; L.v2 = P.v2; L.vb2 = P.vb2; L.p2 = P.p2; L.q2 = P.q2;
     L.wv = wv; L.uo = P.uo; L.iu = P.iu; L.rho0 = P.rho0; L.i1w = P.i1w; L.i1w_ok = P.i1w_ok;
     L.dirs = P.dirs; L.dir_ok = P.dir_ok; L.partials = P.partials;
     rc = solve_level64(L, prm, diag, pd_off, warp_off, P.setup_scratch, P.setup_bytes, st);

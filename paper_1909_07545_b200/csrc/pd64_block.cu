@@ -1,0 +1,125 @@
+// Temporally blocked primal-dual cycles for the float64 parity path.
+//
+// k64_dual + k64_primal (pd64.cu) run one cycle per launch pair and move the
+// whole fp64 state through HBM twice per cycle. This kernel keeps a 32 x 16
+// tile (one pixel per thread, state in registers) on chip for `iters` <= R
+// cycles with an R-pixel halo, exchanging u_bar / v_bar and the edge-masked
+// fluxes through shared memory. The arithmetic is the same helpers in the
+// same order (dual_update_exact, make_flux_exact, the divergence expression
+// of k64_primal, primal_update_exact), compiled with -fmad=false, so the
+// interior results are bit-identical to the one-cycle kernels.
+//
+// Reference: solver.py:279-303 (primal_dual_iterate), rasters.py:144-182.
+
+#include "pd64_block.cuh"
+#include "pd_math.cuh"
+
+namespace fsb {
+
+
+
+namespace {
+
+constexpr int kTX = 32, kTY = 16;
+
+template <int R, bool DIAG>
+__global__ void __launch_bounds__(kTX * kTY, 2) k64_block(const B64 A) {
+  constexpr int TW = kTX - 2 * R, TH = kTY - 2 * R;
+  __shared__ double s_ub[kTY][kTX + 1], s_vb0[kTY][kTX + 1], s_vb1[kTY][kTX + 1];
+  __shared__ double s_f[6][kTY][kTX + 1];  // px py q0x q0y q1x q1y
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int gx = (int)blockIdx.x * TW - R + tx, gy = (int)blockIdx.y * TH - R + ty;
+  const bool in = (unsigned)gx < (unsigned)A.w && (unsigned)gy < (unsigned)A.h;
+  const size_t n = A.n;
+  const size_t i = in ? (size_t)gy * A.w + gx : 0;
+  // edge indicators (ex_at / ey_at of pd64.cu); zero outside the image
+  const bool m = in && A.mask[i];
+  const bool ex = m && gx + 1 < A.w && A.mask[i + 1];
+  const bool ey = m && gy + 1 < A.h && A.mask[i + A.w];
+  double u = 0, ub = 0, v0 = 0, v1 = 0, vb0 = 0, vb1 = 0, p0 = 0, p1 = 0;
+  double q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+  double a = 0, b = 0, c = 0, sp = 0, tu = 0, tv = 0, g = 0, rh = 0, uo = 0;
+  if (in) {
+    u = A.su[i]; ub = A.sub[i];
+    v0 = A.sv[i]; v1 = A.sv[n + i]; vb0 = A.svb[i]; vb1 = A.svb[n + i];
+    p0 = A.sp[i]; p1 = A.sp[n + i];
+    q0 = A.sq[i]; q1 = A.sq[n + i]; q2 = A.sq[2 * n + i]; q3 = A.sq[3 * n + i];
+    a = A.T[i]; b = A.T[n + i]; c = A.T[2 * n + i];
+    sp = A.S[i] * A.alpha1; tu = A.S[n + i]; tv = A.S[2 * n + i];
+    g = A.iu[i]; rh = A.rho0[i]; uo = A.uo[i];
+  }
+  const double sq = A.sigma_q * A.alpha0;
+  const bool interior = tx >= R && tx < kTX - R && ty >= R && ty < kTY - R && in;
+  const int txr = tx + 1 < kTX ? tx + 1 : tx, tyd = ty + 1 < kTY ? ty + 1 : ty;
+  for (int it = 0; it < A.iters; ++it) {
+    s_ub[ty][tx] = ub;
+    s_vb0[ty][tx] = vb0;
+    s_vb1[ty][tx] = vb1;
+    __syncthreads();
+    // dual ascent (k64_dual): forward differences where the edge is in the mask
+    double gxx = 0, gyy = 0, g00 = 0, g01 = 0, g10 = 0, g11 = 0;
+    if (ex) { gxx = s_ub[ty][txr] - ub; g00 = s_vb0[ty][txr] - vb0; g10 = s_vb1[ty][txr] - vb1; }
+    if (ey) { gyy = s_ub[tyd][tx] - ub; g01 = s_vb0[tyd][tx] - vb0; g11 = s_vb1[tyd][tx] - vb1; }
+    dual_update_exact<double>(a, b, c, sp, sq, gxx, gyy, g00, g01, g10, g11, vb0, vb1, p0, p1,
+                              q0, q1, q2, q3, A.heps);
+    const FluxT<double> f = make_flux_exact<double>(a, b, c, ex, ey, p0, p1, q0, q1, q2, q3);
+    s_f[0][ty][tx] = f.px; s_f[1][ty][tx] = f.py;
+    s_f[2][ty][tx] = f.q0x; s_f[3][ty][tx] = f.q0y;
+    s_f[4][ty][tx] = f.q1x; s_f[5][ty][tx] = f.q1y;
+    if (DIAG) {
+      double pn = 0, qn = 0;
+      if (interior) {
+        pn = sqrt(p0 * p0 + p1 * p1);
+        qn = sqrt(((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3);
+      }
+      pn = warp_max(pn);
+      qn = warp_max(qn);
+      if (tx == 0 && A.diag_p) {  // one warp per tile row
+        atomic_max_nonneg(A.diag_p + it, (float)pn);
+        atomic_max_nonneg(A.diag_q + it, (float)qn);
+      }
+    }
+    __syncthreads();
+    // primal descent (k64_primal): backward divergence of the fluxes. The row
+    // above / column left of the tile feed only halo pixels; outside the image
+    // the fluxes are zero (mask 0), as the reference's zero padding.
+    double flx = 0, flq0 = 0, flq1 = 0, fuy = 0, fuq0 = 0, fuq1 = 0;
+    if (tx > 0) { flx = s_f[0][ty][tx - 1]; flq0 = s_f[2][ty][tx - 1]; flq1 = s_f[4][ty][tx - 1]; }
+    if (ty > 0) { fuy = s_f[1][ty - 1][tx]; fuq0 = s_f[3][ty - 1][tx]; fuq1 = s_f[5][ty - 1][tx]; }
+    const double dvv = ((f.px - flx) + f.py) - fuy;
+    const double d0 = ((f.q0x - flq0) + f.q0y) - fuq0;
+    const double d1 = ((f.q1x - flq1) + f.q1y) - fuq1;
+    primal_update_exact<double>(dvv, d0, d1, tu, tv, g, rh, uo, p0, p1, A.lam, A.alpha0,
+                                A.alpha1, A.theta, u, v0, v1, ub, vb0, vb1);
+  }
+  if (!interior) return;
+  A.du[i] = u; A.dub[i] = ub;
+  A.dv[i] = v0; A.dv[n + i] = v1;
+  A.dvb[i] = vb0; A.dvb[n + i] = vb1;
+  A.dp[i] = p0; A.dp[n + i] = p1;
+  A.dq[i] = q0; A.dq[n + i] = q1; A.dq[2 * n + i] = q2; A.dq[3 * n + i] = q3;
+}
+
+template <int R>
+int launch64(const B64& A, cudaStream_t st) {
+  constexpr int TW = kTX - 2 * R, TH = kTY - 2 * R;
+  const dim3 blk(kTX, kTY), grd((A.w + TW - 1) / TW, (A.h + TH - 1) / TH);
+  if (A.diag_p) k64_block<R, true><<<grd, blk, 0, st>>>(A);
+  else k64_block<R, false><<<grd, blk, 0, st>>>(A);
+  return launch_status();
+}
+
+}  // namespace
+
+// `iters` (<= halo) cycles from the src set into the dst set.
+int pd64_block_launch(const B64& A, int halo, cudaStream_t st) {
+  if (A.iters < 1 || A.iters > halo) return FSB_EINVAL;
+  switch (halo) {
+    case 1: return launch64<1>(A, st);
+    case 2: return launch64<2>(A, st);
+    case 3: return launch64<3>(A, st);
+    default: return FSB_EINVAL;
+  }
+}
+
+}  // namespace fsb

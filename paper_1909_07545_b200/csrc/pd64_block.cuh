@@ -1,0 +1,28 @@
+// Launch arguments of the blocked float64 primal-dual kernel (pd64_block.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace fsb {
+
+struct B64 {
+  int h, w;
+  size_t n;
+  const uint8_t* mask;
+  const double* T;  // a, b, c planes
+  const double* S;  // sigma_p, tau_u, tau_v planes
+  const double* iu; const double* rho0; const double* uo;
+  // state sets (src read, dst written): u, u_bar, v (2), v_bar (2), p (2), q (4)
+  const double *su, *sub, *sv, *svb, *sp, *sq;
+  double *du, *dub, *dv, *dvb, *dp, *dq;
+  double lam, alpha0, alpha1, theta, sigma_q, heps;
+  int iters;
+  float* diag_p; float* diag_q;  // per-cycle maxima (nullptr = off)
+};
+
+// `iters` (<= halo, halo in 1..3) cycles from the src set into the dst set.
+int pd64_block_launch(const B64& A, int halo, cudaStream_t st);
+
+}  // namespace fsb

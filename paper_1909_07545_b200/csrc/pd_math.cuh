@@ -112,18 +112,27 @@ FSB_INLINE void dual_update_exact(T a, T b, T c, T sp, T sq, T gx, T gy, T g00, 
     p0 = p0 / dd;
     p1 = p1 / dd;
   }
-  const T pd = fmax(T(1), sqrt(p0 * p0 + p1 * p1));
-  p0 = p0 / pd;
-  p1 = p1 / pd;
+  // x / max(1, |x|): inside the unit ball the reference divides by exactly 1.0
+  // (an identity), so only |x|^2 > 1 takes the sqrt and the divisions; there
+  // sqrt(|x|^2) >= 1 is max(1, |x|) itself. Bit-identical, far fewer fp64 ops.
+  const T pn2 = p0 * p0 + p1 * p1;
+  if (pn2 > T(1)) {
+    const T pd = sqrt(pn2);
+    p0 = p0 / pd;
+    p1 = p1 / pd;
+  }
   q0 = q0 + sq * g00;
   q1 = q1 + sq * g01;
   q2 = q2 + sq * g10;
   q3 = q3 + sq * g11;
-  const T qd = fmax(T(1), sqrt(((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3));
-  q0 = q0 / qd;
-  q1 = q1 / qd;
-  q2 = q2 / qd;
-  q3 = q3 / qd;
+  const T qn2 = ((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3;
+  if (qn2 > T(1)) {
+    const T qd = sqrt(qn2);
+    q0 = q0 / qd;
+    q1 = q1 / qd;
+    q2 = q2 / qd;
+    q3 = q3 / qd;
+  }
 }
 
 template <typename T>

@@ -6,7 +6,11 @@ import torch
 import bench
 from paper_1909_07545_b200 import synth as S
 from paper_1909_07545_b200.solver import Solver
+import os
+from dataclasses import replace
 rig, prm, desc, ss = bench.workload(sys.argv[1] if len(sys.argv) > 1 else "c3")
+if os.environ.get("LEVELS"):
+    prm = replace(prm, pyramid_levels=int(os.environ["LEVELS"]))
 sc = S.default_scene()
 eng = Solver(rig, prm, precision="fp64")
 eng.i0.copy_(S.render_device(sc, rig.cam0, supersample=ss)[0])
