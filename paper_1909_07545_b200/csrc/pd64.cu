@@ -243,8 +243,10 @@ struct Plan64 {
   size_t bytes;
 };
 
-size_t partial_count(int h, int w) {
-  return (size_t)((w + kBX - 1) / kBX) * ((h + kBY - 1) / kBY) + 64;
+size_t partial_count(int h, int w) {  // k64_finish blocks or blocked-kernel tiles (halo <= 3)
+  const size_t blocks = (size_t)((w + kBX - 1) / kBX) * ((h + kBY - 1) / kBY);
+  const size_t tiles = pd64_block_tiles(w, h, 3);
+  return (blocks > tiles ? blocks : tiles) + 64;
 }
 
 int plan64(const fsb_rig* rig, const fsb_params* prm, void* base, Plan64& P) {
@@ -347,11 +349,22 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
       const int64_t slot = pd_off + (int64_t)wi * K + k;
       A.diag_p = dpq ? diag->max_p_norm + slot : nullptr;
       A.diag_q = dpq ? diag->max_q_norm + slot : nullptr;
+      A.fin = k + it == K;  // the warp's last cycles: fused clip / accumulate
+      A.du_max = prm->du_max;
+      A.dirs = L.dirs; A.wv = L.wv;
+      A.diag_du = (A.fin && ddu) ? diag->max_du + warp_off + wi : nullptr;
+      A.partials = L.partials;
       rc = pd64_block_launch(A, halo, st);
       if (rc) return rc;
       L = swapped(L);
       k += it;
+      if (k == K && ddu) {
+        rc = mean_finish_internal(L.partials, (int)pd64_block_tiles(L.w, L.h, halo), L.mask, n,
+                                  diag->mean_abs_du + warp_off + wi, st);
+        if (rc) return rc;
+      }
     }
+    if (halo > 0) continue;  // the blocked launches fused k64_finish
     for (int k = 0; halo == 0 && k < K; ++k) {
       if (dpq) {
         const int64_t slot = pd_off + (int64_t)wi * K + k;

@@ -92,6 +92,30 @@ __global__ void __launch_bounds__(kTX * kTY, 2) k64_block(const B64 A) {
     primal_update_exact<double>(dvv, d0, d1, tu, tv, g, rh, uo, p0, p1, A.lam, A.alpha0,
                                 A.alpha1, A.theta, u, v0, v1, ub, vb0, vb1);
   }
+  if (A.fin) {  // k64_finish (solver.py:356-360) on the interior
+    double adu = 0.0;
+    if (interior) {
+      double du = fmin(fmax(u - uo, -A.du_max), A.du_max);
+      if (!m) du = 0.0;
+      u = uo + du;
+      ub = u;
+      A.wv[2 * i] = A.wv[2 * i] + du * A.dirs[2 * i];
+      A.wv[2 * i + 1] = A.wv[2 * i + 1] + du * A.dirs[2 * i + 1];
+      adu = fabs(du);
+    }
+    if (DIAG && A.diag_du) {
+      __shared__ double s_sum[kTY], s_max[kTY];
+      const double mx = warp_max(adu), sm = warp_sum(adu);
+      if (tx == 0) { s_sum[ty] = sm; s_max[ty] = mx; }
+      __syncthreads();
+      if (tx == 0 && ty == 0) {
+        double t = 0.0, mm = 0.0;
+        for (int k = 0; k < kTY; ++k) { t += s_sum[k]; mm = fmax(mm, s_max[k]); }
+        A.partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+        atomic_max_nonneg(A.diag_du, (float)mm);
+      }
+    }
+  }
   if (!interior) return;
   A.du[i] = u; A.dub[i] = ub;
   A.dv[i] = v0; A.dv[n + i] = v1;
@@ -104,12 +128,17 @@ template <int R>
 int launch64(const B64& A, cudaStream_t st) {
   constexpr int TW = kTX - 2 * R, TH = kTY - 2 * R;
   const dim3 blk(kTX, kTY), grd((A.w + TW - 1) / TW, (A.h + TH - 1) / TH);
-  if (A.diag_p) k64_block<R, true><<<grd, blk, 0, st>>>(A);
+  if (A.diag_p || A.diag_du) k64_block<R, true><<<grd, blk, 0, st>>>(A);
   else k64_block<R, false><<<grd, blk, 0, st>>>(A);
   return launch_status();
 }
 
 }  // namespace
+
+size_t pd64_block_tiles(int w, int h, int halo) {
+  const int TW = kTX - 2 * halo, TH = kTY - 2 * halo;
+  return (size_t)((w + TW - 1) / TW) * ((h + TH - 1) / TH);
+}
 
 // `iters` (<= halo) cycles from the src set into the dst set.
 int pd64_block_launch(const B64& A, int halo, cudaStream_t st) {

@@ -20,9 +20,15 @@ struct B64 {
   double lam, alpha0, alpha1, theta, sigma_q, heps;
   int iters;
   float* diag_p; float* diag_q;  // per-cycle maxima (nullptr = off)
+  // last launch of a warp: clip / accumulate epilogue of k64_finish fused in
+  int fin;
+  double du_max;
+  const double* dirs; double* wv;
+  float* diag_du; double* partials;  // max |du| and per-tile sums of |du| (nullptr = off)
 };
 
 // `iters` (<= halo, halo in 1..3) cycles from the src set into the dst set.
 int pd64_block_launch(const B64& A, int halo, cudaStream_t st);
+size_t pd64_block_tiles(int w, int h, int halo);
 
 }  // namespace fsb
