@@ -243,9 +243,9 @@ struct Plan64 {
   size_t bytes;
 };
 
-size_t partial_count(int h, int w) {  // k64_finish blocks or blocked-kernel tiles (halo <= 3)
+size_t partial_count(int h, int w) {  // k64_finish blocks or blocked-kernel tiles (halo <= 5)
   const size_t blocks = (size_t)((w + kBX - 1) / kBX) * ((h + kBY - 1) / kBY);
-  const size_t tiles = pd64_block_tiles(w, h, 3);
+  const size_t tiles = pd64_block_tiles(w, h, 5);
   return (blocks > tiles ? blocks : tiles) + 64;
 }
 
@@ -335,7 +335,13 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
   for (int wi = 0; wi < N; ++wi) {
     k64_sample<<<grd, blk, 0, st>>>(L);
     k64_linearize<<<grd, blk, 0, st>>>(L);
-    const int halo = L.u2 ? pd64_halo() : 0;
+    // latency-bound small levels: 5 cycles per launch when those tiles fit
+    // two resident CTAs per SM (C3: 64^2, 128^2), else R = 2 (throughput)
+    int halo = L.u2 ? pd64_halo() : 0;
+    if (halo == 2 && getenv("FSB_PD64") == nullptr) {
+      if (pd64_block_tiles(L.w, L.h, 5) <= 2 * 148) halo = 5;
+      else if (pd64_block_tiles(L.w, L.h, 3) <= 2 * 148) halo = 3;
+    }
     for (int k = 0; halo > 0 && k < K;) {  // blocked: `it` cycles per launch, src -> dst
       const int it = K - k < halo ? K - k : halo;
       B64 A;

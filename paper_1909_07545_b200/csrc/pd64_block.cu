@@ -147,6 +147,7 @@ int pd64_block_launch(const B64& A, int halo, cudaStream_t st) {
     case 1: return launch64<1>(A, st);
     case 2: return launch64<2>(A, st);
     case 3: return launch64<3>(A, st);
+    case 5: return launch64<5>(A, st);
     default: return FSB_EINVAL;
   }
 }

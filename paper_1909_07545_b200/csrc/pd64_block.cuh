@@ -27,7 +27,7 @@ struct B64 {
   float* diag_du; double* partials;  // max |du| and per-tile sums of |du| (nullptr = off)
 };
 
-// `iters` (<= halo, halo in 1..3) cycles from the src set into the dst set.
+// `iters` (<= halo, halo in 1..3 or 5) cycles from the src set into the dst set.
 int pd64_block_launch(const B64& A, int halo, cudaStream_t st);
 size_t pd64_block_tiles(int w, int h, int halo);
 
