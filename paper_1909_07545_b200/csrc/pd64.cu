@@ -58,6 +58,8 @@ struct L64 {
   double* partials;
   // second state set for the blocked cycles (pd64_block.cu); nullptr = one-cycle kernels
   double *u2, *ub2, *v2, *vb2, *p2, *q2;
+  // per-pixel flags: bit0 all 16 bicubic taps in mask, bit1 all in traj_ok (nullptr = off)
+  uint8_t* full16;
 };
 
 __device__ __forceinline__ bool ex_at(const uint8_t* __restrict__ m, int w, int x, size_t i) {
@@ -67,6 +69,25 @@ __device__ __forceinline__ bool ey_at(const uint8_t* __restrict__ m, int h, int 
   return y + 1 < h && m[i] && m[i + w];
 }
 
+// All-16-taps-valid flags of a level (mask -> bit0, traj_ok -> bit1) for the
+// sampler's unmasked fast path.
+__global__ void k64_full16(L64 L) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+  if (x >= L.w || y >= L.h) return;
+  uint8_t fl = 0;
+  if (x >= 1 && x + 2 < L.w && y >= 1 && y + 2 < L.h) {
+    bool am = true, at = true;
+    for (int a = -1; a <= 2; ++a)
+      for (int b = -1; b <= 2; ++b) {
+        const size_t k = (size_t)(y + a) * L.w + (x + b);
+        am = am && L.mask[k];
+        at = at && L.traj_ok[k];
+      }
+    fl = (am ? 1 : 0) | (at ? 2 : 0);
+  }
+  L.full16[(size_t)y * L.w + x] = fl;
+}
+
 // solver.py:332-337
 __global__ void k64_sample(L64 L) {
   int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
@@ -74,8 +95,34 @@ __global__ void k64_sample(L64 L) {
   const size_t i = (size_t)y * L.w + x;
   const double px = (double)x + L.wv[2 * i], py = (double)y + L.wv[2 * i + 1];
   double iv[1], dr[2];
-  const bool wok = bicubic_sample<1, double, double>(L.i1, L.mask, L.h, L.w, px, py, iv);
-  bool dok = bicubic_sample<2, double, double>(L.traj, L.traj_ok, L.h, L.w, px, py, dr);
+  bool wok, dok;
+  int ix, iy;
+  double fx, fy;
+  if (L.full16 && split_pos<double>(px, py, L.h, L.w, ix, iy, fx, fy) && ix >= 1 &&
+      ix + 2 < L.w && iy >= 1 && iy + 2 < L.h && L.full16[(size_t)iy * L.w + ix] == 3) {
+    // every tap valid in both fields: the all-valid Catmull-Rom branch of
+    // bicubic_bits (same weights, same order), without the per-tap mask gathers
+    double wx[4], wy[4];
+    cubic_weights(fx, wx);
+    cubic_weights(fy, wy);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int a = 0; a < 4; ++a) {
+      const size_t row = (size_t)(iy + a - 1) * L.w + (ix - 1);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const double wt = wy[a] * wx[b];
+        const double2 t = __ldg(reinterpret_cast<const double2*>(L.traj) + row + b);
+        a0 = tap_acc(a0, wt, __ldg(L.i1 + row + b));
+        a1 = tap_acc(a1, wt, t.x);
+        a2 = tap_acc(a2, wt, t.y);
+      }
+    }
+    iv[0] = a0; dr[0] = a1; dr[1] = a2;
+    wok = dok = true;
+  } else {
+    wok = bicubic_sample<1, double, double>(L.i1, L.mask, L.h, L.w, px, py, iv);
+    dok = bicubic_sample<2, double, double>(L.traj, L.traj_ok, L.h, L.w, px, py, dr);
+  }
   const bool mk = L.mask[i] != 0;
   double d0 = 0.0, d1 = 0.0;
   if (dok) {
@@ -239,7 +286,7 @@ struct Plan64 {
   void* setup_scratch; size_t setup_bytes;
   double *T, *S, *u[2], *wv[2], *ub, *v, *vb, *p, *q, *uo, *iu, *rho0, *i1w, *dirs, *partials;
   double *u2, *ub2, *v2, *vb2, *p2, *q2;
-  uint8_t *i1w_ok, *dir_ok;
+  uint8_t *i1w_ok, *dir_ok, *full16;
   size_t bytes;
 };
 
@@ -284,6 +331,7 @@ int plan64(const fsb_rig* rig, const fsb_params* prm, void* base, Plan64& P) {
   P.u2 = c.take<double>(n0); P.ub2 = c.take<double>(n0);
   P.v2 = c.take<double>(2 * n0); P.vb2 = c.take<double>(2 * n0);
   P.p2 = c.take<double>(2 * n0); P.q2 = c.take<double>(4 * n0);
+  P.full16 = c.take<uint8_t>(n0);
   P.bytes = c.off;
   return FSB_OK;
 }
@@ -320,6 +368,10 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
                   int64_t warp_off, void* scratch, size_t scratch_bytes, cudaStream_t st) {
   L64 L = L0;  // L's state pointers follow the ping-pong of the blocked cycles
   const size_t n = L.n;
+  if (L.full16) {
+    dim3 b(kBX, kBY);
+    k64_full16<<<grid2d(L.w, L.h, b), b, 0, st>>>(L);
+  }
   int rc = level_setup64_internal(L.i0, L.mask, L.h, L.w, prm, L.T, L.S, scratch, scratch_bytes,
                                   st);
   if (rc) return rc;
@@ -501,6 +553,7 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
     L.T = P.T; L.S = P.S;
     L.u = u; L.ub = P.ub; L.v = P.v; L.vb = P.vb; L.p = P.p; L.q = P.q;
     L.u2 = P.u2; L.ub2 = P.ub2; L.v2 = P.v2; L.vb2 = P.vb2; L.p2 = P.p2; L.q2 = P.q2;
+    L.full16 = P.full16;
     L.wv = wv; L.uo = P.uo; L.iu = P.iu; L.rho0 = P.rho0; L.i1w = P.i1w; L.i1w_ok = P.i1w_ok;
     L.dirs = P.dirs; L.dir_ok = P.dir_ok; L.partials = P.partials;
     rc = solve_level64(L, prm, diag, pd_off, warp_off, P.setup_scratch, P.setup_bytes, st);
