@@ -93,6 +93,13 @@ __global__ void k64_sample(L64 L) {
   int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= L.w || y >= L.h) return;
   const size_t i = (size_t)y * L.w + x;
+  if (!L.mask[i]) {  // i1w_ok = warp_ok & mask and dir_ok & mask are false: unused
+    L.i1w[i] = 0.0;
+    L.i1w_ok[i] = 0;
+    L.dirs[2 * i] = 0.0; L.dirs[2 * i + 1] = 0.0;
+    L.dir_ok[i] = 0;
+    return;
+  }
   const double px = (double)x + L.wv[2 * i], py = (double)y + L.wv[2 * i + 1];
   double iv[1], dr[2];
   bool wok, dok;
@@ -142,12 +149,12 @@ __global__ void k64_linearize(L64 L) {
   if (x >= L.w || y >= L.h) return;
   const size_t i = (size_t)y * L.w + x, n = L.n;
   double ahead[1];
-  const bool ok = bicubic_sample<1, double, double>(L.i1w, L.i1w_ok, L.h, L.w,
-                                                    (double)x + L.dirs[2 * i],
-                                                    (double)y + L.dirs[2 * i + 1], ahead);
   const double i1w = L.i1w[i];
-  const bool iu_ok = ok && L.i1w_ok[i];
-  const bool data_ok = iu_ok && L.dir_ok[i];
+  // data_ok needs i1w_ok and dir_ok: only then is the gather needed
+  const bool data_ok = L.i1w_ok[i] && L.dir_ok[i] &&
+                       bicubic_sample<1, double, double>(L.i1w, L.i1w_ok, L.h, L.w,
+                                                         (double)x + L.dirs[2 * i],
+                                                         (double)y + L.dirs[2 * i + 1], ahead);
   L.iu[i] = data_ok ? ahead[0] - i1w : 0.0;
   L.rho0[i] = data_ok ? i1w - L.i0[i] : 0.0;
   const double u = L.u[i];
@@ -380,6 +387,14 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
   cudaMemsetAsync(L.p, 0, 2 * n * sizeof(double), st);
   cudaMemsetAsync(L.q, 0, 4 * n * sizeof(double), st);
   cudaMemcpyAsync(L.ub, L.u, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  if (L.u2) {  // the blocked kernel skips masked pixels: their state is 0 in both sets
+    cudaMemsetAsync(L.u2, 0, n * sizeof(double), st);
+    cudaMemsetAsync(L.ub2, 0, n * sizeof(double), st);
+    cudaMemsetAsync(L.v2, 0, 2 * n * sizeof(double), st);
+    cudaMemsetAsync(L.vb2, 0, 2 * n * sizeof(double), st);
+    cudaMemsetAsync(L.p2, 0, 2 * n * sizeof(double), st);
+    cudaMemsetAsync(L.q2, 0, 4 * n * sizeof(double), st);
+  }
   const int N = prm->warp_iters, K = prm->pd_iters;
   dim3 blk(kBX, kBY), grd = grid2d(L.w, L.h, blk);
   const bool dpq = diag && diag->max_p_norm && diag->max_q_norm;

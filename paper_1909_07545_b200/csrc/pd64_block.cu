@@ -36,10 +36,16 @@ __global__ void __launch_bounds__(kTX * kTY, 2) k64_block(const B64 A) {
   const bool m = in && A.mask[i];
   const bool ex = m && gx + 1 < A.w && A.mask[i + 1];
   const bool ey = m && gy + 1 < A.h && A.mask[i + A.w];
+  // Outside the solve mask the whole state is exactly zero for the level
+  // (upsample_state zeroes u there, v / p / q start at 0, and with both edge
+  // indicators false every update maps 0 to 0), and no masked pixel feeds an
+  // unmasked one (its fluxes and the differences towards it are masked out).
+  // So masked pixels neither load nor store; both state sets are zeroed at
+  // the level start.
   double u = 0, ub = 0, v0 = 0, v1 = 0, vb0 = 0, vb1 = 0, p0 = 0, p1 = 0;
   double q0 = 0, q1 = 0, q2 = 0, q3 = 0;
   double a = 0, b = 0, c = 0, sp = 0, tu = 0, tv = 0, g = 0, rh = 0, uo = 0;
-  if (in) {
+  if (m) {
     u = A.su[i]; ub = A.sub[i];
     v0 = A.sv[i]; v1 = A.sv[n + i]; vb0 = A.svb[i]; vb1 = A.svb[n + i];
     p0 = A.sp[i]; p1 = A.sp[n + i];
@@ -94,7 +100,7 @@ __global__ void __launch_bounds__(kTX * kTY, 2) k64_block(const B64 A) {
   }
   if (A.fin) {  // k64_finish (solver.py:356-360) on the interior
     double adu = 0.0;
-    if (interior) {
+    if (interior && m) {  // masked pixels: du = 0, nothing changes
       double du = fmin(fmax(u - uo, -A.du_max), A.du_max);
       if (!m) du = 0.0;
       u = uo + du;
@@ -116,7 +122,7 @@ __global__ void __launch_bounds__(kTX * kTY, 2) k64_block(const B64 A) {
       }
     }
   }
-  if (!interior) return;
+  if (!interior || !m) return;
   A.du[i] = u; A.dub[i] = ub;
   A.dv[i] = v0; A.dv[n + i] = v1;
   A.dvb[i] = vb0; A.dvb[n + i] = vb1;
