@@ -261,3 +261,28 @@ def test_c5_headline_invariants():
     assert not r1.v.any()
     assert np.isfinite(r1.u).all() and np.isfinite(r1.w).all()
     assert 0.6 < r1.mask.mean() < 0.9
+
+
+@pytest.mark.parametrize("shape", [(12, 10), (9, 40), (40, 9), (1, 64)])
+def test_tiny_and_degenerate_shapes(shape):
+    """Single-level solves on tiny / one-pixel-wide images (cluster path, empty
+    interiors, no right or lower neighbours) against the oracle."""
+    from paper_1909_07545_b200.camera import PinholeCamera, RelativePose, StereoRig
+    from paper_1909_07545_b200.solver import SolverParams, solve_pyramid
+    h, w = shape
+    cam = PinholeCamera(width=w, height=h, fx=8.0, fy=8.0, cx=(w - 1) / 2.0, cy=(h - 1) / 2.0,
+                        fov=np.deg2rad(150.0))
+    rig = StereoRig(cam, cam, RelativePose.from_displacement((0.1, 0.0, 0.0)))
+    rng = np.random.default_rng(h * 100 + w)
+    i0 = rng.random((h, w))
+    i1 = np.roll(i0, 1, axis=1) * 0.9 + 0.05
+    prm = SolverParams(warp_iters=3, pd_iters=4, pyramid_levels=1, min_width=1)
+    res = solve_pyramid(i0, i1, rig, prm, collect_diagnostics=True)
+    sol = O.pyramid_solve(i0, i1, rig, prm)
+    np.testing.assert_array_equal(res.mask, sol.mask)
+    if sol.mask.any():
+        e = np.abs(res.u - sol.u)[sol.mask]
+        assert np.median(e) <= 1e-4 and e.max() <= 1e-3
+    assert np.isfinite(res.u).all() and np.isfinite(res.w).all()
+    r64 = solve_pyramid(i0, i1, rig, prm, precision="fp64")
+    assert np.max(np.abs(r64.u - sol.u)) <= 1e-9
