@@ -124,6 +124,14 @@ int fsb_calibrate_second_image(const fsb_rig* rig, const float* i1, const uint8_
                                void* stream);
 size_t fsb_calibrate_scratch_bytes(const fsb_rig* rig);
 
+/* trace_epipolar_curves (fields.py:111-139): Euler integration of a (h,w,2)
+ * f64 direction field (validity `valid`) from n starts (n,2) f64 for n_steps =
+ * ceil(length / step) steps; verts (n, n_steps+1, 2) f64 (NaN after a trace
+ * dies), alive (n, n_steps+1) u8. */
+int fsb_trace_epipolar_curves(const double* dirs, const uint8_t* valid, int32_t h, int32_t w,
+                              const double* starts, int64_t n, int32_t n_steps, double length,
+                              double step, double* verts, uint8_t* alive, void* stream);
+
 /* ------------------------------------------------------- post-solve depth */
 
 /* compose_with_calibration (fields.py:170-182): full = w + cal(x + w) where the

@@ -325,6 +325,28 @@ def main() -> int:
                         d_gt=d_gt, taus=np.array(taus), err=err, report=rep.to_json(),
                         report_empty=rep0.to_json(), pfm1=pfm1, pfm3=pfm3)
 
+    # ---- epipolar curve tracing (acceptance criterion 04 helpers)
+    rt = np.random.default_rng(404)
+    rec = {}
+    for k, (c, t) in enumerate([(cams["unified"], (-0.1, 0.015, 0.0)),
+                                (cams["kb"], (-0.064, 0.001, 0.002))]):
+        rigk = camera.StereoRig(c, c, camera.RelativePose(np.eye(3), np.array(t, dtype=float)))
+        d, ok = fields.generate_trajectory_field(rigk)
+        starts = np.stack([rt.uniform(2, c.width - 3, 40), rt.uniform(2, c.height - 3, 40)], -1)
+        verts, alive = fields.trace_epipolar_curves(d, ok, starts, 15.0, 0.7)
+        one = fields.trace_epipolar_curve(d, ok, starts[0], 9.0, 0.5)
+        rig_c = camera.StereoRig(c, c, camera.RelativePose.from_displacement(
+            (0.1, 0.02, 0.0), rotvec=(0.0, 0.03, 0.01)))
+        x0 = np.array([c.cx + 3.0, c.cy - 2.0])
+        depths = np.geomspace(0.3, 50.0, 25)
+        sw, swok = fields.depth_swept_curve(rig_c, x0, depths)
+        rec.update({f"cam_{k}": cam_record(c), f"t_{k}": np.array(t, dtype=float),
+                    f"dirs_{k}": d, f"ok_{k}": ok, f"starts_{k}": starts, f"verts_{k}": verts,
+                    f"alive_{k}": alive, f"one_{k}": one, f"R_{k}": rig_c.pose.rotation,
+                    f"tr_{k}": rig_c.pose.translation, f"x0_{k}": x0, f"depths_{k}": depths,
+                    f"swept_{k}": sw, f"swept_ok_{k}": swok})
+    np.savez_compressed(OUT / "trace.npz", **rec)
+
     total = sum(f.stat().st_size for f in OUT.glob("*.npz"))
     print(f"wrote {len(list(OUT.glob('*.npz')))} fixtures, {total / 1024:.0f} KiB -> {OUT}")
     return 0

@@ -25,7 +25,7 @@ CAM_MODELS = {"pinhole": 0, "unified": 1, "polynomial": 2}
 EXPORTED = (
     "fsb_fov_mask", "fsb_fov_mask_scratch_bytes", "fsb_unproject", "fsb_project",
     "fsb_unproject_scratch_bytes", "fsb_calibration_field", "fsb_calibrate_second_image",
-    "fsb_calibrate_scratch_bytes", "fsb_compose_calibration", "fsb_triangulate_midpoint",
+    "fsb_calibrate_scratch_bytes", "fsb_trace_epipolar_curves", "fsb_compose_calibration", "fsb_triangulate_midpoint",
     "fsb_triangulate_scratch_bytes", "fsb_depth_from_correspondence", "fsb_trajectory_field", "fsb_trajectory_scratch_bytes",
     "fsb_sample_bicubic", "fsb_gradient", "fsb_divergence", "fsb_smooth_masked",
     "fsb_smooth_scratch_bytes", "fsb_pyramid_shapes", "fsb_downsample_area",
@@ -106,6 +106,8 @@ def lib() -> C.CDLL:
             "fsb_calibrate_second_image": (C.c_int, [P(FsbRig), vp, vp, vp, vp, vp, sz, vp]),
             "fsb_calibrate_scratch_bytes": (sz, [P(FsbRig)]),
             "fsb_compose_calibration": (C.c_int, [vp, vp, vp, i32, i32, vp, vp, vp]),
+            "fsb_trace_epipolar_curves": (C.c_int, [vp, vp, i32, i32, vp, i64, i32, dbl, dbl, vp,
+                                                    vp, vp]),
             "fsb_triangulate_midpoint": (C.c_int, [P(FsbRig), vp, vp, i64, dbl, vp, vp, vp, sz,
                                                    vp]),
             "fsb_triangulate_scratch_bytes": (sz, []),

@@ -125,6 +125,39 @@ __global__ void k_triangulate(Cam c0, Cam c1, RigGeom G, Pairs P, int64_t n, dou
   okv[i] = ok;
 }
 
+// trace_epipolar_curves (fields.py:111-139): Euler steps of length `step`
+// (a shorter last one) along the bicubic-sampled direction field, one thread
+// per start; a trace dies where the sample is invalid or its norm <= 0.5.
+__global__ void k_trace(const double* __restrict__ dirs, const uint8_t* __restrict__ valid, int h,
+                        int w, const double* __restrict__ starts, int64_t n, int n_steps,
+                        double length, double step, double* __restrict__ verts,
+                        uint8_t* __restrict__ alive) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  double px = starts[2 * s], py = starts[2 * s + 1];
+  double* v = verts + (size_t)s * (n_steps + 1) * 2;
+  uint8_t* al = alive + (size_t)s * (n_steps + 1);
+  v[0] = px; v[1] = py;
+  al[0] = 1;
+  bool live = true;
+  for (int i = 0; i < n_steps; ++i) {
+    const double seg = fmin(step, length - (double)i * step);
+    double d[2] = {0.0, 0.0};
+    bool ok = bicubic_sample<2, double, double>(dirs, valid, h, w, px, py, d);
+    const double d0 = ok ? d[0] : 0.0, d1 = ok ? d[1] : 0.0;
+    const double nrm = sqrt(d0 * d0 + d1 * d1);
+    ok = ok && nrm > 0.5;
+    live = live && ok;
+    const double den = fmax(nrm, 1e-300);
+    const double ux = live ? d0 / den : 0.0, uy = live ? d1 / den : 0.0;
+    px = px + seg * ux;
+    py = py + seg * uy;
+    v[2 * (i + 1)] = live ? px : NAN;
+    v[2 * (i + 1) + 1] = live ? py : NAN;
+    al[i + 1] = live;
+  }
+}
+
 RigGeom rig_geom(const fsb_rig& r) {
   RigGeom G;
   for (int k = 0; k < 9; ++k) G.R[k] = r.rotation[k];
@@ -168,6 +201,19 @@ int fsb_compose_calibration(const double* wv, const double* cal, const uint8_t* 
   if (h <= 0 || w <= 0 || !wv || !cal || !cal_ok || !full || !ok) return FSB_EINVAL;
   const dim3 blk(32, 8);
   k_compose<<<grid2d(w, h, blk), blk, 0, as_stream(stream)>>>(wv, cal, cal_ok, h, w, full, ok);
+  return launch_status();
+}
+
+int fsb_trace_epipolar_curves(const double* dirs, const uint8_t* valid, int32_t h, int32_t w,
+                              const double* starts, int64_t n, int32_t n_steps, double length,
+                              double step, double* verts, uint8_t* alive, void* stream) {
+  if (h <= 0 || w <= 0 || n < 0 || n_steps < 0 || !(step > 0) || !dirs || !valid ||
+      (n > 0 && (!starts || !verts || !alive)))
+    return FSB_EINVAL;
+  if (n == 0) return FSB_OK;
+  const int threads = 128;
+  k_trace<<<(unsigned)((n + threads - 1) / threads), threads, 0, as_stream(stream)>>>(
+      dirs, valid, h, w, starts, n, n_steps, length, step, verts, alive);
   return launch_status();
 }
 

@@ -104,3 +104,49 @@ def compose_with_calibration(w, cal_field, cal_valid):
                                          _dev.ptr(full), _dev.ptr(ok), _dev.stream_ptr()),
                "compose_with_calibration")
     return _dev.download(full), _dev.download(ok, bool)
+
+
+def trace_epipolar_curves(dirs, valid, starts, length: float, step: float):
+    """Euler-integrate the direction field from several start pixels at once
+    (fields.py:111-139), one GPU thread per start. Returns (vertices, alive):
+    vertices (n_starts, n_steps + 1, 2) (NaN once a trace left the valid
+    region), alive flags."""
+    import math
+    if step <= 0:
+        raise ValueError("step must be positive")
+    L = _ext.lib()
+    d = np.asarray(dirs, dtype=np.float64)
+    v = np.asarray(valid, dtype=bool)
+    h, w = v.shape
+    st = np.atleast_2d(np.asarray(starts, dtype=np.float64))
+    n = st.shape[0]
+    n_steps = max(int(math.ceil(length / step)), 0)
+    dd = _dev.upload(d, torch.float64)
+    dv = _dev.upload(v, torch.uint8)
+    ds = _dev.upload(st.reshape(n, 2), torch.float64)
+    verts = _dev.empty((max(n, 1), n_steps + 1, 2), torch.float64)
+    alive = _dev.empty((max(n, 1), n_steps + 1), torch.uint8)
+    _ext.check(L.fsb_trace_epipolar_curves(_dev.ptr(dd), _dev.ptr(dv), h, w, _dev.ptr(ds), n,
+                                           n_steps, float(length), float(step), _dev.ptr(verts),
+                                           _dev.ptr(alive), _dev.stream_ptr()),
+               "trace_epipolar_curves")
+    return _dev.download(verts)[:n], _dev.download(alive, bool)[:n]
+
+
+def trace_epipolar_curve(dirs, valid, start, length: float, step: float):
+    """Polyline (k, 2) traced from one pixel, truncated at the mask edge
+    (fields.py:142-146)."""
+    verts, alive = trace_epipolar_curves(dirs, valid, [start], length, step)
+    return verts[0][alive[0]]
+
+
+def depth_swept_curve(rig, x0, depths):
+    """Exact epipolar curve of a pixel: its ray projected at each depth
+    (fields.py:149-156), on the GPU lens models."""
+    from .camera import project, unproject
+    ray, ok0 = unproject(rig.cam0, np.asarray(x0, dtype=np.float64))
+    if not bool(np.all(ok0)):
+        raise ValueError(f"pixel {x0} is outside the camera-0 field of view")
+    depths = np.asarray(depths, dtype=np.float64)
+    pts = rig.pose.transform(ray[None, :] * depths[:, None])
+    return project(rig.cam1, pts)

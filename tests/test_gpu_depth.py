@@ -162,3 +162,24 @@ def test_make_report_matches_reference():
         v[np.argwhere(v)[0][0], np.argwhere(v)[0][1]] = False
     e = np.linalg.norm(g["w_est"] - g["w_gt"], axis=-1)[v]
     assert make_report(g["w_est"], g["w_gt"], v, taus).median_error_px == float(np.median(e))
+
+
+@pytest.mark.parametrize("k", [0, 1])
+def test_trace_epipolar_curves_match_reference(k):
+    """trace_epipolar_curves / trace_epipolar_curve / depth_swept_curve
+    (fields.py:111-156) against the reference on its own trajectory fields."""
+    from paper_1909_07545_b200.camera import RelativePose, StereoRig
+    from paper_1909_07545_b200.fields import (depth_swept_curve, trace_epipolar_curve,
+                                              trace_epipolar_curves)
+    g = load_golden("trace")
+    verts, alive = trace_epipolar_curves(g[f"dirs_{k}"], g[f"ok_{k}"], g[f"starts_{k}"], 15.0, 0.7)
+    np.testing.assert_array_equal(alive, g[f"alive_{k}"])
+    np.testing.assert_allclose(verts[alive], g[f"verts_{k}"][alive], rtol=0, atol=1e-12)
+    assert np.isnan(verts[~alive]).all()
+    one = trace_epipolar_curve(g[f"dirs_{k}"], g[f"ok_{k}"], g[f"starts_{k}"][0], 9.0, 0.5)
+    np.testing.assert_allclose(one, g[f"one_{k}"], rtol=0, atol=1e-12)
+    cam = camera_from_record(g[f"cam_{k}"])
+    rig = StereoRig(cam, cam, RelativePose(g[f"R_{k}"], g[f"tr_{k}"]))
+    sw, ok = depth_swept_curve(rig, g[f"x0_{k}"], g[f"depths_{k}"])
+    np.testing.assert_array_equal(ok, g[f"swept_ok_{k}"])
+    np.testing.assert_allclose(sw, g[f"swept_{k}"], rtol=0, atol=1e-9)
