@@ -325,6 +325,11 @@ def main() -> int:
                         d_gt=d_gt, taus=np.array(taus), err=err, report=rep.to_json(),
                         report_empty=rep0.to_json(), pfm1=pfm1, pfm3=pfm3)
 
+    # ---- a noisy render (sensor noise drawn from numpy's default_rng(seed))
+    img, dep, hit = synth.render(synth.default_scene(), cams["unified"], noise_sigma=0.02,
+                                 noise_seed=23, supersample=2)
+    np.savez_compressed(OUT / "render_noise.npz", img=img, hit=hit)
+
     # ---- epipolar curve tracing (acceptance criterion 04 helpers)
     rt = np.random.default_rng(404)
     rec = {}

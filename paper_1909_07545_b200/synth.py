@@ -154,11 +154,18 @@ def render_device(scene, cam, pose: RelativePose | None = None, supersample: int
 
 def render(scene, cam, pose: RelativePose | None = None, noise_sigma: float = 0.0,
            noise_seed: int = 0, supersample: int = 1):
-    """(image, depth, valid) host arrays like synth.render (synth.py:217-254)."""
-    if noise_sigma > 0:
-        raise NotImplementedError("sensor noise is not supported by the GPU renderer")
+    """(image, depth, valid) host arrays like synth.render (synth.py:217-254).
+
+    The ray casting runs on the GPU; sensor noise (noise_sigma > 0) is drawn on
+    the host from numpy's default_rng(noise_seed), exactly as the reference
+    draws it, so noisy renders use the reference's noise stream."""
     img, depth, hit = render_device(scene, cam, pose, supersample)
-    return _dev.download(img), _dev.download(depth), _dev.download(hit, bool)
+    image, dep, valid = _dev.download(img), _dev.download(depth), _dev.download(hit, bool)
+    if noise_sigma > 0:
+        rng = np.random.default_rng(noise_seed)
+        image = image + rng.normal(0.0, noise_sigma, size=image.shape)
+        image = np.where(valid, np.clip(image, 0.0, 1.0), 0.0)
+    return image, dep, valid
 
 
 @dataclass(frozen=True)

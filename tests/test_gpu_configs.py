@@ -286,3 +286,16 @@ def test_tiny_and_degenerate_shapes(shape):
     assert np.isfinite(res.u).all() and np.isfinite(res.w).all()
     r64 = solve_pyramid(i0, i1, rig, prm, precision="fp64")
     assert np.max(np.abs(r64.u - sol.u)) <= 1e-9
+
+
+def test_noisy_render_matches_reference():
+    """render(noise_sigma > 0): GPU ray casting plus the reference's own numpy
+    noise stream (default_rng(noise_seed)), clipped inside the hit mask."""
+    from paper_1909_07545_b200 import synth as S
+    g = load_golden("render_noise")
+    cam = camera_from_record(load_golden("camera_unified")["cam"])
+    img, _, hit = S.render(S.default_scene(), cam, noise_sigma=0.02, noise_seed=23, supersample=2)
+    assert np.mean(hit == g["hit"]) >= 0.999
+    both = hit & g["hit"]
+    assert (np.abs(img - g["img"])[both] <= 1e-5).mean() >= 0.995
+    assert (img[~hit] == 0).all()
