@@ -60,7 +60,7 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 
 def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
-    objs = []
+    objs, jobs = [], []
     for src, extra in UNITS:
         s = CSRC / src
         o = BUILD / (s.stem + ".o")
@@ -71,7 +71,13 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
                 cmd += ["-Xptxas", "-v"]
             if verbose:
                 print(" ".join(cmd), flush=True)
-            subprocess.run(cmd, check=True)
+            jobs.append(cmd)
+    if jobs:  # translation units compile independently: run them in parallel
+        from concurrent.futures import ThreadPoolExecutor
+        workers = max(1, min(len(jobs), os.cpu_count() or 1))
+        with ThreadPoolExecutor(workers) as ex:
+            for f in [ex.submit(subprocess.run, cmd, check=True) for cmd in jobs]:
+                f.result()
     if force or _stale(LIB, objs):
         cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"]
         if verbose:
