@@ -1,0 +1,97 @@
+"""The reference's acceptance criteria 03, 04, 06, 07 and 08
+(reference tests/test_acceptance.py:118-219) run end to end on the B200 path:
+GPU renders and ground truth, GPU trajectory fields and curve tracing, GPU
+solves, GPU correspondence composition and error reports — with the
+reference's own thresholds."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def default_setup():
+    from paper_1909_07545_b200 import fields
+    from paper_1909_07545_b200 import synth as S
+    rig = S.default_rig()
+    scene = S.default_scene()
+    i0, _, _ = S.render(scene, rig.cam0, supersample=2)
+    i1, _, _ = S.render(scene, rig.cam1, pose=rig.pose, supersample=2)
+    gt = S.make_ground_truth(scene, rig)
+    cal, cal_ok = fields.generate_calibration_field(rig)
+    return rig, i0, i1, gt, cal, cal_ok
+
+
+@pytest.fixture(scope="module")
+def solve_grid(default_setup):
+    """tau>1 percentages over the acceptance grid (test_acceptance.py:42-57)."""
+    from paper_1909_07545_b200 import evaluate, fields
+    from paper_1909_07545_b200.solver import SolverParams, solve_pyramid
+    rig, i0, i1, gt, cal, cal_ok = default_setup
+    out = {}
+    for n, du in [(2, 0.2), (5, 0.2), (10, 0.2), (50, 0.2), (50, 0.1), (50, 1.0)]:
+        res = solve_pyramid(i0, i1, rig, SolverParams(warp_iters=n, du_max=du))
+        corr, corr_ok = fields.compose_with_calibration(res.w, cal, cal_ok)
+        valid = gt.covisibility & corr_ok & res.mask
+        out[(n, du)] = evaluate.make_report(corr, gt.correspondence, valid)
+    return out
+
+
+def test_criterion_03_trajectory_limit():
+    from paper_1909_07545_b200 import synth as S
+    from paper_1909_07545_b200.fields import generate_trajectory_field, translation_only_rig
+    rig_t = translation_only_rig(S.default_rig())
+    d1, ok1 = generate_trajectory_field(rig_t, epsilon_scale=0.1)
+    d2, ok2 = generate_trajectory_field(rig_t, epsilon_scale=0.05)
+    both = ok1 & ok2
+    angle = float(np.max(np.arccos(np.clip(np.sum(d1[both] * d2[both], -1), -1, 1))))
+    dp, okp = generate_trajectory_field(translation_only_rig(S.pinhole_rig()))
+    # the directions are stored fp32: 1e-3 rad holds, the pinhole y-component
+    # is exactly zero as in the reference
+    assert angle <= 1e-3, angle
+    assert float(np.max(np.abs(dp[okp][:, 1]))) <= 1e-9
+
+
+def _point_to_polyline(points, poly):
+    a, b = poly[:-1], poly[1:]
+    ab = b - a
+    denom = np.maximum((ab * ab).sum(-1), 1e-30)
+    out = np.empty(len(points))
+    for i, p in enumerate(points):
+        t = np.clip(((p - a) * ab).sum(-1) / denom, 0.0, 1.0)
+        proj = a + t[:, None] * ab
+        out[i] = np.linalg.norm(proj - p, axis=-1).min()
+    return out
+
+
+def test_criterion_04_curve_tracing_fidelity():
+    from paper_1909_07545_b200 import synth as S
+    from paper_1909_07545_b200.fields import (depth_swept_curve, generate_trajectory_field,
+                                              trace_epipolar_curves, translation_only_rig)
+    rig_t = translation_only_rig(S.default_rig())
+    dirs, ok = generate_trajectory_field(rig_t)
+    rng = np.random.default_rng(42)
+    ys, xs = np.where(ok[30:-30, 30:-30])
+    sel = rng.choice(len(ys), 100, replace=False)
+    starts = np.stack([xs[sel] + 30.0, ys[sel] + 30.0], axis=-1)
+    verts, alive = trace_epipolar_curves(dirs, ok, starts, length=50.0, step=0.1)
+    worst = 0.0
+    for i in range(100):
+        sweep, sok = depth_swept_curve(rig_t, starts[i], np.geomspace(1e4, 0.01, 4000))
+        worst = max(worst, float(_point_to_polyline(verts[i][alive[i]], sweep[sok]).max()))
+    assert worst <= 0.1, worst
+
+
+def test_criterion_06_end_to_end_accuracy(solve_grid):
+    rep = solve_grid[(50, 0.1)]
+    assert rep.pct_bad[3.0] <= 8.0 and rep.pct_bad[1.0] <= 20.0, rep.to_dict()
+
+
+def test_criterion_07_warp_iteration_trend(solve_grid):
+    errs = [solve_grid[(n, 0.2)].pct_bad[1.0] for n in (2, 5, 10, 50)]
+    assert all(errs[i] > errs[i + 1] for i in range(3)), errs
+
+
+def test_criterion_08_clipping_effect(solve_grid):
+    assert solve_grid[(50, 0.1)].pct_bad[1.0] < solve_grid[(50, 1.0)].pct_bad[1.0]
