@@ -299,3 +299,43 @@ def test_noisy_render_matches_reference():
     both = hit & g["hit"]
     assert (np.abs(img - g["img"])[both] <= 1e-5).mean() >= 0.995
     assert (img[~hit] == 0).all()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_randomized_configurations(seed):
+    """Randomised rigs (all three lens models), sizes (incl. widths that are not
+    multiples of 4), pyramid depths, N / K / du_max and regularisers: the fp64
+    path reproduces the oracle to round-off, the fp32 path to the parity gate."""
+    from paper_1909_07545_b200.camera import (PinholeCamera, PolynomialFisheyeCamera,
+                                              RelativePose, StereoRig, UnifiedCamera)
+    from paper_1909_07545_b200.solver import SolverParams, solve_pyramid
+    rng = np.random.default_rng(1000 + seed)
+    w = int(rng.integers(70, 180)); h = int(rng.integers(60, 150))
+    f = float(rng.uniform(0.35, 0.55)) * w
+    kind = ["unified", "kb", "pinhole"][seed % 3]
+    kw = dict(width=w, height=h, fx=f, fy=f * rng.uniform(0.97, 1.03), cx=(w - 1) / 2 + rng.uniform(-2, 2),
+              cy=(h - 1) / 2 + rng.uniform(-2, 2))
+    if kind == "unified":
+        cam = UnifiedCamera(fov=np.pi, xi=float(rng.uniform(0.6, 1.0)), **kw)
+    elif kind == "kb":
+        cam = PolynomialFisheyeCamera(fov=np.deg2rad(170.0),
+                                      k=(1.0, float(rng.uniform(-0.02, 0.04)), -0.004, 0.0005), **kw)
+    else:
+        cam = PinholeCamera(fov=np.deg2rad(110.0), **kw)
+    t = (float(rng.uniform(0.05, 0.12)), float(rng.uniform(-0.02, 0.02)), float(rng.uniform(-0.02, 0.02)))
+    rv = tuple(float(x) for x in rng.uniform(-0.02, 0.02, 3))
+    rig = StereoRig(cam, cam, RelativePose.from_displacement(t, rotvec=rv))
+    prm = SolverParams(warp_iters=int(rng.integers(2, 7)), pd_iters=int(rng.integers(3, 12)),
+                       du_max=float(rng.uniform(0.1, 0.4)), pyramid_levels=int(rng.integers(1, 4)),
+                       min_width=30, regularizer=["tgv", "tgv", "tv", "huber"][seed % 4])
+    i0, i1 = _render_pair(rig, ss=1)
+    sol = O.pyramid_solve(i0, i1, rig, prm)
+    r64 = solve_pyramid(i0, i1, rig, prm, precision="fp64")
+    np.testing.assert_array_equal(r64.mask, sol.mask)
+    assert np.max(np.abs(r64.u - sol.u)) <= 1e-8
+    assert np.max(np.abs(r64.w - sol.w)) <= 1e-8
+    r32 = solve_pyramid(i0, i1, rig, prm)
+    np.testing.assert_array_equal(r32.mask, sol.mask)
+    if sol.mask.any():
+        e = np.abs(r32.u - sol.u)[sol.mask]
+        assert np.median(e) <= 1e-3 and np.percentile(e, 99) <= 1e-2, (np.median(e), np.percentile(e, 99))
