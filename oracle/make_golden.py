@@ -325,6 +325,16 @@ def main() -> int:
                         d_gt=d_gt, taus=np.array(taus), err=err, report=rep.to_json(),
                         report_empty=rep0.to_json(), pfm1=pfm1, pfm3=pfm3)
 
+    # ---- rig JSON schema (camera.rig_to_dict / rig_from_dict)
+    rigs = [camera.StereoRig(cams["kb"], cams["unified"],
+                             camera.RelativePose.from_displacement((0.1, 0.02, -0.01),
+                                                                   rotvec=(0.01, -0.02, 0.03))),
+            camera.StereoRig(cams["pinhole"], cams["equidistant"],
+                             camera.RelativePose.from_displacement((-0.05, 0.0, 0.0)))]
+    np.savez_compressed(OUT / "rig_json.npz",
+                        rigs=np.array([json.dumps(camera.rig_to_dict(r), sort_keys=True)
+                                       for r in rigs]))
+
     # ---- a noisy render (sensor noise drawn from numpy's default_rng(seed))
     img, dep, hit = synth.render(synth.default_scene(), cams["unified"], noise_sigma=0.02,
                                  noise_seed=23, supersample=2)
