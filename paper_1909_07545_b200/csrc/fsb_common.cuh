@@ -7,12 +7,28 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/fsb200.h"
 
 #define FSB_INLINE __device__ __forceinline__
 
 namespace fsb {
+
+// Host-side NVTX range around one pyramid level (visible in nsys / ncu --nvtx;
+// a no-op when no tool is attached). Scoped so early error returns pop it.
+struct LevelRange {
+  LevelRange(const char* fmt, int w, int h) {
+    char tag[48];
+    snprintf(tag, sizeof(tag), fmt, w, h);
+    nvtxRangePushA(tag);
+  }
+  ~LevelRange() { nvtxRangePop(); }
+  LevelRange(const LevelRange&) = delete;
+  LevelRange& operator=(const LevelRange&) = delete;
+};
 
 constexpr double kPi = 3.14159265358979311599796346854;  // np.pi
 constexpr int kPolyMaxIter = 50;                          // camera.py:31

@@ -538,6 +538,7 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
     const int l = P.nlev - 1 - k;
     const int h = P.shapes[2 * l], w = P.shapes[2 * l + 1];
     const size_t np = (size_t)h * w;
+    const LevelRange nvtx_range("fsb64 level %dx%d", w, h);  // NVTX range per level
     const double* traj;
     const uint8_t* tok;
     if (traj_dirs) {

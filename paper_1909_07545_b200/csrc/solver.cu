@@ -481,6 +481,7 @@ int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const floa
     const int l = P.nlev - 1 - k;  // coarse -> fine
     const int h = P.shapes[2 * l], w = P.shapes[2 * l + 1];
     const size_t np = (size_t)h * w;
+    const LevelRange nvtx_range("fsb level %dx%d", w, h);  // NVTX range per level
     const float* traj;
     const uint8_t* tok;
     if (traj_dirs) {
