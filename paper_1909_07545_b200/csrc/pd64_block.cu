@@ -14,6 +14,10 @@
 #include "pd64_block.cuh"
 #include "pd_math.cuh"
 
+#include <stddef.h>
+#include <stdlib.h>
+#include <string.h>
+
 namespace fsb {
 
 
@@ -22,11 +26,34 @@ namespace {
 
 constexpr int kTX = 32, kTY = 16;
 
-template <int R, bool DIAG>
-__global__ void __launch_bounds__(kTX * kTY, 2) k64_block(const B64 A) {
-  constexpr int TW = kTX - 2 * R, TH = kTY - 2 * R;
-  __shared__ double s_ub[kTY][kTX + 1], s_vb0[kTY][kTX + 1], s_vb1[kTY][kTX + 1];
-  __shared__ double s_f[6][kTY][kTX + 1];  // px py q0x q0y q1x q1y
+// Shared-memory image of one tile (dynamic): the u_bar / v_bar exchange, the
+// six edge-masked fluxes and (CS) the nine per-pixel constants.
+template <int TY>
+struct Tile64 {
+  double ub[TY][kTX + 1], vb0[TY][kTX + 1], vb1[TY][kTX + 1];
+  double f[6][TY][kTX + 1];  // px py q0x q0y q1x q1y
+  double c[9][TY][kTX];
+};
+
+// Per-pixel constants kept in shared memory (CS) instead of registers: the 9
+// level / warp constants are re-read each cycle with ld.shared (volatile, so
+// they are not hoisted back into registers), which removes the register
+// spills of the 64-register (2 CTAs / SM) build.
+FSB_INLINE double lds64(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+
+template <int R, int TY, bool DIAG, bool CS, int MINB>
+__global__ void __launch_bounds__(kTX * TY, MINB) k64_block(const B64 A) {
+  constexpr int TW = kTX - 2 * R, TH = TY - 2 * R;
+  extern __shared__ double s_dyn[];
+  Tile64<TY>& S = *reinterpret_cast<Tile64<TY>*>(s_dyn);
+  auto& s_ub = S.ub;
+  auto& s_vb0 = S.vb0;
+  auto& s_vb1 = S.vb1;
+  auto& s_f = S.f;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int gx = (int)blockIdx.x * TW - R + tx, gy = (int)blockIdx.y * TH - R + ty;
   const bool in = (unsigned)gx < (unsigned)A.w && (unsigned)gy < (unsigned)A.h;
@@ -54,10 +81,17 @@ __global__ void __launch_bounds__(kTX * kTY, 2) k64_block(const B64 A) {
     sp = A.S[i] * A.alpha1; tu = A.S[n + i]; tv = A.S[2 * n + i];
     g = A.iu[i]; rh = A.rho0[i]; uo = A.uo[i];
   }
+  double* const sc = &S.c[0][ty][tx];
+  constexpr int PL = kTX * TY;
+  if (CS) {
+    sc[0] = a; sc[PL] = b; sc[2 * PL] = c; sc[3 * PL] = sp; sc[4 * PL] = tu;
+    sc[5 * PL] = tv; sc[6 * PL] = g; sc[7 * PL] = rh; sc[8 * PL] = uo;
+  }
   const double sq = A.sigma_q * A.alpha0;
-  const bool interior = tx >= R && tx < kTX - R && ty >= R && ty < kTY - R && in;
-  const int txr = tx + 1 < kTX ? tx + 1 : tx, tyd = ty + 1 < kTY ? ty + 1 : ty;
+  const bool interior = tx >= R && tx < kTX - R && ty >= R && ty < TY - R && in;
+  const int txr = tx + 1 < kTX ? tx + 1 : tx, tyd = ty + 1 < TY ? ty + 1 : ty;
   for (int it = 0; it < A.iters; ++it) {
+    if (CS) { a = lds64(sc); b = lds64(sc + PL); c = lds64(sc + 2 * PL); sp = lds64(sc + 3 * PL); }
     s_ub[ty][tx] = ub;
     s_vb0[ty][tx] = vb0;
     s_vb1[ty][tx] = vb1;
@@ -95,10 +129,15 @@ __global__ void __launch_bounds__(kTX * kTY, 2) k64_block(const B64 A) {
     const double dvv = ((f.px - flx) + f.py) - fuy;
     const double d0 = ((f.q0x - flq0) + f.q0y) - fuq0;
     const double d1 = ((f.q1x - flq1) + f.q1y) - fuq1;
+    if (CS) {
+      tu = lds64(sc + 4 * PL); tv = lds64(sc + 5 * PL); g = lds64(sc + 6 * PL);
+      rh = lds64(sc + 7 * PL); uo = lds64(sc + 8 * PL);
+    }
     primal_update_exact<double>(dvv, d0, d1, tu, tv, g, rh, uo, p0, p1, A.lam, A.alpha0,
                                 A.alpha1, A.theta, u, v0, v1, ub, vb0, vb1);
   }
   if (A.fin) {  // k64_finish (solver.py:356-360) on the interior
+    if (CS) uo = lds64(sc + 8 * PL);
     double adu = 0.0;
     if (interior && m) {  // masked pixels: du = 0, nothing changes
       double du = fmin(fmax(u - uo, -A.du_max), A.du_max);
@@ -110,13 +149,13 @@ __global__ void __launch_bounds__(kTX * kTY, 2) k64_block(const B64 A) {
       adu = fabs(du);
     }
     if (DIAG && A.diag_du) {
-      __shared__ double s_sum[kTY], s_max[kTY];
+      __shared__ double s_sum[TY], s_max[TY];
       const double mx = warp_max(adu), sm = warp_sum(adu);
       if (tx == 0) { s_sum[ty] = sm; s_max[ty] = mx; }
       __syncthreads();
       if (tx == 0 && ty == 0) {
         double t = 0.0, mm = 0.0;
-        for (int k = 0; k < kTY; ++k) { t += s_sum[k]; mm = fmax(mm, s_max[k]); }
+        for (int k = 0; k < TY; ++k) { t += s_sum[k]; mm = fmax(mm, s_max[k]); }
         A.partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
         atomic_max_nonneg(A.diag_du, (float)mm);
       }
@@ -130,13 +169,39 @@ __global__ void __launch_bounds__(kTX * kTY, 2) k64_block(const B64 A) {
   A.dq[i] = q0; A.dq[n + i] = q1; A.dq[2 * n + i] = q2; A.dq[3 * n + i] = q3;
 }
 
+template <int R, int TY, bool DIAG, bool CS, int MINB>
+int launch64v(const B64& A, cudaStream_t st) {
+  constexpr int TW = kTX - 2 * R, TH = TY - 2 * R;
+  const dim3 blk(kTX, TY), grd((A.w + TW - 1) / TW, (A.h + TH - 1) / TH);
+  const size_t dyn = CS ? sizeof(Tile64<TY>) : offsetof(Tile64<TY>, c);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k64_block<R, TY, DIAG, CS, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    attr = true;
+  }
+  k64_block<R, TY, DIAG, CS, MINB><<<grd, blk, dyn, st>>>(A);
+  return launch_status();
+}
+
+// Measured on C3 (fp64 frame): constants in shared memory 29.4 ms, in
+// registers 31.2 ms; 32 x 32 tiles at one CTA / SM 32.0 ms; 32 x 16 tiles at
+// one CTA / SM without spills 35.4 ms (occupancy matters more than spills).
+bool pd64_const_regs() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FSB_PD64_CONST");
+    v = e && strcmp(e, "regs") == 0;
+  }
+  return v;
+}
+
 template <int R>
 int launch64(const B64& A, cudaStream_t st) {
-  constexpr int TW = kTX - 2 * R, TH = kTY - 2 * R;
-  const dim3 blk(kTX, kTY), grd((A.w + TW - 1) / TW, (A.h + TH - 1) / TH);
-  if (A.diag_p || A.diag_du) k64_block<R, true><<<grd, blk, 0, st>>>(A);
-  else k64_block<R, false><<<grd, blk, 0, st>>>(A);
-  return launch_status();
+  const bool diag = A.diag_p || A.diag_du;
+  if (pd64_const_regs())  // FSB_PD64_CONST=regs: constants in registers (spills)
+    return diag ? launch64v<R, kTY, true, false, 2>(A, st) : launch64v<R, kTY, false, false, 2>(A, st);
+  return diag ? launch64v<R, kTY, true, true, 2>(A, st) : launch64v<R, kTY, false, true, 2>(A, st);
 }
 
 }  // namespace
