@@ -144,7 +144,7 @@ __global__ void k64_sample(L64 L) {
 }
 
 // solver.py:339-346 with image_derivative_along 192-202
-__global__ void k64_linearize(L64 L) {
+__global__ void k64_linearize(L64 L, bool reset) {
   int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= L.w || y >= L.h) return;
   const size_t i = (size_t)y * L.w + x, n = L.n;
@@ -157,6 +157,7 @@ __global__ void k64_linearize(L64 L) {
                                                          (double)y + L.dirs[2 * i + 1], ahead);
   L.iu[i] = data_ok ? ahead[0] - i1w : 0.0;
   L.rho0[i] = data_ok ? i1w - L.i0[i] : 0.0;
+  if (!reset) return;  // the blocked path resets in its first launch (A.first)
   const double u = L.u[i];
   L.uo[i] = u;
   L.ub[i] = u;
@@ -400,8 +401,6 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
   const bool dpq = diag && diag->max_p_norm && diag->max_q_norm;
   const bool ddu = diag && diag->max_du && diag->mean_abs_du;
   for (int wi = 0; wi < N; ++wi) {
-    k64_sample<<<grd, blk, 0, st>>>(L);
-    k64_linearize<<<grd, blk, 0, st>>>(L);
     // latency-bound small levels: 5 cycles per launch when those tiles fit
     // two resident CTAs per SM (C3: 64^2, 128^2), else R = 2 (throughput)
     int halo = L.u2 ? pd64_halo() : 0;
@@ -409,11 +408,13 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
       if (pd64_block_tiles(L.w, L.h, 5) <= 2 * 148) halo = 5;
       else if (pd64_block_tiles(L.w, L.h, 3) <= 2 * 148) halo = 3;
     }
+    k64_sample<<<grd, blk, 0, st>>>(L);
+    k64_linearize<<<grd, blk, 0, st>>>(L, halo == 0);
     for (int k = 0; halo > 0 && k < K;) {  // blocked: `it` cycles per launch, src -> dst
       const int it = K - k < halo ? K - k : halo;
       B64 A;
       A.h = L.h; A.w = L.w; A.n = n; A.mask = L.mask; A.T = L.T; A.S = L.S;
-      A.iu = L.iu; A.rho0 = L.rho0; A.uo = L.uo;
+      A.iu = L.iu; A.rho0 = L.rho0; A.uo = L.uo; A.first = k == 0;
       A.su = L.u; A.sub = L.ub; A.sv = L.v; A.svb = L.vb; A.sp = L.p; A.sq = L.q;
       A.du = L.u2; A.dub = L.ub2; A.dv = L.v2; A.dvb = L.vb2; A.dp = L.p2; A.dq = L.q2;
       A.lam = prm->lam; A.alpha0 = prm->alpha0; A.alpha1 = prm->alpha1; A.theta = prm->theta;

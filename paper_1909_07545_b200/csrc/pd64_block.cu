@@ -73,13 +73,18 @@ __global__ void __launch_bounds__(kTX * TY, MINB) k64_block(const B64 A) {
   double q0 = 0, q1 = 0, q2 = 0, q3 = 0;
   double a = 0, b = 0, c = 0, sp = 0, tu = 0, tv = 0, g = 0, rh = 0, uo = 0;
   if (m) {
-    u = A.su[i]; ub = A.sub[i];
-    v0 = A.sv[i]; v1 = A.sv[n + i]; vb0 = A.svb[i]; vb1 = A.svb[n + i];
+    u = A.su[i];
+    v0 = A.sv[i]; v1 = A.sv[n + i];
+    if (A.first) {
+      ub = u; vb0 = v0; vb1 = v1; uo = u;
+    } else {
+      ub = A.sub[i]; vb0 = A.svb[i]; vb1 = A.svb[n + i]; uo = A.uo[i];
+    }
     p0 = A.sp[i]; p1 = A.sp[n + i];
     q0 = A.sq[i]; q1 = A.sq[n + i]; q2 = A.sq[2 * n + i]; q3 = A.sq[3 * n + i];
     a = A.T[i]; b = A.T[n + i]; c = A.T[2 * n + i];
     sp = A.S[i] * A.alpha1; tu = A.S[n + i]; tv = A.S[2 * n + i];
-    g = A.iu[i]; rh = A.rho0[i]; uo = A.uo[i];
+    g = A.iu[i]; rh = A.rho0[i];
   }
   double* const sc = &S.c[0][ty][tx];
   constexpr int PL = kTX * TY;
@@ -162,6 +167,7 @@ __global__ void __launch_bounds__(kTX * TY, MINB) k64_block(const B64 A) {
     }
   }
   if (!interior || !m) return;
+  if (A.first) A.uo[i] = CS ? lds64(sc + 8 * PL) : uo;
   A.du[i] = u; A.dub[i] = ub;
   A.dv[i] = v0; A.dv[n + i] = v1;
   A.dvb[i] = vb0; A.dvb[n + i] = vb1;

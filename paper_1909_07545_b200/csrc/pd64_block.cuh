@@ -13,7 +13,11 @@ struct B64 {
   const uint8_t* mask;
   const double* T;  // a, b, c planes
   const double* S;  // sigma_p, tau_u, tau_v planes
-  const double* iu; const double* rho0; const double* uo;
+  const double* iu; const double* rho0;
+  double* uo;  // read; written by the first launch of a warp (`first`)
+  // first launch of a warp: the warp-start reset of k64_linearize (solver.py:
+  // 347-350: u0 = u, u_bar = u, v_bar = v) is done here from the loaded u / v
+  int first;
   // state sets (src read, dst written): u, u_bar, v (2), v_bar (2), p (2), q (4)
   const double *su, *sub, *sv, *svb, *sp, *sq;
   double *du, *dub, *dv, *dvb, *dp, *dq;
