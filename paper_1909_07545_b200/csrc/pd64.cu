@@ -89,74 +89,132 @@ __global__ void k64_full16(L64 L) {
 }
 
 // solver.py:332-337
+// The loads of the fast path are issued speculatively: the warp position
+// does not wait for the mask byte, and the 16 taps do not wait for the
+// full16 flag (inner stencils only; the flag decides which result is used),
+// so the chain is wv -> taps instead of mask -> wv -> flag -> taps. The fast
+// branch is the all-valid Catmull-Rom branch of bicubic_bits (same weights,
+// same order); everything else takes the masked gathers.
 __global__ void k64_sample(L64 L) {
   int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= L.w || y >= L.h) return;
   const size_t i = (size_t)y * L.w + x;
-  if (!L.mask[i]) {  // i1w_ok = warp_ok & mask and dir_ok & mask are false: unused
+  const uint8_t mk = L.mask[i];
+  const double2 wv = reinterpret_cast<const double2*>(L.wv)[i];
+  const double px = (double)x + wv.x, py = (double)y + wv.y;
+  double iv[1], dr[2];
+  bool wok = false, dok = false, fast = false;
+  int ix, iy;
+  double fx, fy;
+  if (L.full16 && split_pos<double>(px, py, L.h, L.w, ix, iy, fx, fy) && ix >= 1 &&
+      ix + 2 < L.w && iy >= 1 && iy + 2 < L.h) {
+    const size_t base = (size_t)(iy - 1) * L.w + (ix - 1);
+    double ti[16];
+    double2 tt[16];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        ti[4 * a + b] = __ldg(L.i1 + base + (size_t)a * L.w + b);
+        tt[4 * a + b] = __ldg(reinterpret_cast<const double2*>(L.traj) + base + (size_t)a * L.w + b);
+      }
+    if (L.full16[(size_t)iy * L.w + ix] == 3) {
+      double wx[4], wy[4];
+      cubic_weights(fx, wx);
+      cubic_weights(fy, wy);
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const double wt = wy[a] * wx[b];
+          a0 = tap_acc(a0, wt, ti[4 * a + b]);
+          a1 = tap_acc(a1, wt, tt[4 * a + b].x);
+          a2 = tap_acc(a2, wt, tt[4 * a + b].y);
+        }
+      iv[0] = a0; dr[0] = a1; dr[1] = a2;
+      wok = dok = fast = true;
+    }
+  }
+  if (!mk) {  // i1w_ok = warp_ok & mask and dir_ok & mask are false: unused
     L.i1w[i] = 0.0;
     L.i1w_ok[i] = 0;
     L.dirs[2 * i] = 0.0; L.dirs[2 * i + 1] = 0.0;
     L.dir_ok[i] = 0;
     return;
   }
-  const double px = (double)x + L.wv[2 * i], py = (double)y + L.wv[2 * i + 1];
-  double iv[1], dr[2];
-  bool wok, dok;
-  int ix, iy;
-  double fx, fy;
-  if (L.full16 && split_pos<double>(px, py, L.h, L.w, ix, iy, fx, fy) && ix >= 1 &&
-      ix + 2 < L.w && iy >= 1 && iy + 2 < L.h && L.full16[(size_t)iy * L.w + ix] == 3) {
-    // every tap valid in both fields: the all-valid Catmull-Rom branch of
-    // bicubic_bits (same weights, same order), without the per-tap mask gathers
-    double wx[4], wy[4];
-    cubic_weights(fx, wx);
-    cubic_weights(fy, wy);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int a = 0; a < 4; ++a) {
-      const size_t row = (size_t)(iy + a - 1) * L.w + (ix - 1);
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const double wt = wy[a] * wx[b];
-        const double2 t = __ldg(reinterpret_cast<const double2*>(L.traj) + row + b);
-        a0 = tap_acc(a0, wt, __ldg(L.i1 + row + b));
-        a1 = tap_acc(a1, wt, t.x);
-        a2 = tap_acc(a2, wt, t.y);
-      }
-    }
-    iv[0] = a0; dr[0] = a1; dr[1] = a2;
-    wok = dok = true;
-  } else {
+  if (!fast) {
     wok = bicubic_sample<1, double, double>(L.i1, L.mask, L.h, L.w, px, py, iv);
     dok = bicubic_sample<2, double, double>(L.traj, L.traj_ok, L.h, L.w, px, py, dr);
   }
-  const bool mk = L.mask[i] != 0;
   double d0 = 0.0, d1 = 0.0;
   if (dok) {
     const double nrm = sqrt(dr[0] * dr[0] + dr[1] * dr[1]);
-    if (nrm > 0.5 && mk) { d0 = dr[0] / fmax(nrm, 1e-300); d1 = dr[1] / fmax(nrm, 1e-300); }
+    if (nrm > 0.5) { d0 = dr[0] / fmax(nrm, 1e-300); d1 = dr[1] / fmax(nrm, 1e-300); }
     else dok = false;
   }
   L.i1w[i] = wok ? iv[0] : 0.0;
-  L.i1w_ok[i] = wok && mk;
+  L.i1w_ok[i] = wok;
   L.dirs[2 * i] = d0; L.dirs[2 * i + 1] = d1;
   L.dir_ok[i] = dok;
 }
 
 // solver.py:339-346 with image_derivative_along 192-202
+// Loads issued ahead of their conditions (flags, direction, the 16 taps and
+// their validity bytes together): two dependent memory round trips instead of
+// four. The all-valid case is bicubic_bits' Catmull-Rom branch on the
+// preloaded taps (same weights, same order); partial stencils take
+// bicubic_bits itself.
 __global__ void k64_linearize(L64 L, bool reset) {
   int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= L.w || y >= L.h) return;
   const size_t i = (size_t)y * L.w + x, n = L.n;
-  double ahead[1];
-  const double i1w = L.i1w[i];
+  const double i1w = L.i1w[i], i0 = L.i0[i];
+  const bool ok0 = L.i1w_ok[i] && L.dir_ok[i];
+  const double2 dv = reinterpret_cast<const double2*>(L.dirs)[i];
   // data_ok needs i1w_ok and dir_ok: only then is the gather needed
-  const bool data_ok = L.i1w_ok[i] && L.dir_ok[i] &&
-                       bicubic_sample<1, double, double>(L.i1w, L.i1w_ok, L.h, L.w,
-                                                         (double)x + L.dirs[2 * i],
-                                                         (double)y + L.dirs[2 * i + 1], ahead);
-  L.iu[i] = data_ok ? ahead[0] - i1w : 0.0;
-  L.rho0[i] = data_ok ? i1w - L.i0[i] : 0.0;
+  bool data_ok = false;
+  double ahead = 0.0;
+  int ix, iy;
+  double fx, fy;
+  if (split_pos<double>((double)x + dv.x, (double)y + dv.y, L.h, L.w, ix, iy, fx, fy)) {
+    const bool inner = ix >= 1 && ix + 2 < L.w && iy >= 1 && iy + 2 < L.h;
+    if (inner) {
+      const size_t base = (size_t)(iy - 1) * L.w + (ix - 1);
+      double t[16];
+      unsigned okb = 0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const size_t k = base + (size_t)a * L.w + b;
+          t[4 * a + b] = L.i1w[k];
+          okb |= (L.i1w_ok[k] ? 1u : 0u) << (4 * a + b);
+        }
+      if (ok0 && okb == 0xFFFFu) {
+        double wx[4], wy[4];
+        cubic_weights(fx, wx);
+        cubic_weights(fy, wy);
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc = tap_acc(acc, wy[a] * wx[b], t[4 * a + b]);
+        ahead = acc;
+        data_ok = true;
+      } else if (ok0) {
+        double o[1];
+        data_ok = bicubic_bits<1, double, true, double>(L.i1w, okb, L.w, ix, iy, fx, fy, o);
+        ahead = o[0];
+      }
+    } else if (ok0) {
+      double o[1];
+      data_ok = bicubic_at<1, double, true, double>(L.i1w, L.i1w_ok, L.h, L.w, ix, iy, fx, fy, o);
+      ahead = o[0];
+    }
+  }
+  L.iu[i] = data_ok ? ahead - i1w : 0.0;
+  L.rho0[i] = data_ok ? i1w - i0 : 0.0;
   if (!reset) return;  // the blocked path resets in its first launch (A.first)
   const double u = L.u[i];
   L.uo[i] = u;
