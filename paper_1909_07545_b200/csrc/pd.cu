@@ -380,14 +380,17 @@ __global__ void __launch_bounds__(256) k_sample_px(fsb_level L) {
   float iw = 0.f;
   bool iok = false, dok = false;
   float2 d = make_float2(0.f, 0.f);
-  if (L.mask[i]) {
+  // the warp is loaded with the mask byte, not after it (one round trip less)
+  const uint8_t mk = L.mask[i];
+  const float2 wv = reinterpret_cast<const float2*>(L.wv)[i];
+  if (mk) {
     if (kNanSampler)
-      warp_sample_nan(reinterpret_cast<const float4*>(L.packed), L.h, L.w, x, y,
-                      reinterpret_cast<const float2*>(L.wv)[i], iw, iok, d, dok);
+      warp_sample_nan(reinterpret_cast<const float4*>(L.packed), L.h, L.w, x, y, wv, iw, iok, d,
+                      dok);
     else {
       const SampleSrc S{L.i1, L.mask, L.traj, L.traj_ok,
                         reinterpret_cast<const float4*>(L.packed), L.full16, L.h, L.w};
-      warp_sample_px(S, x, y, reinterpret_cast<const float2*>(L.wv)[i], true, iw, iok, d, dok);
+      warp_sample_px(S, x, y, wv, true, iw, iok, d, dok);
     }
   }
   // i1w is stored NaN where invalid (warp_ok & mask false): k_iu_px reads the
@@ -404,9 +407,12 @@ __global__ void __launch_bounds__(256) k_iu_px(fsb_level L) {
   if (x >= L.w || y >= L.h) return;
   const size_t i = (size_t)y * L.w + x;
   float iu = 0.f, rho0 = 0.f;
+  // loaded together, ahead of their conditions (one round trip less)
   const float iw = L.i1w[i];
-  if (!isnan(iw) && L.dir_ok[i]) {
-    const float2 d = reinterpret_cast<const float2*>(L.dirs)[i];
+  const bool dk = L.dir_ok[i];
+  const float2 d = reinterpret_cast<const float2*>(L.dirs)[i];
+  const float i0 = L.i0[i];
+  if (!isnan(iw) && dk) {
     int ix, iy;
     float fx, fy;
     if (split_off(x, y, d.x, d.y, L.h, L.w, ix, iy, fx, fy)) {
@@ -438,7 +444,7 @@ __global__ void __launch_bounds__(256) k_iu_px(fsb_level L) {
       float ahead = cub;
       if (okb == 0xFFFFu || bicubic_regs(t, okb, fx, fy, ahead)) {
         iu = ahead - iw;
-        rho0 = iw - L.i0[i];
+        rho0 = iw - i0;
       }
     }
   }
