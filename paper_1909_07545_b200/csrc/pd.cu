@@ -372,7 +372,8 @@ int warp_sample_internal(const fsb_level* L, cudaStream_t st) {
 // Split prologue for large levels: the samples at x + w once per pixel (no
 // halo re-sampling), then I_u from the sampled image in global memory (L1/L2
 // resident) in a second kernel. Same arithmetic as k_warp_prologue.
-__global__ void __launch_bounds__(256) k_sample_px(fsb_level L) {
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_sample_px(fsb_level L) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   if (x >= L.w || y >= L.h) return;
@@ -461,8 +462,13 @@ int warp_prologue_internal(const fsb_level* L, cudaStream_t st) {
   const bool big = (size_t)L->w * L->h >= (size_t)512 * 512;
   if (mode == 1 || (mode == 0 && kSplitDefault)) {
     dim3 blk(kBX, kBY), grd = grid2d(L->w, L->h, blk);
-    k_sample_px<<<grd, blk, 0, st>>>(*L);
-    k_iu_px<<<grd, blk, 0, st>>>(*L);
+    // 6 CTAs / SM (42 registers; spills only on the masked fallback) hides the
+    // gather latency on >= 512^2 levels: C3 1024^2 7.83 -> 7.49 ms, bench 69.5
+    // -> 71.5 frames/s (A/B, 3 x 30 steps); at 256^2 the unconstrained build
+    // is 0.05 ms faster (tools/level_times.py)
+    if (big) k_sample_px<6><<<grd, blk, 0, st>>>(*L);
+    else k_sample_px<1><<<grd, blk, 0, st>>>(*L);
+    k_iu_px<<<grd, blk, 0, st>>>(*L);  // (8 CTAs / SM measured slower)
     return launch_status();
   }
   // small levels: 16 x 16 tiles so the grid still spreads over the SMs
