@@ -17,6 +17,7 @@ graph, and exposes device-tensor entry points for throughput measurement.
 from __future__ import annotations
 
 import ctypes as C
+import sys
 from collections import OrderedDict
 from dataclasses import asdict, dataclass, field
 
@@ -439,6 +440,7 @@ class Solver:
                                      _dev.ptr(self.d_du), _dev.ptr(self.d_mean))
         self._traj = None
         self._host = None
+        self._out_pool: list = []  # pinned output sets (see _out_set)
         self.graph = None
         self.kernels_per_frame = None
 
@@ -520,6 +522,31 @@ class Solver:
                          "i1": torch.empty((self.H1, self.W1), **D)}
         return self._host
 
+    _OUT = (("u", torch.float64), ("w", torch.float64), ("v", torch.float64),
+            ("mask", torch.bool), ("i1c", torch.float64))
+    _POOL = 3  # output sets kept pinned per engine
+
+    def _out_set(self) -> dict:
+        """Pinned host buffers for one result, as (tensor, owner ndarray) pairs.
+
+        The arrays handed to the caller are views of the owner ndarray, so a
+        set is free again exactly when no caller-held view remains (its
+        refcount is back to the pool's own). Reusing a free set avoids a
+        cudaHostAlloc of ~50 MB per call; a set still referenced is never
+        written, so every StereoResult stays fresh as in the reference.
+        """
+        for st in self._out_pool:
+            if all(sys.getrefcount(st[k][1]) <= st["_free"] for k, _ in self._OUT):
+                return st
+        st = {}
+        for k, dt in self._OUT:
+            t = torch.empty(tuple(getattr(self, k).shape), dtype=dt, pin_memory=True)
+            st[k] = (t, t.numpy())
+        st["_free"] = sys.getrefcount(st["u"][1])
+        if len(self._out_pool) < self._POOL:
+            self._out_pool.append(st)
+        return st
+
     def solve(self, i0, i1) -> StereoResult:
         """Host images in, StereoResult (float64 host arrays) out.
 
@@ -536,23 +563,25 @@ class Solver:
         if i1a.shape != (self.H1, self.W1):
             raise ValueError("image 1 does not match camera 1 dimensions")
         h = self._staging()
-        h["i0"].copy_(torch.from_numpy(np.ascontiguousarray(i0a)))
-        h["i1"].copy_(torch.from_numpy(np.ascontiguousarray(i1a)))
-        self._d64["i0"].copy_(h["i0"], non_blocking=True)
-        self._d64["i1"].copy_(h["i1"], non_blocking=True)
+        # row chunks: the DMA of chunk k overlaps the host copy of chunk k + 1
+        for key, src in (("i0", i0a), ("i1", i1a)):
+            src_t = torch.from_numpy(np.ascontiguousarray(src))
+            rows = src_t.shape[0]
+            step = max(1, -(-rows // 4))
+            for r in range(0, rows, step):
+                h[key][r:r + step].copy_(src_t[r:r + step])
+                self._d64[key][r:r + step].copy_(h[key][r:r + step], non_blocking=True)
         self.i0.copy_(self._d64["i0"])
         self.i1.copy_(self._d64["i1"])
         if self._traj is None:
             self.replay()
         else:
             self.run()
+        st = self._out_set()
         outs = {}
-        for k, dt in (("u", torch.float64), ("w", torch.float64), ("v", torch.float64),
-                      ("mask", torch.bool), ("i1c", torch.float64)):
-            d = getattr(self, k).to(dt)
-            hb = torch.empty(d.shape, dtype=dt, pin_memory=True)
-            hb.copy_(d, non_blocking=True)
-            outs[k] = hb
+        for k, dt in self._OUT:
+            st[k][0].copy_(getattr(self, k).to(dt), non_blocking=True)
+            outs[k] = st[k][1].view()
         torch.cuda.current_stream().synchronize()
         diag = None
         if self.diag is not None:
@@ -561,9 +590,8 @@ class Solver:
             diag.max_q_norm = [float(x) for x in _dev.download(self.d_q)]
             diag.max_du = [float(x) for x in _dev.download(self.d_du)]
             diag.mean_abs_du = [float(x) for x in _dev.download(self.d_mean)]
-        return StereoResult(u=outs["u"].numpy(), w=outs["w"].numpy(), v=outs["v"].numpy(),
-                            mask=outs["mask"].numpy(), i1_calibrated=outs["i1c"].numpy(),
-                            diagnostics=diag)
+        return StereoResult(u=outs["u"], w=outs["w"], v=outs["v"], mask=outs["mask"],
+                            i1_calibrated=outs["i1c"], diagnostics=diag)
 
 
 _CACHE: "OrderedDict[tuple, Solver]" = OrderedDict()

@@ -156,3 +156,30 @@ def test_empty_mask_frame():
     np.testing.assert_array_equal(res.mask, sol.mask)
     assert not res.mask.any()
     assert np.all(res.u == 0) and np.all(res.w == 0) and np.isfinite(res.v).all()
+
+
+def test_results_stay_fresh_with_pinned_pool():
+    """Each StereoResult owns its arrays (solver.py:451-452 returns fresh arrays):
+    a held result is never overwritten by later calls, and a dropped one's
+    pinned buffers are reused (no per-call cudaHostAlloc)."""
+    from paper_1909_07545_b200.solver import Solver
+    g = load_golden("pyramid_solve")
+    eng = Solver(_rig(g), _params(g))
+    r1 = eng.solve(g["i0"], g["i1"])
+    keep = r1.u[2:, 3:]  # a slice of the result must pin it too
+    u1, w1 = r1.u.copy(), r1.w.copy()
+    del r1
+    r2 = eng.solve(np.flipud(g["i0"]).copy(), np.flipud(g["i1"]).copy())
+    assert not np.array_equal(r2.u, u1)
+    assert np.array_equal(keep, u1[2:, 3:])  # still the first frame's values
+    del keep
+    r3 = eng.solve(g["i0"], g["i1"])
+    assert np.array_equal(r3.u, u1) and np.array_equal(r3.w, w1)
+    del r2
+    r3 = eng.solve(g["i0"], g["i1"])  # r3 of the previous call is alive during it
+    n_sets = len(eng._out_pool)
+    for _ in range(4):  # at most one earlier result alive: the pool stops growing
+        r3 = eng.solve(g["i0"], g["i1"])
+    assert len(eng._out_pool) == n_sets <= 3
+    assert np.array_equal(r3.u, u1)
+    assert r3.u.flags.writeable and r3.mask.dtype == bool

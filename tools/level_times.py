@@ -10,6 +10,9 @@ from paper_1909_07545_b200 import synth as S
 from paper_1909_07545_b200.solver import Solver
 
 rig, prm, desc, ss = bench.workload(sys.argv[1] if len(sys.argv) > 1 else "c3")
+import os
+if os.environ.get("PD_ITERS"):  # cost model: per-warp fixed part vs per-cycle part
+    prm = replace(prm, pd_iters=int(os.environ["PD_ITERS"]))
 sc = S.default_scene()
 i0 = S.render_device(sc, rig.cam0, supersample=ss)[0]
 i1 = S.render_device(sc, rig.cam1, pose=rig.pose, supersample=ss)[0]
