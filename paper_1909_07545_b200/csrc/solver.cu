@@ -10,6 +10,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <mutex>
 #include <vector>
 
 #include "fsb_common.cuh"
@@ -103,14 +104,14 @@ struct Carve {
 struct LevelState {  // state buffers sized for the finest level, reused per level
   float* state_a;  // 12 planes u, u_bar, v x2, v_bar x2, p x2, q x4 (plane stride = level n)
   float* state_b;  // ping-pong copy
-  float* consts;   // 10 planes T x3, steps x3, iu, rho0, u_omega, maskf
+  float* consts[kMaxLevels];    // per level: 10 planes T x3, steps x3, iu, rho0, u_omega, maskf
   float* carry_u;  // previous level's u for upsample_state
   float* wv[2];
   float *i1w, *dirs;
   uint8_t *i1w_ok, *dir_ok;
   double* partials;
-  float* packed;
-  uint8_t* full16;
+  float* packed[kMaxLevels];    // per level gather tables (filled ahead on the side stream)
+  uint8_t* full16[kMaxLevels];
   int* tiles;
 };
 
@@ -163,7 +164,12 @@ int make_plan(const fsb_rig* rig, const fsb_params* prm, void* base, Plan& P) {
   LevelState& s = P.st;
   for (int k = 0; k < 2; ++k) s.wv[k] = c.take<float>(2 * n0);
   s.state_a = c.take<float>(12 * n0);
-  s.consts = c.take<float>(10 * n0);
+  for (int l = 0; l < n; ++l) {
+    const size_t np = (size_t)P.shapes[2 * l] * P.shapes[2 * l + 1];
+    s.consts[l] = c.take<float>(10 * np);
+    s.packed[l] = c.take<float>(4 * np);
+    s.full16[l] = c.take<uint8_t>(np);
+  }
   s.carry_u = c.take<float>(n0);
   s.i1w = c.take<float>(n0);
   s.dirs = c.take<float>(2 * n0);
@@ -171,8 +177,6 @@ int make_plan(const fsb_rig* rig, const fsb_params* prm, void* base, Plan& P) {
   s.dir_ok = c.take<uint8_t>(n0);
   s.partials = c.take<double>(level_partials_internal(H, W) + 64);
   s.state_b = c.take<float>(12 * n0);
-  s.packed = c.take<float>(4 * n0);
-  s.full16 = c.take<uint8_t>(n0);
   s.tiles = c.take<int>(pd_tma_partials(W, H, 10) + 1);
   P.bytes = c.off;
   return FSB_OK;
@@ -388,9 +392,9 @@ int pd_iterate_blocked(const fsb_level* L, const fsb_params* prm, int iters, flo
 
 int solve_level_internal(const fsb_level* L, const fsb_params* prm, const fsb_diag* diag,
                          int64_t pd_off, int64_t warp_off, void* scratch, size_t scratch_bytes,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool prepared = false) {
   const size_t n = (size_t)L->h * L->w;
-  int rc = level_prepare(L, prm, scratch, scratch_bytes, st);
+  int rc = prepared ? FSB_OK : level_prepare(L, prm, scratch, scratch_bytes, st);
   if (rc) return rc;
   // solver.py:323-327: v, p, q, v_bar start at zero, u_bar = u
   cudaMemsetAsync(L->v, 0, 2 * n * sizeof(float), st);
@@ -418,6 +422,53 @@ int solve_level_internal(const fsb_level* L, const fsb_params* prm, const fsb_di
   }
   return FSB_OK;
 }
+
+namespace {
+
+// Side stream of a caller stream (one per device and caller stream, created on
+// first use and kept): the per-level setup of every level (trajectory field,
+// tensor, steps, gather tables) runs there, ahead of and concurrently with the
+// level solves on the caller's stream, which wait on one event per level. The
+// coarse levels (64^2 - 256^2) leave most SMs idle, so the finer levels'
+// setup fills them. Works eagerly and under stream capture (fork / join by
+// events). FSB_OVERLAP=0 keeps everything on the caller's stream.
+struct SideCtx {
+  int dev;
+  cudaStream_t main, side;
+  cudaEvent_t ev[kMaxLevels + 2];
+};
+
+SideCtx* side_ctx(cudaStream_t main) {
+  static const bool off = [] {
+    const char* e = getenv("FSB_OVERLAP");
+    return e && e[0] == '0';
+  }();
+  if (off) return nullptr;
+  static std::mutex mu;
+  static std::vector<SideCtx*> ctxs;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  for (SideCtx* c : ctxs)
+    if (c->dev == dev && c->main == main) return c;
+  SideCtx* c = new SideCtx();
+  c->dev = dev;
+  c->main = main;
+  if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    cudaGetLastError();
+    return nullptr;
+  }
+  for (cudaEvent_t& e : c->ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;  // (leaks the partial context; never expected)
+    }
+  ctxs.push_back(c);
+  return c;
+}
+
+}  // namespace
 
 int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const float* i0,
                            const float* i1, const float* const* traj_dirs,
@@ -449,6 +500,23 @@ int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const floa
     if (diag->mean_abs_du) cudaMemsetAsync(diag->mean_abs_du, 0, nw * sizeof(double), st);
   }
 
+  // fork: trajectory fields (rig only) start on the side stream right away
+  SideCtx* sc = side_ctx(st);
+  cudaStream_t ss = sc ? sc->side : st;
+  if (sc) {
+    cudaEventRecord(sc->ev[0], st);
+    cudaStreamWaitEvent(ss, sc->ev[0], 0);
+  }
+  auto traj_level = [&](int l) -> int {
+    const int h = P.shapes[2 * l], w = P.shapes[2 * l + 1];
+    fsb_camera cl = scaled_to(rig->cam0, h, w);
+    return trajectory_field_internal(&cl, t_res, prm->epsilon_scale, 1.0, P.traj[l],
+                                     P.traj_ok[l], P.traj_scratch, P.traj_scratch_bytes, ss);
+  };
+  if (!traj_dirs)
+    for (int l = P.nlev - 1; l >= 1; --l)
+      if ((rc = traj_level(l))) return rc;
+
   // masks + calibration (solver.py:418-420)
   rc = fov_mask_internal(&rig->cam0, P.mask0, P.iters + 0, st);
   if (rc) return rc;
@@ -473,6 +541,44 @@ int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const floa
     if (rc) return rc;
   }
 
+  // fsb_level views of every level (coarse -> fine index k)
+  LevelState& S = P.st;
+  std::vector<fsb_level> lv(P.nlev);
+  for (int k = 0; k < P.nlev; ++k) {
+    const int l = P.nlev - 1 - k;
+    const int h = P.shapes[2 * l], w = P.shapes[2 * l + 1];
+    const size_t np = (size_t)h * w;
+    fsb_level& L = lv[k];
+    memset(&L, 0, sizeof(L));
+    float* u = S.state_a;  // plane 0 of the level's state block
+    L.h = h; L.w = w;
+    L.i0 = P.lvl_i0[l]; L.i1 = P.lvl_i1[l]; L.mask = P.lvl_mask[l];
+    L.traj = traj_dirs ? traj_dirs[k] : P.traj[l];
+    L.traj_ok = traj_dirs ? traj_okv[k] : P.traj_ok[l];
+    L.u = u; L.u_bar = u + np; L.v = u + 2 * np; L.v_bar = u + 4 * np; L.p = u + 6 * np;
+    L.q = u + 8 * np;
+    L.tensor = S.consts[l]; L.steps = S.consts[l] + 3 * np; L.iu = S.consts[l] + 6 * np;
+    L.rho0 = S.consts[l] + 7 * np; L.u_omega = S.consts[l] + 8 * np;
+    L.maskf = S.consts[l] + 9 * np;
+    L.i1w = S.i1w;
+    L.i1w_ok = S.i1w_ok; L.dirs = S.dirs; L.dir_ok = S.dir_ok; L.partials = S.partials;
+    L.tiles = S.tiles;
+    L.state_b = S.state_b;
+    L.packed = S.packed[l]; L.full16 = S.full16[l];
+  }
+  // side stream: after the pyramids, every level's setup, coarse first, one
+  // event per level (the finest trajectory field goes after the coarse setups)
+  if (sc) {
+    cudaEventRecord(sc->ev[kMaxLevels + 1], st);
+    cudaStreamWaitEvent(ss, sc->ev[kMaxLevels + 1], 0);
+  }
+  for (int k = 0; k < P.nlev; ++k) {
+    if (!traj_dirs && k == P.nlev - 1 && (rc = traj_level(0))) return rc;
+    rc = level_prepare(&lv[k], prm, P.setup_scratch, P.setup_scratch_bytes, ss);
+    if (rc) return rc;
+    if (sc) cudaEventRecord(sc->ev[1 + k], ss);
+  }
+
   int64_t pd_off = 0, warp_off = 0;
   int cur = 0;
   int prev_h = 0, prev_w = 0;
@@ -482,20 +588,6 @@ int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const floa
     const int h = P.shapes[2 * l], w = P.shapes[2 * l + 1];
     const size_t np = (size_t)h * w;
     const LevelRange nvtx_range("fsb level %dx%d", w, h);  // NVTX range per level
-    const float* traj;
-    const uint8_t* tok;
-    if (traj_dirs) {
-      traj = traj_dirs[k];
-      tok = traj_okv[k];
-    } else {
-      fsb_camera cl = scaled_to(rig->cam0, h, w);
-      rc = trajectory_field_internal(&cl, t_res, prm->epsilon_scale, 1.0, P.traj[l], P.traj_ok[l],
-                                     P.traj_scratch, P.traj_scratch_bytes, st);
-      if (rc) return rc;
-      traj = P.traj[l];
-      tok = P.traj_ok[l];
-    }
-    LevelState& S = P.st;
     float* u = S.state_a;  // plane 0 of the level's state block
     float* wv = S.wv[cur];
     if (k == 0) {
@@ -506,22 +598,11 @@ int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const floa
                              h, w, u, wv, st);
       if (rc) return rc;
     }
-    fsb_level L;
-    memset(&L, 0, sizeof(L));
-    L.h = h; L.w = w;
-    L.i0 = P.lvl_i0[l]; L.i1 = P.lvl_i1[l]; L.mask = P.lvl_mask[l];
-    L.traj = traj; L.traj_ok = tok;
-    L.u = u; L.u_bar = u + np; L.v = u + 2 * np; L.v_bar = u + 4 * np; L.p = u + 6 * np;
-    L.q = u + 8 * np;
-    L.tensor = S.consts; L.steps = S.consts + 3 * np; L.iu = S.consts + 6 * np;
-    L.rho0 = S.consts + 7 * np; L.u_omega = S.consts + 8 * np; L.maskf = S.consts + 9 * np;
-    L.wv = wv; L.i1w = S.i1w;
-    L.i1w_ok = S.i1w_ok; L.dirs = S.dirs; L.dir_ok = S.dir_ok; L.partials = S.partials;
-    L.tiles = S.tiles;
-    L.state_b = S.state_b;
-    L.packed = S.packed; L.full16 = S.full16;
+    fsb_level L = lv[k];
+    L.wv = wv;
+    if (sc) cudaStreamWaitEvent(st, sc->ev[1 + k], 0);  // join: this level's setup done
     rc = solve_level_internal(&L, prm, diag, pd_off, warp_off, P.setup_scratch,
-                              P.setup_scratch_bytes, st);
+                              P.setup_scratch_bytes, st, /*prepared=*/true);
     if (rc) return rc;
     pd_off += (int64_t)N * K;
     warp_off += N;
@@ -627,6 +708,7 @@ int capture_graph(void* stream, fsb_graph** out, int64_t* n_kernels, Enqueue enq
   if (!out || !stream) return FSB_EINVAL;  // capture needs a non-default stream
   *out = nullptr;
   cudaStream_t st = as_stream(stream);
+  side_ctx(st);  // create the side stream / events outside the capture
   cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return (int)e;
   int rc = enqueue(st);
