@@ -510,7 +510,7 @@ def run_b200(a) -> None:
     if not a.no_e2e:
         h0 = img0.cpu().numpy().astype(np.float64)
         h1 = img1.cpu().numpy().astype(np.float64)
-        for _ in range(max(a.warmup, 3)):  # engine build, graph capture, pinned-pool warm-up
+        for _ in range(max(a.warmup, 10)):  # engine build, graph capture, pinned pool, host threads
             res = solve_pyramid(h0, h1, rig, prm)
         del res
         torch.cuda.synchronize()
