@@ -188,6 +188,21 @@ __global__ void k_and_mask(const uint8_t* __restrict__ a, const uint8_t* __restr
   if (i < n) o[i] = a[i] && b[i];
 }
 
+// Frame outputs of the finest level (solver.py:451-452): u, w copied, v from
+// planes to the interleaved (H,W,2) layout, the solve mask.
+__global__ void k_outputs(const float* __restrict__ u, const float2* __restrict__ wv,
+                          const float* __restrict__ v0, const float* __restrict__ v1,
+                          const uint8_t* __restrict__ m, size_t n, float* __restrict__ uo,
+                          float2* __restrict__ wo, float2* __restrict__ vo,
+                          uint8_t* __restrict__ mo) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uo[i] = u[i];
+  wo[i] = wv[i];
+  vo[i] = make_float2(v0[i], v1[i]);
+  mo[i] = m[i];
+}
+
 }  // namespace
 
 size_t level_partials_count(int h, int w) { return level_partials_internal(h, w) + 64; }
@@ -609,14 +624,11 @@ int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const floa
     prev_h = h; prev_w = w; prev_mask = P.lvl_mask[l];
     if (l > 0) cudaMemcpyAsync(S.carry_u, u, np * sizeof(float), cudaMemcpyDeviceToDevice, st);
     if (l == 0) {
-      cudaMemcpyAsync(u_out, u, n0 * sizeof(float), cudaMemcpyDeviceToDevice, st);
-      cudaMemcpyAsync(w_out, wv, 2 * n0 * sizeof(float), cudaMemcpyDeviceToDevice, st);
-      // v planes -> interleaved (H,W,2) output
-      cudaMemcpy2DAsync(v_out, 2 * sizeof(float), L.v, sizeof(float), sizeof(float), n0,
-                        cudaMemcpyDeviceToDevice, st);
-      cudaMemcpy2DAsync(v_out + 1, 2 * sizeof(float), L.v + n0, sizeof(float), sizeof(float), n0,
-                        cudaMemcpyDeviceToDevice, st);
-      cudaMemcpyAsync(mask_out, P.solve_mask, n0, cudaMemcpyDeviceToDevice, st);
+      // one pass: u, w, the v planes interleaved to (H,W,2), mask (two 4-byte-wide
+      // cudaMemcpy2DAsync copies for v alone measured 185 us per frame)
+      k_outputs<<<(unsigned)((n0 + 255) / 256), 256, 0, st>>>(
+          u, reinterpret_cast<const float2*>(wv), L.v, L.v + n0, P.solve_mask, n0, u_out,
+          reinterpret_cast<float2*>(w_out), reinterpret_cast<float2*>(v_out), mask_out);
     }
     cur ^= 1;
   }
