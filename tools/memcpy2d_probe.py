@@ -34,3 +34,26 @@ for name, f in (("memcpy2d", memcpy2d), ("torch", tcopy)):
     e1.record()
     torch.cuda.synchronize()
     print(name, round(e0.elapsed_time(e1) / 20 * 1e3, 1), "us")
+
+# contiguous D2D memcpy / memset of the level-start state (1024^2: 12 planes)
+big_s = torch.randn(12 * n, device="cuda")
+big_d = torch.empty_like(big_s)
+def d2d():
+    assert rt.cudaMemcpyAsync(C.c_void_p(big_d.data_ptr()), C.c_void_p(big_s.data_ptr()),
+                              C.c_size_t(12 * n * 4), C.c_int(3), C.c_void_p(st)) == 0
+def mset():
+    assert rt.cudaMemsetAsync(C.c_void_p(big_d.data_ptr()), C.c_int(0), C.c_size_t(12 * n * 4),
+                              C.c_void_p(st)) == 0
+def tcopy_big():
+    big_d.copy_(big_s)
+for name, f in (("d2d 48MB", d2d), ("memset 48MB", mset), ("torch copy 48MB", tcopy_big)):
+    for _ in range(3):
+        f()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        f()
+    e1.record()
+    torch.cuda.synchronize()
+    print(name, round(e0.elapsed_time(e1) / 20 * 1e3, 1), "us")
