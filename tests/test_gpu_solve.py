@@ -183,3 +183,35 @@ def test_results_stay_fresh_with_pinned_pool():
     assert len(eng._out_pool) == n_sets <= 3
     assert np.array_equal(r3.u, u1)
     assert r3.u.flags.writeable and r3.mask.dtype == bool
+
+
+_OVERLAP_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+from conftest import load_golden
+import test_gpu_solve as T
+from paper_1909_07545_b200.solver import Solver
+g = load_golden("pyramid_solve")
+r = Solver(T._rig(g), T._params(g)).solve(g["i0"], g["i1"])
+np.savez(sys.argv[2], u=r.u, w=r.w, v=r.v)
+"""
+
+
+def test_side_stream_overlap_is_bit_identical(tmp_path):
+    """Per-level setup on the side stream (default) and everything on the
+    caller's stream (FSB_OVERLAP=0, read once per process: a child process)
+    give bit-identical frames."""
+    import os
+    import subprocess
+    import sys
+    from conftest import ROOT
+    from paper_1909_07545_b200.solver import Solver
+    g = load_golden("pyramid_solve")
+    r = Solver(_rig(g), _params(g)).solve(g["i0"], g["i1"])
+    out = tmp_path / "serial.npz"
+    env = dict(os.environ, FSB_OVERLAP="0")
+    subprocess.run([sys.executable, "-c", _OVERLAP_CHILD, str(ROOT), str(out)], env=env,
+                   check=True, timeout=600)
+    with np.load(out) as z:
+        assert np.array_equal(z["u"], r.u) and np.array_equal(z["w"], r.w)
+        assert np.array_equal(z["v"], r.v)
