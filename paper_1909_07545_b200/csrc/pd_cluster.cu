@@ -71,7 +71,10 @@ constexpr int kMaxRows = 16, kMaxCols = 192;  // per CTA band: rows x padded col
 constexpr int kPlanes = 9;                     // ub vb0 vb1 | px py q0x q0y q1x q1y
 constexpr int kMaxWarps = 64;                  // warp iterations with the in-kernel mean
 
-__global__ void __launch_bounds__(512, 1) k_level_cluster(const ClusterArgs A) {
+// MAXT: block size bound. Bands of <= 256 threads (64^2 levels) get up to
+// 255 registers instead of 128 (no spills in the sampling part).
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_level_cluster(const ClusterArgs A) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank(), ncta = (int)cluster.num_blocks();
   extern __shared__ float s_dyn[];  // kPlanes planes of rpc rows x (ncols + 2) columns
@@ -431,16 +434,21 @@ int level_cluster_solve(const fsb_level* L, const fsb_params* prm, const fsb_dia
     A.diag_du = diag->max_du + warp_off;
     A.diag_mean = diag->mean_abs_du + warp_off;
   }
+  const int nthreads = 32 * A.wr * A.rpc;
+  void (*kern)(const ClusterArgs) =
+      nthreads <= 256 ? k_level_cluster<256> : k_level_cluster<512>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_level_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(k_level_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kPlanes * kMaxRows * (kMaxCols + 2) * (int)sizeof(float));
+    for (auto k : {k_level_cluster<256>, k_level_cluster<512>}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kPlanes * kMaxRows * (kMaxCols + 2) * (int)sizeof(float));
+    }
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ncta, 1, 1);
-  cfg.blockDim = dim3(32 * A.wr * A.rpc, 1, 1);
+  cfg.blockDim = dim3(nthreads, 1, 1);
   cfg.dynamicSmemBytes = (size_t)kPlanes * A.rpc * (A.wr * 64 + 2) * sizeof(float);
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -450,7 +458,7 @@ int level_cluster_solve(const fsb_level* L, const fsb_params* prm, const fsb_dia
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_level_cluster, A);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A);
   if (e != cudaSuccess) return (int)e;
   return launch_status();
 }
