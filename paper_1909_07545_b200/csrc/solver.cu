@@ -474,11 +474,17 @@ SideCtx* side_ctx(cudaStream_t main) {
     cudaGetLastError();
     return nullptr;
   }
-  for (cudaEvent_t& e : c->ev)
+  int made = 0;
+  for (cudaEvent_t& e : c->ev) {
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
       cudaGetLastError();
-      return nullptr;  // (leaks the partial context; never expected)
+      for (int k = 0; k < made; ++k) cudaEventDestroy(c->ev[k]);
+      cudaStreamDestroy(c->side);
+      delete c;
+      return nullptr;  // callers fall back to the caller's stream
     }
+    ++made;
+  }
   ctxs.push_back(c);
   return c;
 }
