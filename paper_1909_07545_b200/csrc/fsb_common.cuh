@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -441,6 +442,16 @@ FSB_INLINE void atomic_max_nonneg(float* addr, float v) {
 FSB_INLINE void atomic_max_nonneg(double* addr, double v) {
   atomicMax(reinterpret_cast<unsigned long long*>(addr),
             (unsigned long long)__double_as_longlong(v));
+}
+
+// True the first time it is called for the current device with this mask:
+// kernel attributes (dynamic shared memory, cluster size) are per device, so
+// they are set once per device, not once per process.
+inline bool once_per_device(std::atomic<unsigned long long>& mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return true;
+  const unsigned long long bit = 1ull << (dev & 63);
+  return !(mask.fetch_or(bit) & bit);
 }
 
 }  // namespace fsb

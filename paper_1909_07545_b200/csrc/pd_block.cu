@@ -272,12 +272,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_pd_block(const BlockArgs A) {
 template <int CX, int NW, int PY, int R, bool LIN, bool FIN>
 int launch_shape(const BlockArgs& A, cudaStream_t st, int* nblocks) {
   using TL = Tile<CX, NW, PY, R>;
-  static bool attr = false;
+  static std::atomic<unsigned long long> attr{0};
   auto kern = k_pd_block<CX, NW, PY, R, LIN, FIN>;
-  if (!attr) {
+  if (once_per_device(attr))
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TL::SMEM);
-    attr = true;
-  }
   dim3 grd((A.w + TL::TW - 1) / TL::TW, (A.h + TL::TH - 1) / TL::TH);
   if (nblocks) *nblocks = (int)(grd.x * grd.y);
   kern<<<grd, NW * 32, TL::SMEM, st>>>(A);

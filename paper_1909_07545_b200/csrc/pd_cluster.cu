@@ -437,14 +437,13 @@ int level_cluster_solve(const fsb_level* L, const fsb_params* prm, const fsb_dia
   const int nthreads = 32 * A.wr * A.rpc;
   void (*kern)(const ClusterArgs) =
       nthreads <= 256 ? k_level_cluster<256> : k_level_cluster<512>;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (once_per_device(attr)) {
     for (auto k : {k_level_cluster<256>, k_level_cluster<512>}) {
       cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kPlanes * kMaxRows * (kMaxCols + 2) * (int)sizeof(float));
     }
-    attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ncta, 1, 1);

@@ -460,12 +460,10 @@ int launch_tma(const BlockArgs& A, const CUtensorMap& ms, const CUtensorMap& mc,
                int* ntiles_out) {
   constexpr int TW = kEW - 2 * R, TH = kEH - 2 * R;
   const int ntx = (A.w + TW - 1) / TW, nty = (A.h + TH - 1) / TH, ntiles = ntx * nty;
-  static bool attr = false;
+  static std::atomic<unsigned long long> attr{0};
   auto kern = k_pd_tma<R, LIN, FIN, DIAG>;
-  if (!attr) {
+  if (once_per_device(attr))
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-    attr = true;
-  }
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
   if (ntiles_out) *ntiles_out = ntiles;
   kern<<<grid, kNW * 32, kSmemBytes, st>>>(A, ms, mc, ntx, ntiles, A.tile_list);
