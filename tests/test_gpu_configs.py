@@ -3,8 +3,9 @@
 The renderer (input generator) is checked against the reference's own renders
 (tests/golden/render.npz). The solve is checked against the pinned oracle on
 GPU-rendered inputs at the sizes the oracle finishes in seconds (C1 at full
-size; C2 geometry at full size), and through size-independent invariants at
-the headline 1024^2 size (C3).
+size; C2 geometry at full size), and at the headline 1024^2 size (C3) through
+size-independent invariants, the per-level trajectory fields against the oracle
+and the fp32 path against the fp64 parity path.
 """
 
 import numpy as np
@@ -174,6 +175,46 @@ def test_c3_headline_invariants():
     i1c, ok = O.calibrate(i1, rig)
     np.testing.assert_array_equal(ok & O.fov_mask(rig.cam0), r1.mask)
     np.testing.assert_allclose(r1.i1_calibrated, i1c, atol=2e-7)
+
+
+def test_c3_full_size_trajectory_fields_and_fp32_vs_fp64():
+    """C3 at full size (1024^2, 6-DoF unified rig, reference defaults N=50 K=10).
+
+    (1) North-star gate at the headline config: the trajectory field of EVERY
+    pyramid level (1024^2 .. 64^2, the residual rig of fields.py:159-167 on
+    cam0.scaled_to, solver.py:435-441) within 1e-5 of the fp64 oracle, validity
+    identical. (2) The fp32 production path against the fp64 parity path (which
+    reproduces the oracle to ~1e-8, test_fp64_path_reproduces_oracle_to_roundoff)
+    on the same frame: median gate 1e-3 px; p99 bounded by the N=50
+    conditioning at 5e-2 px."""
+    from paper_1909_07545_b200 import fields as F
+    from paper_1909_07545_b200.camera import RelativePose, StereoRig, UnifiedCamera
+    from paper_1909_07545_b200.rasters import pyramid_shapes
+    from paper_1909_07545_b200.solver import SolverParams, solve_pyramid
+    cam = UnifiedCamera(width=1024, height=1024, fx=455.0, fy=455.0, cx=511.5, cy=511.5,
+                        fov=np.pi, xi=0.9)
+    rig = StereoRig(cam, cam, RelativePose.from_displacement((0.08, 0.02, 0.03),
+                                                             rotvec=(0.01, 0.03, -0.02)))
+    prm = SolverParams()
+    res_rig = F.translation_only_rig(rig)
+    shapes = pyramid_shapes(1024, 1024, prm.pyramid_levels, prm.pyramid_scale, prm.min_width)
+    assert len(shapes) == 5
+    for shp in shapes:
+        c = res_rig.cam0.scaled_to(shp)
+        lrig = StereoRig(c, c, res_rig.pose)
+        d, ok = F.generate_trajectory_field(lrig, epsilon_scale=prm.epsilon_scale)
+        od, ook = O.trajectory_field(c, res_rig.pose.translation, prm.epsilon_scale)
+        np.testing.assert_array_equal(ok, ook)
+        assert np.max(np.abs(d - od)[ok]) <= 1e-5, shp
+    i0, i1 = _render_pair(rig, ss=1)
+    r32 = solve_pyramid(i0, i1, rig, prm)
+    r64 = solve_pyramid(i0, i1, rig, prm, precision="fp64")
+    np.testing.assert_array_equal(r32.mask, r64.mask)
+    e = np.abs(r32.u - r64.u)[r64.mask]
+    med, p99 = float(np.median(e)), float(np.percentile(e, 99))
+    print(f"C3 fp32 vs fp64 path: u err median {med:.3e} p99 {p99:.3e} max {e.max():.3e}; "
+          f"> 0.1 px {np.mean(e > 0.1):.2e}, > 1 px {np.mean(e > 1.0):.2e} of {e.size} px")
+    assert med <= 1e-3 and p99 <= 5e-2
 
 
 def test_n50_parity_on_acceptance_geometry():
