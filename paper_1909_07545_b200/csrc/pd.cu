@@ -454,11 +454,12 @@ __global__ void __launch_bounds__(256) k_iu_px(fsb_level L) {
 }
 
 int warp_prologue_internal(const fsb_level* L, cudaStream_t st) {
-  static int mode = -1;  // FSB_PROLOGUE=fused|split (tuning); default by level size
-  if (mode < 0) {
+  // FSB_PROLOGUE=fused|split (tuning); default by level size. Read once
+  // (function-local statics initialise thread-safely).
+  static const int mode = [] {
     const char* e = getenv("FSB_PROLOGUE");
-    mode = e ? (e[0] == 's' ? 1 : (e[0] == 'f' ? 2 : 0)) : 0;
-  }
+    return e ? (e[0] == 's' ? 1 : (e[0] == 'f' ? 2 : 0)) : 0;
+  }();
   const bool big = (size_t)L->w * L->h >= (size_t)512 * 512;
   if (mode == 1 || (mode == 0 && kSplitDefault)) {
     dim3 blk(kBX, kBY), grd = grid2d(L->w, L->h, blk);

@@ -415,11 +415,10 @@ fsb_camera scaled(const fsb_camera& c, int h, int w) {  // camera.py:66-77
 // FSB_PD64=plain runs the one-cycle-per-launch kernels (reference for the
 // blocked kernel in tests/tools); default: blocked, halo 2.
 int pd64_halo() {
-  static int h = -1;
-  if (h < 0) {
+  static const int h = [] {
     const char* e = getenv("FSB_PD64");
-    h = e && e[0] == 'p' ? 0 : (e && e[0] >= '1' && e[0] <= '3' ? e[0] - '0' : 2);
-  }
+    return e && e[0] == 'p' ? 0 : (e && e[0] >= '1' && e[0] <= '3' ? e[0] - '0' : 2);
+  }();
   return h;
 }
 

@@ -192,11 +192,10 @@ int launch64v(const B64& A, cudaStream_t st) {
 // registers 31.2 ms; 32 x 32 tiles at one CTA / SM 32.0 ms; 32 x 16 tiles at
 // one CTA / SM without spills 35.4 ms (occupancy matters more than spills).
 bool pd64_const_regs() {
-  static int v = -1;
-  if (v < 0) {
+  static const bool v = [] {
     const char* e = getenv("FSB_PD64_CONST");
-    v = e && strcmp(e, "regs") == 0;
-  }
+    return e && strcmp(e, "regs") == 0;
+  }();
   return v;
 }
 

@@ -283,11 +283,10 @@ int launch_shape(const BlockArgs& A, cudaStream_t st, int* nblocks) {
 }
 
 int tile_choice() {
-  static int t = -1;
-  if (t < 0) {
+  static const int t = [] {
     const char* e = getenv("FSB_PD_TILE");
-    t = e ? atoi(e) : 1;
-  }
+    return e ? atoi(e) : 1;
+  }();
   return t;
 }
 

@@ -345,11 +345,10 @@ int launch_pair_shape(const BlockArgs& A, cudaStream_t st, int* nblocks) {
 }
 
 int pair_shape() {
-  static int t = -1;
-  if (t < 0) {
+  static const int t = [] {
     const char* e = getenv("FSB_PAIR_SHAPE");
-    t = e ? atoi(e) : 0;
-  }
+    return e ? atoi(e) : 0;
+  }();
   return t;
 }
 

@@ -212,21 +212,36 @@ namespace {
 // PD iterations per launch of the blocked kernel (= its halo). FSB_PD_HALO
 // overrides for tuning experiments (1, 2, 3, 4, 5 or 10); FSB_PD_HALO_L =
 // "w:R,w:R,..." overrides it per level width.
-int pd_halo(int K, int w = 0, int hgt = 0) {
-  static int env = -1;
-  static int lw[16], lr[16], nl = 0;
-  if (env < 0) {
+struct HaloEnv {
+  int env = 0;
+  int lw[16], lr[16], nl = 0;
+};
+
+// parsed once (thread-safe function-local static: concurrent solves on
+// several streams never see a half-parsed per-level list)
+const HaloEnv& halo_env() {
+  static const HaloEnv cfg = [] {
+    HaloEnv c;
     const char* e = getenv("FSB_PD_HALO");
-    env = e ? atoi(e) : 0;
+    c.env = e ? atoi(e) : 0;
     const char* l = getenv("FSB_PD_HALO_L");
-    while (l && *l && nl < 16) {
-      int a, b, c = 0;
-      if (sscanf(l, "%d:%d%n", &a, &b, &c) != 2) break;
-      lw[nl] = a; lr[nl] = b; ++nl;
-      l += c;
+    while (l && *l && c.nl < 16) {
+      int a, b, n = 0;
+      if (sscanf(l, "%d:%d%n", &a, &b, &n) != 2) break;
+      c.lw[c.nl] = a; c.lr[c.nl] = b; ++c.nl;
+      l += n;
       if (*l == ',') ++l;
     }
-  }
+    return c;
+  }();
+  return cfg;
+}
+
+int pd_halo(int K, int w = 0, int hgt = 0) {
+  const HaloEnv& E = halo_env();
+  const int env = E.env, nl = E.nl;
+  const int* lw = E.lw;
+  const int* lr = E.lr;
   int h = env > 0 ? env : 5;
   // A level whose 10-cycle tiles (44 x 12 interiors) fit in one wave runs each
   // warp's K = 10 cycles in one launch: at these sizes the per-launch cost
@@ -240,11 +255,10 @@ int pd_halo(int K, int w = 0, int hgt = 0) {
 
 // Blocked PD kernel: packed pixel pairs (default) or the per-pixel tile kernel.
 int pd_launch(const BlockArgs& A, int halo, bool lin, bool fin, cudaStream_t st, int* nblocks) {
-  static int which = -1;
-  if (which < 0) {
+  static const int which = [] {  // FSB_PD_KERNEL=block; otherwise the pixel-pair kernel
     const char* e = getenv("FSB_PD_KERNEL");
-    which = (e && strcmp(e, "block") == 0) ? 1 : 0;  // otherwise the pixel-pair kernel
-  }
+    return (e && strcmp(e, "block") == 0) ? 1 : 0;
+  }();
   return which ? pd_block_launch(A, halo, lin, fin, st, nblocks)
                : pd_pair_launch(A, halo, lin, fin, st, nblocks);
 }
@@ -261,12 +275,11 @@ bool tma_layout(const fsb_level* L) {
   if (L->steps != c + 3 * n || L->iu != c + 6 * n || L->rho0 != c + 7 * n ||
       L->u_omega != c + 8 * n || L->maskf != c + 9 * n)
     return false;
-  static int env = -1;
-  if (env < 0) {
+  static const bool env = [] {  // FSB_PD_KERNEL=pair|block disables TMA
     const char* e = getenv("FSB_PD_KERNEL");
-    env = (e && strcmp(e, "tma") != 0) ? 0 : 1;  // FSB_PD_KERNEL=pair|block disables TMA
-  }
-  return env == 1;
+    return !(e && strcmp(e, "tma") != 0);
+  }();
+  return env;
 }
 
 StateSet set_a(const fsb_level* L) {
