@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import sys
+import threading
 from collections import OrderedDict
 from dataclasses import asdict, dataclass, field
 
@@ -596,6 +597,7 @@ class Solver:
 
 _CACHE: "OrderedDict[tuple, Solver]" = OrderedDict()
 _CACHE_SIZE = 4
+_CACHE_LOCK = threading.Lock()
 
 
 def _rig_key(rig) -> tuple:
@@ -627,15 +629,24 @@ def solve_pyramid(i0, i1, rig, params: SolverParams, collect_diagnostics: bool =
     if traj_override is None and not np.any(rig.pose.rotation.T @ rig.pose.translation):
         raise ValueError("trajectory field undefined for zero baseline")
     key = (_rig_key(rig), tuple(asdict(params).items()), bool(collect_diagnostics), precision)
-    eng = None if traj_override is not None else _CACHE.get(key)
+    if traj_override is not None:
+        eng = Solver(rig, params, collect_diagnostics, precision)
+        eng.set_traj_override(traj_override)
+        return eng.solve(i0a, i1a)
+    # An engine is exclusive-use (workspace, graph, staging): it is checked OUT
+    # of the cache for the call, so concurrent callers with the same rig each
+    # get their own engine and the function stays re-entrant like the
+    # reference's.
+    with _CACHE_LOCK:
+        eng = _CACHE.pop(key, None)
     if eng is None:
         eng = Solver(rig, params, collect_diagnostics, precision)
-        if traj_override is not None:
-            eng.set_traj_override(traj_override)
-        else:
-            _CACHE[key] = eng
+    try:
+        return eng.solve(i0a, i1a)
+    finally:
+        with _CACHE_LOCK:
+            if key not in _CACHE:  # a concurrent caller's engine may be back first
+                _CACHE[key] = eng
+            _CACHE.move_to_end(key)
             while len(_CACHE) > _CACHE_SIZE:
                 _CACHE.popitem(last=False)
-    else:
-        _CACHE.move_to_end(key)
-    return eng.solve(i0a, i1a)

@@ -185,6 +185,38 @@ def test_results_stay_fresh_with_pinned_pool():
     assert r3.u.flags.writeable and r3.mask.dtype == bool
 
 
+def test_concurrent_callers_same_rig():
+    """solve_pyramid is re-entrant like the reference: threads
+    solving with the same (rig, params) check out separate engines and each get
+    the serial result, bit for bit."""
+    import threading
+    from paper_1909_07545_b200.solver import solve_pyramid
+    g = load_golden("pyramid_solve")
+    rig, prm = _rig(g), _params(g)
+    pairs = [(g["i0"], g["i1"]), (np.flipud(g["i0"]).copy(), np.flipud(g["i1"]).copy())]
+    want = [solve_pyramid(a, b, rig, prm) for a, b in pairs]
+    out, errs = {}, []
+
+    def work(t):
+        try:
+            for k in range(6):
+                j = (t + k) % 2
+                r = solve_pyramid(*pairs[j], rig, prm)
+                out[(t, k)] = (j, r.u.copy(), r.w.copy())
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    assert len(out) == 24
+    for j, u, w in out.values():
+        assert np.array_equal(u, want[j].u) and np.array_equal(w, want[j].w)
+
+
 _OVERLAP_CHILD = r"""
 import sys, numpy as np
 sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
