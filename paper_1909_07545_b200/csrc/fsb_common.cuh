@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 #include <atomic>
+#include <mutex>
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -444,14 +445,24 @@ FSB_INLINE void atomic_max_nonneg(double* addr, double v) {
             (unsigned long long)__double_as_longlong(v));
 }
 
-// True the first time it is called for the current device with this mask:
-// kernel attributes (dynamic shared memory, cluster size) are per device, so
-// they are set once per device, not once per process.
-inline bool once_per_device(std::atomic<unsigned long long>& mask) {
+// Runs `set` once per device for this `done` mask: kernel attributes (dynamic
+// shared memory, cluster size) are per device, so they are set once per
+// device, not once per process. The bit is published only after `set` ran
+// (under a lock), so a concurrent first launch never sees it early.
+template <class F>
+inline void once_per_device(std::atomic<unsigned long long>& done, F&& set) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return true;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    set();
+    return;
+  }
   const unsigned long long bit = 1ull << (dev & 63);
-  return !(mask.fetch_or(bit) & bit);
+  if (done.load(std::memory_order_acquire) & bit) return;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.load(std::memory_order_relaxed) & bit) return;
+  set();
+  done.fetch_or(bit, std::memory_order_release);
 }
 
 }  // namespace fsb

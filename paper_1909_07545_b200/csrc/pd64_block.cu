@@ -181,9 +181,10 @@ int launch64v(const B64& A, cudaStream_t st) {
   const dim3 blk(kTX, TY), grd((A.w + TW - 1) / TW, (A.h + TH - 1) / TH);
   const size_t dyn = CS ? sizeof(Tile64<TY>) : offsetof(Tile64<TY>, c);
   static std::atomic<unsigned long long> attr{0};
-  if (once_per_device(attr))
+  once_per_device(attr, [&] {
     cudaFuncSetAttribute(k64_block<R, TY, DIAG, CS, MINB>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  });
   k64_block<R, TY, DIAG, CS, MINB><<<grd, blk, dyn, st>>>(A);
   return launch_status();
 }

@@ -274,8 +274,9 @@ int launch_shape(const BlockArgs& A, cudaStream_t st, int* nblocks) {
   using TL = Tile<CX, NW, PY, R>;
   static std::atomic<unsigned long long> attr{0};
   auto kern = k_pd_block<CX, NW, PY, R, LIN, FIN>;
-  if (once_per_device(attr))
+  once_per_device(attr, [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TL::SMEM);
+  });
   dim3 grd((A.w + TL::TW - 1) / TL::TW, (A.h + TL::TH - 1) / TL::TH);
   if (nblocks) *nblocks = (int)(grd.x * grd.y);
   kern<<<grd, NW * 32, TL::SMEM, st>>>(A);

@@ -438,13 +438,13 @@ int level_cluster_solve(const fsb_level* L, const fsb_params* prm, const fsb_dia
   void (*kern)(const ClusterArgs) =
       nthreads <= 256 ? k_level_cluster<256> : k_level_cluster<512>;
   static std::atomic<unsigned long long> attr{0};
-  if (once_per_device(attr)) {
+  once_per_device(attr, [] {
     for (auto k : {k_level_cluster<256>, k_level_cluster<512>}) {
       cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kPlanes * kMaxRows * (kMaxCols + 2) * (int)sizeof(float));
     }
-  }
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ncta, 1, 1);
   cfg.blockDim = dim3(nthreads, 1, 1);

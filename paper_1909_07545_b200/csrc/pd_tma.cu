@@ -462,8 +462,9 @@ int launch_tma(const BlockArgs& A, const CUtensorMap& ms, const CUtensorMap& mc,
   const int ntx = (A.w + TW - 1) / TW, nty = (A.h + TH - 1) / TH, ntiles = ntx * nty;
   static std::atomic<unsigned long long> attr{0};
   auto kern = k_pd_tma<R, LIN, FIN, DIAG>;
-  if (once_per_device(attr))
+  once_per_device(attr, [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  });
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
   if (ntiles_out) *ntiles_out = ntiles;
   kern<<<grid, kNW * 32, kSmemBytes, st>>>(A, ms, mc, ntx, ntiles, A.tile_list);
