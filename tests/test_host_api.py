@@ -37,3 +37,55 @@ def test_solver_params_strict_from_dict():
     with pytest.raises(ValueError):
         SolverParams(pd_iters=0)
     assert SolverParams.from_dict(p.to_dict()) == p
+
+
+def test_engine_cache_checkout_is_exclusive(monkeypatch):
+    """solve_pyramid's engine cache (no GPU: the engine is stubbed): an engine
+    is never used by two threads at once, same-rig callers beyond the first get
+    their own engine, and the LRU keeps at most _CACHE_SIZE engines."""
+    import threading
+    import time
+    from paper_1909_07545_b200 import solver as SV
+    from paper_1909_07545_b200.camera import RelativePose, StereoRig, UnifiedCamera
+
+    made, clash = [], []
+
+    class FakeSolver:
+        def __init__(self, rig, params, diag=False, precision="fp32"):
+            self.busy = threading.Lock()
+            made.append(self)
+
+        def solve(self, i0, i1):
+            if not self.busy.acquire(blocking=False):
+                clash.append(self)
+                return None
+            try:
+                time.sleep(0.002)
+                return self
+            finally:
+                self.busy.release()
+
+    monkeypatch.setattr(SV, "Solver", FakeSolver)
+    monkeypatch.setattr(SV, "_CACHE", SV.OrderedDict())
+    cam = UnifiedCamera(width=8, height=6, fx=4.0, fy=4.0, cx=3.5, cy=2.5, fov=np.pi, xi=0.9)
+
+    def rig(k):
+        return StereoRig(cam, cam, RelativePose.from_displacement((0.1 + 0.01 * k, 0, 0)))
+
+    img = np.zeros((6, 8))
+    prm = SV.SolverParams()
+
+    def work(t):
+        for k in range(20):
+            SV.solve_pyramid(img, img, rig((t + k) % 6 if t % 2 else 0), prm)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(6)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not clash
+    assert len(SV._CACHE) <= SV._CACHE_SIZE
+    # serial reuse: the same rig twice in a row hits the cached engine
+    a = SV.solve_pyramid(img, img, rig(0), prm)
+    assert SV.solve_pyramid(img, img, rig(0), prm) is a
