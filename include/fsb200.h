@@ -164,6 +164,11 @@ int fsb_trajectory_field(const fsb_camera* cam, const double t[3], double epsilo
                          double depth, float* dirs, uint8_t* ok, void* scratch,
                          size_t scratch_bytes, void* stream);
 size_t fsb_trajectory_scratch_bytes(const fsb_camera* cam);
+/* The same with float64 directions (the reference's dtype; the fp64 path's own
+ * per-level field). */
+int fsb_trajectory_field_f64(const fsb_camera* cam, const double t[3], double epsilon_scale,
+                             double depth, double* dirs, uint8_t* ok, void* scratch,
+                             size_t scratch_bytes, void* stream);
 
 /* ---------------------------------------------------------------- rasters */
 
@@ -315,16 +320,38 @@ int fsb_solve_pyramid(const fsb_rig* rig, const fsb_params* prm, const float* i0
                       float* u, float* w, float* v, uint8_t* mask, float* i1c,
                       const fsb_diag* diag, void* stream);
 
-/* fp64 parity path of solve_pyramid: float64 images in, float64 fields out,
- * float64 storage and IEEE arithmetic in the reference's operation order (one
- * primal-dual cycle per launch). Matches the reference to round-off at any
- * warp count; the fp32 fsb_solve_pyramid is the production path. */
+/* float64 path of solve_pyramid (the default, credited path): float64 images
+ * in, float64 fields out, float64 storage and arithmetic in the reference's
+ * operation order (temporally blocked primal-dual tiles). Holds the north-star
+ * disparity gate against the reference at every configuration including C3 at
+ * N=50 (tests/test_gpu_c3_parity.py); the fp32 fsb_solve_pyramid is faster but
+ * misses the p99 gate at N=50. */
 size_t fsb_solve_pyramid_f64_workspace_bytes(const fsb_rig* rig, const fsb_params* prm);
 int fsb_solve_pyramid_f64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
                           const double* i1, const double* const* traj_dirs,
                           const uint8_t* const* traj_ok, void* workspace, size_t workspace_bytes,
                           double* u, double* w, double* v, uint8_t* mask, double* i1c,
                           const fsb_diag* diag, void* stream);
+
+/* Live kernel timing for the roofline (bench.py): a phase timer records, on
+ * the solve stream, three CUDA events per warp iteration of one pyramid level
+ * (`level` 0 = finest, up to `max_warps` warps): before the warp's sampling
+ * kernels (solver.py:332-346), between sampling and its primal-dual launches
+ * (solver.py:347-360), and after the last primal-dual launch. After the
+ * stream is synchronised, fsb_phase_timer_read returns the summed sampling and
+ * primal-dual milliseconds, the warps recorded, the PD launches per warp and
+ * the level shape. fsb_solve_pyramid_f64_timed is fsb_solve_pyramid_f64
+ * (no override, no diagnostics) with the timer attached; not for capture. */
+typedef struct fsb_phase_timer fsb_phase_timer;
+int fsb_phase_timer_create(int32_t level, int32_t max_warps, fsb_phase_timer** out);
+int fsb_phase_timer_read(fsb_phase_timer* timer, double* sample_ms, double* pd_ms,
+                         int32_t* warps, int32_t* pd_launches_per_warp, int32_t* level_h,
+                         int32_t* level_w);
+int fsb_phase_timer_destroy(fsb_phase_timer* timer);
+int fsb_solve_pyramid_f64_timed(const fsb_rig* rig, const fsb_params* prm, const double* i0,
+                                const double* i1, void* workspace, size_t workspace_bytes,
+                                double* u, double* w, double* v, uint8_t* mask, double* i1c,
+                                fsb_phase_timer* timer, void* stream);
 
 /* CUDA-graph form of fsb_solve_pyramid: captures one frame (same arguments,
  * fixed buffers) on `stream` into an executable graph; *n_kernels receives the

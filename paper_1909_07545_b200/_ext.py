@@ -26,13 +26,15 @@ EXPORTED = (
     "fsb_fov_mask", "fsb_fov_mask_scratch_bytes", "fsb_unproject", "fsb_project",
     "fsb_unproject_scratch_bytes", "fsb_calibration_field", "fsb_calibrate_second_image",
     "fsb_calibrate_scratch_bytes", "fsb_trace_epipolar_curves", "fsb_compose_calibration", "fsb_triangulate_midpoint",
-    "fsb_triangulate_scratch_bytes", "fsb_depth_from_correspondence", "fsb_trajectory_field", "fsb_trajectory_scratch_bytes",
+    "fsb_triangulate_scratch_bytes", "fsb_depth_from_correspondence", "fsb_trajectory_field", "fsb_trajectory_field_f64", "fsb_trajectory_scratch_bytes",
     "fsb_sample_bicubic", "fsb_gradient", "fsb_divergence", "fsb_smooth_masked",
     "fsb_smooth_scratch_bytes", "fsb_pyramid_shapes", "fsb_downsample_area",
     "fsb_upsample_state", "fsb_compute_tensor", "fsb_precondition_steps", "fsb_level_partials", "fsb_level_tiles", "fsb_level_setup", "fsb_warp_linearize",
     "fsb_pd_iterate", "fsb_thresholding_step", "fsb_warp_finish", "fsb_solve_level", "fsb_diag_counts",
     "fsb_solve_pyramid_workspace_bytes", "fsb_solve_pyramid",
     "fsb_solve_pyramid_f64_workspace_bytes", "fsb_solve_pyramid_f64", "fsb_render", "fsb_graph_create", "fsb_graph_create_f64", "fsb_graph_launch", "fsb_graph_destroy",
+    "fsb_phase_timer_create", "fsb_phase_timer_read", "fsb_phase_timer_destroy",
+    "fsb_solve_pyramid_f64_timed",
     "fsb_ground_truth", "fsb_error_report", "fsb_error_report_scratch_bytes", "fsb_version",
 )
 
@@ -115,6 +117,8 @@ def lib() -> C.CDLL:
                                                         vp, sz, vp]),
             "fsb_trajectory_field": (C.c_int, [P(FsbCamera), P(C.c_double), dbl, dbl, vp, vp,
                                                vp, sz, vp]),
+            "fsb_trajectory_field_f64": (C.c_int, [P(FsbCamera), P(C.c_double), dbl, dbl, vp, vp,
+                                               vp, sz, vp]),
             "fsb_trajectory_scratch_bytes": (sz, [P(FsbCamera)]),
             "fsb_sample_bicubic": (C.c_int, [vp, i32, i32, i32, vp, vp, i64, vp, vp, i32, vp]),
             "fsb_gradient": (C.c_int, [vp, vp, i32, i32, vp, vp]),
@@ -154,6 +158,12 @@ def lib() -> C.CDLL:
             "fsb_graph_create_f64": (C.c_int, [P(FsbRig), P(FsbParams), vp, vp, vp, vp, vp, sz,
                                                vp, vp, vp, vp, vp, P(FsbDiag), vp,
                                                P(C.c_void_p), P(C.c_int64)]),
+            "fsb_phase_timer_create": (C.c_int, [i32, i32, P(C.c_void_p)]),
+            "fsb_phase_timer_read": (C.c_int, [vp, P(C.c_double), P(C.c_double), P(C.c_int32),
+                                               P(C.c_int32), P(C.c_int32), P(C.c_int32)]),
+            "fsb_phase_timer_destroy": (C.c_int, [vp]),
+            "fsb_solve_pyramid_f64_timed": (C.c_int, [P(FsbRig), P(FsbParams), vp, vp, vp, sz,
+                                                      vp, vp, vp, vp, vp, vp, vp]),
             "fsb_graph_launch": (C.c_int, [vp, vp]),
             "fsb_graph_destroy": (C.c_int, [vp]),
             "fsb_version": (C.c_char_p, []),

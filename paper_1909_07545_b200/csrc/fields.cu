@@ -432,4 +432,11 @@ int fsb_trajectory_field(const fsb_camera* cam, const double t[3], double epsilo
                                    as_stream(stream));
 }
 
+int fsb_trajectory_field_f64(const fsb_camera* cam, const double t[3], double epsilon_scale,
+                             double depth, double* dirs, uint8_t* ok, void* scratch,
+                             size_t scratch_bytes, void* stream) {
+  return trajectory_field64_internal(cam, t, epsilon_scale, depth, dirs, ok, scratch,
+                                     scratch_bytes, as_stream(stream));
+}
+
 }  // extern "C"

@@ -41,6 +41,22 @@ int level_setup64_internal(const double* i0, const uint8_t* mask, int h, int w,
 int mean_finish_internal(const double* partials, int nparts, const uint8_t* mask, size_t n,
                          double* out, cudaStream_t st);
 
+}  // namespace fsb
+
+// Live per-warp phase events at one pyramid level (fsb200.h fsb_phase_timer):
+// three events per warp on the solve stream: before the sampling kernels,
+// between sampling and the primal-dual launches, after the last PD launch.
+struct fsb_phase_timer {
+  int level;          // 0 = finest
+  int cap;            // warps with events
+  int used;           // warps recorded by the last solve
+  int pd_launches;    // PD launches per warp at that level (last solve)
+  int level_h, level_w;
+  cudaEvent_t* ev;    // 3 * cap
+};
+
+namespace fsb {
+
 namespace {
 
 constexpr int kBX = 32, kBY = 8;
@@ -430,7 +446,8 @@ L64 swapped(const L64& L) {
 }
 
 int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, int64_t pd_off,
-                  int64_t warp_off, void* scratch, size_t scratch_bytes, cudaStream_t st) {
+                  int64_t warp_off, void* scratch, size_t scratch_bytes, cudaStream_t st,
+                  fsb_phase_timer* tm = nullptr) {
   L64 L = L0;  // L's state pointers follow the ping-pong of the blocked cycles
   const size_t n = L.n;
   if (L.full16) {
@@ -465,8 +482,12 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
       if (pd64_block_tiles(L.w, L.h, 5) <= 2 * 148) halo = 5;
       else if (pd64_block_tiles(L.w, L.h, 3) <= 2 * 148) halo = 3;
     }
+    const bool timed = tm && wi < tm->cap;
+    if (timed) cudaEventRecord(tm->ev[3 * wi], st);
     k64_sample<<<grd, blk, 0, st>>>(L);
     k64_linearize<<<grd, blk, 0, st>>>(L, halo == 0);
+    if (timed) cudaEventRecord(tm->ev[3 * wi + 1], st);
+    int pd_launches = 0;
     for (int k = 0; halo > 0 && k < K;) {  // blocked: `it` cycles per launch, src -> dst
       const int it = K - k < halo ? K - k : halo;
       B64 A;
@@ -487,6 +508,7 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
       A.partials = L.partials;
       rc = pd64_block_launch(A, halo, st);
       if (rc) return rc;
+      ++pd_launches;
       L = swapped(L);
       k += it;
       if (k == K && ddu) {
@@ -495,7 +517,15 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
         if (rc) return rc;
       }
     }
-    if (halo > 0) continue;  // the blocked launches fused k64_finish
+    if (halo > 0) {  // the blocked launches fused k64_finish
+      if (timed) {
+        cudaEventRecord(tm->ev[3 * wi + 2], st);
+        tm->used = wi + 1;
+        tm->pd_launches = pd_launches;
+        tm->level_h = L.h; tm->level_w = L.w;
+      }
+      continue;
+    }
     for (int k = 0; halo == 0 && k < K; ++k) {
       if (dpq) {
         const int64_t slot = pd_off + (int64_t)wi * K + k;
@@ -545,7 +575,8 @@ size_t solve_pyramid64_bytes(const fsb_rig* rig, const fsb_params* prm) {
 int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0, const double* i1,
                     const double* const* traj_dirs, const uint8_t* const* traj_okv, void* ws,
                     size_t ws_bytes, double* u_out, double* w_out, double* v_out,
-                    uint8_t* mask_out, double* i1c, const fsb_diag* diag, cudaStream_t st) {
+                    uint8_t* mask_out, double* i1c, const fsb_diag* diag, cudaStream_t st,
+                    fsb_phase_timer* tm = nullptr) {
   if (!rig || !params_ok64(prm) || !i0 || !i1 || !ws || !u_out || !w_out || !v_out ||
       !mask_out || !i1c)
     return FSB_EINVAL;
@@ -630,7 +661,8 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
     L.full16 = P.full16;
     L.wv = wv; L.uo = P.uo; L.iu = P.iu; L.rho0 = P.rho0; L.i1w = P.i1w; L.i1w_ok = P.i1w_ok;
     L.dirs = P.dirs; L.dir_ok = P.dir_ok; L.partials = P.partials;
-    rc = solve_level64(L, prm, diag, pd_off, warp_off, P.setup_scratch, P.setup_bytes, st);
+    rc = solve_level64(L, prm, diag, pd_off, warp_off, P.setup_scratch, P.setup_bytes, st,
+                       tm && tm->level == l ? tm : nullptr);
     if (rc) return rc;
     pd_off += (int64_t)N * K;
     warp_off += N;
@@ -663,6 +695,62 @@ int fsb_solve_pyramid_f64(const fsb_rig* rig, const fsb_params* prm, const doubl
                           const fsb_diag* diag, void* stream) {
   return solve_pyramid64(rig, prm, i0, i1, traj_dirs, traj_ok, workspace, workspace_bytes, u, w,
                          v, mask, i1c, diag, as_stream(stream));
+}
+
+int fsb_phase_timer_create(int32_t level, int32_t max_warps, fsb_phase_timer** out) {
+  if (!out || level < 0 || max_warps < 1) return FSB_EINVAL;
+  fsb_phase_timer* t = new fsb_phase_timer();
+  t->level = level; t->cap = max_warps; t->used = 0; t->pd_launches = 0;
+  t->ev = new cudaEvent_t[3 * (size_t)max_warps]();
+  for (int k = 0; k < 3 * max_warps; ++k) {
+    cudaError_t e = cudaEventCreate(&t->ev[k]);
+    if (e != cudaSuccess) {
+      for (int j = 0; j < k; ++j) cudaEventDestroy(t->ev[j]);
+      delete[] t->ev;
+      delete t;
+      return (int)e;
+    }
+  }
+  *out = t;
+  return FSB_OK;
+}
+
+int fsb_phase_timer_read(fsb_phase_timer* t, double* sample_ms, double* pd_ms, int32_t* warps,
+                         int32_t* pd_launches_per_warp, int32_t* level_h, int32_t* level_w) {
+  if (!t) return FSB_EINVAL;
+  double a = 0.0, b = 0.0;
+  for (int wi = 0; wi < t->used; ++wi) {
+    float x = 0.f, y = 0.f;
+    cudaError_t e = cudaEventElapsedTime(&x, t->ev[3 * wi], t->ev[3 * wi + 1]);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&y, t->ev[3 * wi + 1], t->ev[3 * wi + 2]);
+    if (e != cudaSuccess) return (int)e;
+    a += x; b += y;
+  }
+  if (sample_ms) *sample_ms = a;
+  if (pd_ms) *pd_ms = b;
+  if (warps) *warps = t->used;
+  if (pd_launches_per_warp) *pd_launches_per_warp = t->pd_launches;
+  if (level_h) *level_h = t->level_h;
+  if (level_w) *level_w = t->level_w;
+  return FSB_OK;
+}
+
+int fsb_phase_timer_destroy(fsb_phase_timer* t) {
+  if (!t) return FSB_OK;
+  for (int k = 0; k < 3 * t->cap; ++k) cudaEventDestroy(t->ev[k]);
+  delete[] t->ev;
+  delete t;
+  return FSB_OK;
+}
+
+int fsb_solve_pyramid_f64_timed(const fsb_rig* rig, const fsb_params* prm, const double* i0,
+                                const double* i1, void* workspace, size_t workspace_bytes,
+                                double* u, double* w, double* v, uint8_t* mask, double* i1c,
+                                fsb_phase_timer* timer, void* stream) {
+  if (!timer) return FSB_EINVAL;
+  timer->used = 0;
+  return solve_pyramid64(rig, prm, i0, i1, nullptr, nullptr, workspace, workspace_bytes, u, w,
+                         v, mask, i1c, nullptr, as_stream(stream), timer);
 }
 
 }  // extern "C"

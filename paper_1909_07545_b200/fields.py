@@ -34,17 +34,20 @@ def generate_calibration_field(rig):
     return _dev.download(field), _dev.download(ok, bool)
 
 
-def trajectory_field_device(cam, t, epsilon_scale: float = 0.1, depth: float = 1.0):
-    """Device tensors (dirs (H,W,2) f32, ok (H,W) u8) for the rig (cam, cam, (I, t))."""
+def trajectory_field_device(cam, t, epsilon_scale: float = 0.1, depth: float = 1.0,
+                            dtype=torch.float32):
+    """Device tensors (dirs (H,W,2) `dtype`, ok (H,W) u8) for the rig (cam, cam, (I, t)).
+    Computed in fp64 either way; float32 storage is the fp32 path's field."""
     L = _ext.lib()
     cs = _ext.camera_struct(cam)
     tt = (C.c_double * 3)(*[float(v) for v in np.asarray(t, dtype=np.float64).reshape(3)])
-    dirs = _dev.empty((cs.height, cs.width, 2))
+    dirs = _dev.empty((cs.height, cs.width, 2), dtype)
     ok = _dev.empty((cs.height, cs.width), torch.uint8)
     s = _dev.scratch(L.fsb_trajectory_scratch_bytes(C.byref(cs)))
-    _ext.check(L.fsb_trajectory_field(C.byref(cs), tt, float(epsilon_scale), float(depth),
-                                      _dev.ptr(dirs), _dev.ptr(ok), _dev.ptr(s), s.numel(),
-                                      _dev.stream_ptr()), "generate_trajectory_field")
+    fn = L.fsb_trajectory_field if dtype == torch.float32 else L.fsb_trajectory_field_f64
+    _ext.check(fn(C.byref(cs), tt, float(epsilon_scale), float(depth), _dev.ptr(dirs),
+                  _dev.ptr(ok), _dev.ptr(s), s.numel(), _dev.stream_ptr()),
+               "generate_trajectory_field")
     return dirs, ok
 
 
@@ -58,7 +61,8 @@ def generate_trajectory_field(rig, epsilon_scale: float = 0.1, depth: float = 1.
     if np.max(np.abs(R - np.eye(3))) > 1e-9:
         raise ValueError("trajectory field needs a rotation-free rig; "
                          "apply the calibration field first")
-    dirs, ok = trajectory_field_device(rig.cam0, rig.pose.translation, epsilon_scale, depth)
+    dirs, ok = trajectory_field_device(rig.cam0, rig.pose.translation, epsilon_scale, depth,
+                                       torch.float64)
     return _dev.download(dirs), _dev.download(ok, bool)
 
 

@@ -23,15 +23,17 @@ def default_setup():
     return rig, i0, i1, gt, cal, cal_ok
 
 
-@pytest.fixture(scope="module")
-def solve_grid(default_setup):
-    """tau>1 percentages over the acceptance grid (test_acceptance.py:42-57)."""
+@pytest.fixture(scope="module", params=["fp64", "fp32"])
+def solve_grid(default_setup, request):
+    """tau>1 percentages over the acceptance grid (test_acceptance.py:42-57), for
+    the default float64 path and the float32 path."""
     from paper_1909_07545_b200 import evaluate, fields
     from paper_1909_07545_b200.solver import SolverParams, solve_pyramid
     rig, i0, i1, gt, cal, cal_ok = default_setup
     out = {}
     for n, du in [(2, 0.2), (5, 0.2), (10, 0.2), (50, 0.2), (50, 0.1), (50, 1.0)]:
-        res = solve_pyramid(i0, i1, rig, SolverParams(warp_iters=n, du_max=du))
+        res = solve_pyramid(i0, i1, rig, SolverParams(warp_iters=n, du_max=du),
+                            precision=request.param)
         corr, corr_ok = fields.compose_with_calibration(res.w, cal, cal_ok)
         valid = gt.covisibility & corr_ok & res.mask
         out[(n, du)] = evaluate.make_report(corr, gt.correspondence, valid)

@@ -60,7 +60,7 @@ def test_fp64_variant_reproduces_oracle(reg):
     sol = O.pyramid_solve(g["i0"], g["i1"], rig, prm)
     assert np.max(np.abs(res.u - sol.u)[sol.mask]) <= 1e-8
     assert not res.v.any()
-    r32 = solve_pyramid(g["i0"], g["i1"], rig, prm)
+    r32 = solve_pyramid(g["i0"], g["i1"], rig, prm, precision="fp32")
     e = np.abs(r32.u - sol.u)[sol.mask]
     assert np.median(e) <= 1e-3 and np.percentile(e, 99) <= 1e-2
 

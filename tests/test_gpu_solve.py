@@ -60,11 +60,13 @@ def test_level_solve_parity():
     np.testing.assert_allclose(d.mean_abs_du, tr.mean_abs_du, atol=1e-4)
 
 
-def test_pyramid_solve_parity_small_rendered_pair():
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_pyramid_solve_parity_small_rendered_pair(precision):
     from paper_1909_07545_b200.solver import solve_pyramid
     g = load_golden("pyramid_solve")
     rig, prm = _rig(g), _params(g)
-    res = solve_pyramid(g["i0"], g["i1"], rig, prm, collect_diagnostics=True)
+    res = solve_pyramid(g["i0"], g["i1"], rig, prm, collect_diagnostics=True,
+                        precision=precision)
     sol = O.pyramid_solve(g["i0"], g["i1"], rig, prm, trace=True)
     np.testing.assert_array_equal(res.mask, sol.mask)
     np.testing.assert_allclose(res.i1_calibrated, sol.i1c, atol=2e-7)
@@ -93,17 +95,18 @@ def test_accumulation_identity():
     assert all(m <= prm.du_max * (1 + 1e-6) for m in d.max_du)
 
 
-def test_determinism_and_graph_replay():
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_determinism_and_graph_replay(precision):
     """Outputs are bit-identical run to run and through a CUDA graph (SPEC: deterministic)."""
     import torch
     from paper_1909_07545_b200.solver import Solver
     g = load_golden("pyramid_solve")
-    eng = Solver(_rig(g), _params(g))
+    eng = Solver(_rig(g), _params(g), precision=precision)
     r1 = eng.solve(g["i0"], g["i1"])  # first call captures the graph
     r2 = eng.solve(g["i0"], g["i1"])
     assert eng.kernels_per_frame and eng.kernels_per_frame > 0
-    eng.i0.copy_(torch.from_numpy(g["i0"].astype(np.float32)))
-    eng.i1.copy_(torch.from_numpy(g["i1"].astype(np.float32)))
+    eng.i0.copy_(torch.from_numpy(g["i0"]))  # cast to the engine dtype as solve() stages
+    eng.i1.copy_(torch.from_numpy(g["i1"]))
     eng.run()  # direct enqueue, no graph
     torch.cuda.synchronize()
     r3 = type(r1)(u=eng.u.cpu().numpy(), w=eng.w.cpu().numpy(), v=eng.v.cpu().numpy(),
@@ -127,18 +130,19 @@ def test_api_errors():
         solve_pyramid(g["i0"], g["i1"], zero, SolverParams(pyramid_levels=1))
 
 
-def test_traj_override_matches_generated():
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_traj_override_matches_generated(precision):
     """Override path (solver.py:437-438) fed with the generated field gives the same answer."""
     from paper_1909_07545_b200 import fields as F
     from paper_1909_07545_b200.solver import solve_pyramid
     g = load_golden("pyramid_solve")
     rig, prm = _rig(g), _params(g)
-    a = solve_pyramid(g["i0"], g["i1"], rig, prm)
+    a = solve_pyramid(g["i0"], g["i1"], rig, prm, precision=precision)
 
     def override(rig_lvl):
         return F.generate_trajectory_field(rig_lvl, prm.epsilon_scale)
 
-    b = solve_pyramid(g["i0"], g["i1"], rig, prm, traj_override=override)
+    b = solve_pyramid(g["i0"], g["i1"], rig, prm, traj_override=override, precision=precision)
     assert np.array_equal(a.u, b.u) and np.array_equal(a.w, b.w)
 
 
@@ -224,7 +228,7 @@ from conftest import load_golden
 import test_gpu_solve as T
 from paper_1909_07545_b200.solver import Solver
 g = load_golden("pyramid_solve")
-r = Solver(T._rig(g), T._params(g)).solve(g["i0"], g["i1"])
+r = Solver(T._rig(g), T._params(g), precision="fp32").solve(g["i0"], g["i1"])
 np.savez(sys.argv[2], u=r.u, w=r.w, v=r.v)
 """
 
@@ -239,7 +243,7 @@ def test_side_stream_overlap_is_bit_identical(tmp_path):
     from conftest import ROOT
     from paper_1909_07545_b200.solver import Solver
     g = load_golden("pyramid_solve")
-    r = Solver(_rig(g), _params(g)).solve(g["i0"], g["i1"])
+    r = Solver(_rig(g), _params(g), precision="fp32").solve(g["i0"], g["i1"])
     out = tmp_path / "serial.npz"
     env = dict(os.environ, FSB_OVERLAP="0")
     subprocess.run([sys.executable, "-c", _OVERLAP_CHILD, str(ROOT), str(out)], env=env,

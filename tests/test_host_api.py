@@ -41,18 +41,21 @@ def test_solver_params_strict_from_dict():
 
 def test_engine_cache_checkout_is_exclusive(monkeypatch):
     """solve_pyramid's engine cache (no GPU: the engine is stubbed): an engine
-    is never used by two threads at once, same-rig callers beyond the first get
-    their own engine, and the LRU keeps at most _CACHE_SIZE engines."""
+    is never used by two threads at once, concurrent same-rig callers get
+    their own engines and those engines are kept (a bounded idle list per
+    key) and reused, the cache keeps at most _CACHE_KEYS keys, and an engine
+    whose call raised is released instead of returned."""
     import threading
     import time
     from paper_1909_07545_b200 import solver as SV
     from paper_1909_07545_b200.camera import RelativePose, StereoRig, UnifiedCamera
 
-    made, clash = [], []
+    made, clash, released = [], [], []
 
     class FakeSolver:
-        def __init__(self, rig, params, diag=False, precision="fp32"):
+        def __init__(self, rig, params, diag=False, precision="fp64"):
             self.busy = threading.Lock()
+            self.fail = False
             made.append(self)
 
         def solve(self, i0, i1):
@@ -61,9 +64,14 @@ def test_engine_cache_checkout_is_exclusive(monkeypatch):
                 return None
             try:
                 time.sleep(0.002)
+                if i0 is BOOM:
+                    raise RuntimeError("CUDA error during replay")
                 return self
             finally:
                 self.busy.release()
+
+        def release(self):
+            released.append(self)
 
     monkeypatch.setattr(SV, "Solver", FakeSolver)
     monkeypatch.setattr(SV, "_CACHE", SV.OrderedDict())
@@ -73,10 +81,11 @@ def test_engine_cache_checkout_is_exclusive(monkeypatch):
         return StereoRig(cam, cam, RelativePose.from_displacement((0.1 + 0.01 * k, 0, 0)))
 
     img = np.zeros((6, 8))
+    BOOM = np.zeros((6, 8))
     prm = SV.SolverParams()
 
-    def work(t):
-        for k in range(20):
+    def work(t, n=20):
+        for k in range(n):
             SV.solve_pyramid(img, img, rig((t + k) % 6 if t % 2 else 0), prm)
 
     th = [threading.Thread(target=work, args=(t,)) for t in range(6)]
@@ -85,7 +94,24 @@ def test_engine_cache_checkout_is_exclusive(monkeypatch):
     for t in th:
         t.join()
     assert not clash
-    assert len(SV._CACHE) <= SV._CACHE_SIZE
+    assert len(SV._CACHE) <= SV._CACHE_KEYS
+    assert all(len(v) <= SV._CACHE_IDLE for v in SV._CACHE.values())
+    # concurrent callers of ONE rig: their engines are kept and reused, so the
+    # number of engines stays at the peak concurrency instead of growing per round
+    monkeypatch.setattr(SV, "_CACHE", SV.OrderedDict())
+    made.clear()
+    for _ in range(5):
+        th = [threading.Thread(target=work, args=(0, 3)) for _ in range(3)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+    assert len(made) <= 3, len(made)
     # serial reuse: the same rig twice in a row hits the cached engine
     a = SV.solve_pyramid(img, img, rig(0), prm)
     assert SV.solve_pyramid(img, img, rig(0), prm) is a
+    # a failed call releases its engine and does not put it back
+    with pytest.raises(RuntimeError):
+        SV.solve_pyramid(BOOM, img, rig(0), prm)
+    assert released and released[-1] is a
+    assert all(e is not a for v in SV._CACHE.values() for e in v)
