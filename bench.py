@@ -173,6 +173,11 @@ def product_params(name: str):
     return SolverParams.from_dict(params_dict(name))
 
 
+def workload(name: str):
+    """(rig, params, description, supersample) with the product's classes (tools/)."""
+    return product_rig(name), product_params(name), WORKLOADS[name]["desc"], WORKLOADS[name]["ss"]
+
+
 def load_c3_pair() -> tuple[np.ndarray, np.ndarray]:
     with np.load(C3_PAIR) as z:
         return z["i0"].astype(np.float32), z["i1"].astype(np.float32)

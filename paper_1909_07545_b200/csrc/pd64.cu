@@ -40,6 +40,22 @@ int level_setup64_internal(const double* i0, const uint8_t* mask, int h, int w,
                            size_t scratch_bytes, cudaStream_t st);
 int mean_finish_internal(const double* partials, int nparts, const uint8_t* mask, size_t n,
                          double* out, cudaStream_t st);
+struct P64 {  // sample64.cu
+  int h, w;
+  const double* i0;
+  const uint8_t* mask;
+  const double4* tex;
+  const double* wv;
+  double* i1wn;
+  double* dirs;
+  uint8_t* dir_ok;
+  double* iu;
+  double* rho0;
+};
+int pack64_internal(const double* i1, const uint8_t* mask, const double* traj,
+                    const uint8_t* tok, int h, int w, double4* tex, cudaStream_t st);
+int sample_nan64_internal(const P64& L, int bx, int by, cudaStream_t st);
+int linearize_nan64_internal(const P64& L, int bx, int by, cudaStream_t st);
 
 }  // namespace fsb
 
@@ -76,6 +92,10 @@ struct L64 {
   double *u2, *ub2, *v2, *vb2, *p2, *q2;
   // per-pixel flags: bit0 all 16 bicubic taps in mask, bit1 all in traj_ok (nullptr = off)
   uint8_t* full16;
+  // k64_pipe: per-pixel edge codes and the level's tile work list
+  uint32_t* ecode;
+  int* tiles;
+  double4* tex;  // NaN-encoded packed texels of the level (sample64.cu)
 };
 
 __device__ __forceinline__ bool ex_at(const uint8_t* __restrict__ m, int w, int x, size_t i) {
@@ -369,6 +389,9 @@ struct Plan64 {
   double *T, *S, *u[2], *wv[2], *ub, *v, *vb, *p, *q, *uo, *iu, *rho0, *i1w, *dirs, *partials;
   double *u2, *ub2, *v2, *vb2, *p2, *q2;
   uint8_t *i1w_ok, *dir_ok, *full16;
+  uint32_t* ecode;
+  int* tiles;
+  double4* tex;
   size_t bytes;
 };
 
@@ -414,6 +437,9 @@ int plan64(const fsb_rig* rig, const fsb_params* prm, void* base, Plan64& P) {
   P.v2 = c.take<double>(2 * n0); P.vb2 = c.take<double>(2 * n0);
   P.p2 = c.take<double>(2 * n0); P.q2 = c.take<double>(4 * n0);
   P.full16 = c.take<uint8_t>(n0);
+  P.ecode = c.take<uint32_t>(n0);
+  P.tex = c.take<double4>(n0);
+  P.tiles = c.take<int>(partial_count(H, W) + 1);
   P.bytes = c.off;
   return FSB_OK;
 }
@@ -430,6 +456,48 @@ fsb_camera scaled(const fsb_camera& c, int h, int w) {  // camera.py:66-77
 
 // FSB_PD64=plain runs the one-cycle-per-launch kernels (reference for the
 // blocked kernel in tests/tools); default: blocked, halo 2.
+// Blocked PD kernel choice. FSB_PD64K=block: the round-1 k64_block; =tile:
+// k64_tile everywhere; default (pipe): k64_pipe on levels that run halo 2 / 3
+// (the large ones), k64_tile on the small levels (halo 5).
+enum { K64_BLOCK = 0, K64_TILE = 1, K64_PIPE = 2, K64_TILEL = 3 };
+int pd64_kernel_choice() {
+  static const int v = [] {
+    const char* e = getenv("FSB_PD64K");
+    if (e && strcmp(e, "block") == 0) return (int)K64_BLOCK;
+    if (e && strcmp(e, "tile") == 0) return (int)K64_TILE;
+    if (e && strcmp(e, "pipe") == 0) return (int)K64_PIPE;
+    return (int)K64_TILEL;
+  }();
+  return v;
+}
+int pd64_kernel_for(int halo) {
+  const int k = pd64_kernel_choice();
+  return k == K64_PIPE && halo != 2 && halo != 3 ? K64_TILEL : k;
+}
+int pd64_prefetch() {
+  static const int v = [] {
+    const char* e = getenv("FSB_PD64_PF");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+int pd64_launch(const B64& A, int halo, cudaStream_t st) {
+  switch (pd64_kernel_for(halo)) {
+    case K64_PIPE: return pd64_pipe_launch(A, halo, st);
+    case K64_TILE: case K64_TILEL: return pd64_tile_launch(A, halo, st);
+    default: return pd64_block_launch(A, halo, st);
+  }
+}
+
+size_t pd64_tiles(int w, int h, int halo) {
+  switch (pd64_kernel_for(halo)) {
+    case K64_PIPE: return pd64_pipe_count(w, h, halo);
+    case K64_TILE: case K64_TILEL: return pd64_tile_count(w, h, halo);
+    default: return pd64_block_tiles(w, h, halo);
+  }
+}
+
 int pd64_halo() {
   static const int h = [] {
     const char* e = getenv("FSB_PD64");
@@ -450,10 +518,6 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
                   fsb_phase_timer* tm = nullptr) {
   L64 L = L0;  // L's state pointers follow the ping-pong of the blocked cycles
   const size_t n = L.n;
-  if (L.full16) {
-    dim3 b(kBX, kBY);
-    k64_full16<<<grid2d(L.w, L.h, b), b, 0, st>>>(L);
-  }
   int rc = level_setup64_internal(L.i0, L.mask, L.h, L.w, prm, L.T, L.S, scratch, scratch_bytes,
                                   st);
   if (rc) return rc;
@@ -474,18 +538,55 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
   dim3 blk(kBX, kBY), grd = grid2d(L.w, L.h, blk);
   const bool dpq = diag && diag->max_p_norm && diag->max_q_norm;
   const bool ddu = diag && diag->max_du && diag->mean_abs_du;
+  // latency-bound small levels: 5 cycles per launch when those tiles fit
+  // two resident CTAs per SM (C3: 64^2, 128^2), else R = 2 (throughput)
+  int halo = L.u2 ? pd64_halo() : 0;
+  if (halo == 2 && getenv("FSB_PD64") == nullptr) {
+    if (pd64_tile_count(L.w, L.h, 5) <= 2 * 148) halo = 5;
+    else if (pd64_tile_count(L.w, L.h, 3) <= 2 * 148) halo = 3;
+  }
+  const int kern = halo > 0 ? pd64_kernel_for(halo) : -1;
+  const bool listed = kern == K64_PIPE || kern == K64_TILEL;
+  if (listed) {  // per-level edge codes and tile work list
+    rc = pd64_edge_codes(L.mask, L.w, L.h, L.ecode, st);
+    if (rc) return rc;
+    rc = kern == K64_PIPE ? pd64_pipe_tile_list(L.mask, L.w, L.h, halo, L.tiles, st)
+                          : pd64_tile_tile_list(L.mask, L.w, L.h, halo, L.tiles, st);
+    if (rc) return rc;
+  }
+  // Warp prologue: the NaN-encoded texel kernels (sample64.cu) on levels up to
+  // 256^2, where the masked-gather chains of k64_sample / k64_linearize are
+  // latency floors (C3: 64^2 -0.18 ms, 128^2 -0.34 ms per frame); on larger
+  // levels the 32-byte texels cost more DRAM traffic than they save
+  // (1024^2 +0.8 ms). FSB_PRO64=old / new forces one kind everywhere.
+  static const int pro_mode = [] {
+    const char* e = getenv("FSB_PRO64");
+    return e && strcmp(e, "old") == 0 ? 0 : (e && strcmp(e, "new") == 0 ? 2 : 1);
+  }();
+  const bool pro_nan =
+      halo > 0 && (pro_mode == 2 || (pro_mode == 1 && (size_t)L.w * L.h <= 256 * 256));
+  P64 PL;
+  PL.h = L.h; PL.w = L.w; PL.i0 = L.i0; PL.mask = L.mask; PL.tex = L.tex; PL.wv = L.wv;
+  PL.i1wn = L.i1w; PL.dirs = L.dirs; PL.dir_ok = L.dir_ok; PL.iu = L.iu; PL.rho0 = L.rho0;
+  if (pro_nan) {
+    rc = pack64_internal(L.i1, L.mask, L.traj, L.traj_ok, L.h, L.w, L.tex, st);
+    if (rc) return rc;
+  } else if (L.full16) {  // all-16-taps-valid flags of the masked-gather sampler
+    dim3 b(kBX, kBY);
+    k64_full16<<<grid2d(L.w, L.h, b), b, 0, st>>>(L);
+  }
   for (int wi = 0; wi < N; ++wi) {
-    // latency-bound small levels: 5 cycles per launch when those tiles fit
-    // two resident CTAs per SM (C3: 64^2, 128^2), else R = 2 (throughput)
-    int halo = L.u2 ? pd64_halo() : 0;
-    if (halo == 2 && getenv("FSB_PD64") == nullptr) {
-      if (pd64_block_tiles(L.w, L.h, 5) <= 2 * 148) halo = 5;
-      else if (pd64_block_tiles(L.w, L.h, 3) <= 2 * 148) halo = 3;
-    }
     const bool timed = tm && wi < tm->cap;
     if (timed) cudaEventRecord(tm->ev[3 * wi], st);
-    k64_sample<<<grd, blk, 0, st>>>(L);
-    k64_linearize<<<grd, blk, 0, st>>>(L, halo == 0);
+    if (pro_nan) {
+      rc = sample_nan64_internal(PL, kBX, kBY, st);
+      if (rc) return rc;
+      rc = linearize_nan64_internal(PL, kBX, kBY, st);
+      if (rc) return rc;
+    } else {
+      k64_sample<<<grd, blk, 0, st>>>(L);
+      k64_linearize<<<grd, blk, 0, st>>>(L, halo == 0);
+    }
     if (timed) cudaEventRecord(tm->ev[3 * wi + 1], st);
     int pd_launches = 0;
     for (int k = 0; halo > 0 && k < K;) {  // blocked: `it` cycles per launch, src -> dst
@@ -506,13 +607,18 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
       A.dirs = L.dirs; A.wv = L.wv;
       A.diag_du = (A.fin && ddu) ? diag->max_du + warp_off + wi : nullptr;
       A.partials = L.partials;
-      rc = pd64_block_launch(A, halo, st);
+      A.ecode = listed ? L.ecode : nullptr;
+      A.tiles = listed ? L.tiles : nullptr;
+      A.prefetch = pd64_prefetch();
+      if (listed && A.diag_du)  // tiles off the work list keep a zero partial sum
+        cudaMemsetAsync(L.partials, 0, pd64_tiles(L.w, L.h, halo) * sizeof(double), st);
+      rc = pd64_launch(A, halo, st);
       if (rc) return rc;
       ++pd_launches;
       L = swapped(L);
       k += it;
       if (k == K && ddu) {
-        rc = mean_finish_internal(L.partials, (int)pd64_block_tiles(L.w, L.h, halo), L.mask, n,
+        rc = mean_finish_internal(L.partials, (int)pd64_tiles(L.w, L.h, halo), L.mask, n,
                                   diag->mean_abs_du + warp_off + wi, st);
         if (rc) return rc;
       }
@@ -620,6 +726,23 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
                                P.lvl_mask[l], ch, cw, st);
     if (rc) return rc;
   }
+  // FSB_L2PERSIST=1 (experiment): keep the per-level tensor / step planes
+  // (P.T, P.S: contiguous, 48 B/px) L2-persisting for the frame
+  static const bool l2p = [] {
+    const char* e = getenv("FSB_L2PERSIST");
+    return e && e[0] == '1';
+  }();
+  if (l2p) {
+    const size_t bytes = 6 * n0 * sizeof(double);
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes);
+    cudaStreamAttrValue av = {};
+    av.accessPolicyWindow.base_ptr = P.T;
+    av.accessPolicyWindow.num_bytes = bytes;
+    av.accessPolicyWindow.hitRatio = 1.0f;
+    av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &av);
+  }
   int64_t pd_off = 0, warp_off = 0;
   int cur = 0, prev_h = 0, prev_w = 0;
   const uint8_t* prev_mask = nullptr;
@@ -659,6 +782,7 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
     L.u = u; L.ub = P.ub; L.v = P.v; L.vb = P.vb; L.p = P.p; L.q = P.q;
     L.u2 = P.u2; L.ub2 = P.ub2; L.v2 = P.v2; L.vb2 = P.vb2; L.p2 = P.p2; L.q2 = P.q2;
     L.full16 = P.full16;
+    L.ecode = P.ecode; L.tiles = P.tiles; L.tex = P.tex;
     L.wv = wv; L.uo = P.uo; L.iu = P.iu; L.rho0 = P.rho0; L.i1w = P.i1w; L.i1w_ok = P.i1w_ok;
     L.dirs = P.dirs; L.dir_ok = P.dir_ok; L.partials = P.partials;
     rc = solve_level64(L, prm, diag, pd_off, warp_off, P.setup_scratch, P.setup_bytes, st,

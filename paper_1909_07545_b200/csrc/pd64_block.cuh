@@ -29,10 +29,25 @@ struct B64 {
   double du_max;
   const double* dirs; double* wv;
   float* diag_du; double* partials;  // max |du| and per-tile sums of |du| (nullptr = off)
+  // k64_pipe only: per-pixel edge codes (bit0 mask, bit1 x-edge, bit2 y-edge) and
+  // the level's work list (tiles[0] = count, tiles[1 + k] = tile id; nullptr = all)
+  const uint32_t* ecode;
+  const int* tiles;
+  int prefetch;  // k64_tile with a work list: L2-prefetch the tile this many list entries ahead (0 = off)
 };
 
 // `iters` (<= halo, halo in 1..3 or 5) cycles from the src set into the dst set.
 int pd64_block_launch(const B64& A, int halo, cudaStream_t st);
 size_t pd64_block_tiles(int w, int h, int halo);
+// The issue-lean tile kernel (pd64_tile.cu): same arguments and semantics.
+int pd64_tile_launch(const B64& A, int halo, cudaStream_t st);
+size_t pd64_tile_count(int w, int h, int halo);
+int pd64_tile_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles, cudaStream_t st);
+// The persistent, cp.async-pipelined kernel (pd64_pipe.cu), halo 2 or 3.
+int pd64_pipe_launch(const B64& A, int halo, cudaStream_t st);
+size_t pd64_pipe_count(int w, int h, int halo);
+int pd64_pipe_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles,
+                        cudaStream_t st);
+int pd64_edge_codes(const uint8_t* mask, int w, int h, uint32_t* code, cudaStream_t st);
 
 }  // namespace fsb

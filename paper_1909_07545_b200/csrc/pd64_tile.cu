@@ -1,0 +1,395 @@
+// Temporally blocked float64 primal-dual tiles, issue-lean (the float64 path's
+// hot kernel).
+//
+// Same cycle as k64_block (pd64_block.cu) and the reference's
+// primal_dual_iterate (solver.py:279-303: dual ascent with forward
+// differences + unit-ball projection, backward divergence, data-term
+// shrinkage, over-relaxation) on a 32-wide tile with an R-pixel halo, `iters`
+// <= R cycles per launch, state in registers. What changes is how little the
+// SM issues per pixel-cycle:
+//   * x-neighbours come from warp shuffles (a tile row is a warp), so only the
+//     y-neighbours go through shared memory: 3 doubles published per thread
+//     row for the dual (u_bar, v_bar of its first pixel row) and 3 for the
+//     primal (the y-fluxes of its last pixel row), 2 barriers per cycle;
+//   * PY pixels per thread stacked vertically: the y-neighbours inside a
+//     thread stay in registers (PY = 2 halves the shared traffic and gives two
+//     independent dependency chains per thread);
+//   * the nine per-pixel constants stay in shared memory (registers hold the
+//     12 state doubles per pixel);
+//   * edge indicators and the skip of masked pixels are predicates decided
+//     once per launch; tiles whose interior holds no solve-mask pixel return
+//     right after the mask test (their state is exactly zero, see
+//     pd64_block.cu);
+//   * compiled with FMA contraction (this translation unit is not -fmad=false):
+//     the float64 arithmetic keeps ~53-bit rounding, far below the parity gate
+//     (tests/test_gpu_c3_parity.py holds it against the reference at C3).
+//
+// Reference: solver.py:279-303, 347-360 (warp-start resets and clip/accumulate
+// epilogue, fused as in k64_block), rasters.py:144-182.
+
+#include "pd64_block.cuh"
+#include "pd_math.cuh"
+
+#include <stddef.h>
+#include <stdlib.h>
+#include <string.h>
+
+namespace fsb {
+
+namespace {
+
+constexpr int kW = 32;   // tile width = warp width
+
+template <int kTR, int PY>
+struct SmemT {
+  static constexpr int TH = kTR * PY;
+  double ub[kTR][kW], vb0[kTR][kW], vb1[kTR][kW];  // first pixel row of each thread row
+  double fy[3][kTR][kW];                            // y-fluxes of the last pixel row
+  double c[9][TH][kW];                              // a b c sp tu tv g rho0 u_omega
+};
+
+FSB_INLINE double shfl_dn(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+FSB_INLINE double shfl_up(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+
+// Base pointer of staging plane l (0..20) of the source set and constants.
+FSB_INLINE const double* plane_ptr(const B64& A, int l) {
+  const size_t n = A.n;
+  switch (l) {
+    case 0: return A.su;
+    case 1: return A.sv;
+    case 2: return A.sv + n;
+    case 3: return A.sp;
+    case 4: return A.sp + n;
+    case 5: case 6: case 7: case 8: return A.sq + (l - 5) * n;
+    case 9: case 10: case 11: return A.T + (l - 9) * n;
+    case 12: case 13: case 14: return A.S + (l - 12) * n;
+    case 15: return A.iu;
+    case 16: return A.rho0;
+    case 17: return A.sub;
+    case 18: return A.svb;
+    case 19: return A.svb + n;
+    default: return A.uo;
+  }
+}
+
+template <int R, int PY, int kTR, bool DIAG>
+__global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(const B64 A) {
+  constexpr int TH = kTR * PY;
+  constexpr int OW = kW - 2 * R, OH = TH - 2 * R;
+  extern __shared__ double s_raw[];
+  SmemT<kTR, PY>& S = *reinterpret_cast<SmemT<kTR, PY>*>(s_raw);
+  const int lane = threadIdx.x, ty = threadIdx.y;
+  const size_t n = A.n;
+  const int W = A.w, H = A.h;
+  const int ntx = (W + OW - 1) / OW;
+  int bx = blockIdx.x, by = blockIdx.y;
+  if (A.tiles) {  // 1-D grid over the level's work list of tiles holding mask pixels
+    const int cnt = A.tiles[0];
+    if ((int)blockIdx.x >= cnt) return;
+    const int t = A.tiles[1 + blockIdx.x];
+    bx = t % ntx;
+    by = t / ntx;
+    // L2 prefetch of the tile one resident wave ahead (its CTA starts about one
+    // CTA lifetime from now): lane l < 21 fetches staging plane l of its row
+    const int k2 = (int)blockIdx.x + A.prefetch;
+    if (A.prefetch > 0 && k2 < cnt && lane < 21 + 1 && !(A.first && lane >= 17 && lane < 21)) {
+      const int t2 = A.tiles[1 + k2];
+      const int px0 = max((t2 % ntx) * OW - R, 0), py = (t2 / ntx) * OH - R + ty * PY;
+      const int px1 = min(px0 + kW, W) - 1;
+#pragma unroll
+      for (int j = 0; j < PY; ++j) {
+        if ((unsigned)(py + j) < (unsigned)H) {
+          const size_t r = (size_t)(py + j) * W;
+          const char* b0 = lane < 21 ? reinterpret_cast<const char*>(plane_ptr(A, lane) + r)
+                                     : reinterpret_cast<const char*>(A.ecode + r);
+          const size_t es = lane < 21 ? 8 : 4;
+          for (size_t o = (size_t)px0 * es & ~size_t(127); o <= (size_t)px1 * es; o += 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(b0 + o));
+        }
+      }
+    }
+  }
+  const int gx = bx * OW - R + lane;
+  const int gy0 = by * OH - R + ty * PY;
+  const int tile_id = by * ntx + bx;
+
+  double u[PY], ub[PY], v0[PY], v1[PY], vb0[PY], vb1[PY], p0[PY], p1[PY];
+  double q0[PY], q1[PY], q2[PY], q3[PY];
+  bool m[PY], ex[PY], ey[PY], inner[PY];
+  size_t idx[PY];
+  const double alpha1 = A.alpha1;
+  if (A.ecode) {
+    // Speculative loads: the work list guarantees mask pixels in the interior,
+    // and masked pixels hold exactly zero state (and I_u = 0), so every
+    // in-image pixel loads unconditionally — one memory round trip, no
+    // dependency on the mask.
+#pragma unroll
+    for (int j = 0; j < PY; ++j) {
+      const int gy = gy0 + j;
+      const bool in = (unsigned)gx < (unsigned)W && (unsigned)gy < (unsigned)H;
+      const size_t i = in ? (size_t)gy * W + gx : 0;
+      idx[j] = i;
+      const int ry = ty * PY + j;
+      inner[j] = lane >= R && lane < kW - R && ry >= R && ry < TH - R && in;
+      double cc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      uint32_t code = 0;
+      u[j] = ub[j] = v0[j] = v1[j] = vb0[j] = vb1[j] = p0[j] = p1[j] = 0.0;
+      q0[j] = q1[j] = q2[j] = q3[j] = 0.0;
+      if (in) {
+        code = A.ecode[i];
+        u[j] = A.su[i];
+        v0[j] = A.sv[i]; v1[j] = A.sv[n + i];
+        p0[j] = A.sp[i]; p1[j] = A.sp[n + i];
+        q0[j] = A.sq[i]; q1[j] = A.sq[n + i]; q2[j] = A.sq[2 * n + i]; q3[j] = A.sq[3 * n + i];
+        cc[0] = A.T[i]; cc[1] = A.T[n + i]; cc[2] = A.T[2 * n + i];
+        cc[3] = A.S[i] * alpha1; cc[4] = A.S[n + i]; cc[5] = A.S[2 * n + i];
+        cc[6] = A.iu[i]; cc[7] = A.rho0[i];
+        if (A.first) {
+          ub[j] = u[j]; vb0[j] = v0[j]; vb1[j] = v1[j]; cc[8] = u[j];
+        } else {
+          ub[j] = A.sub[i]; vb0[j] = A.svb[i]; vb1[j] = A.svb[n + i]; cc[8] = A.uo[i];
+        }
+      }
+      m[j] = code & 1u;
+      ex[j] = code & 2u;
+      ey[j] = code & 4u;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) S.c[k][ry][lane] = cc[k];
+    }
+  } else {
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < PY; ++j) {
+      const int gy = gy0 + j;
+      const bool in = (unsigned)gx < (unsigned)W && (unsigned)gy < (unsigned)H;
+      const size_t i = in ? (size_t)gy * W + gx : 0;
+      idx[j] = i;
+      m[j] = in && A.mask[i];
+      ex[j] = m[j] && gx + 1 < W && A.mask[i + 1];
+      ey[j] = m[j] && gy + 1 < H && A.mask[i + W];
+      const int ry = ty * PY + j;
+      inner[j] = lane >= R && lane < kW - R && ry >= R && ry < TH - R && in;
+      any = any || (inner[j] && m[j]);
+    }
+    // no solve-mask pixel in the interior: nothing to update or store
+    if (!__syncthreads_or(any)) {
+      if (A.fin && DIAG && A.diag_du && lane == 0 && ty == 0) A.partials[tile_id] = 0.0;
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < PY; ++j) {
+      double cc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      u[j] = ub[j] = v0[j] = v1[j] = vb0[j] = vb1[j] = p0[j] = p1[j] = 0.0;
+      q0[j] = q1[j] = q2[j] = q3[j] = 0.0;
+      if (m[j]) {
+        const size_t i = idx[j];
+        u[j] = A.su[i];
+        v0[j] = A.sv[i]; v1[j] = A.sv[n + i];
+        p0[j] = A.sp[i]; p1[j] = A.sp[n + i];
+        q0[j] = A.sq[i]; q1[j] = A.sq[n + i]; q2[j] = A.sq[2 * n + i]; q3[j] = A.sq[3 * n + i];
+        cc[0] = A.T[i]; cc[1] = A.T[n + i]; cc[2] = A.T[2 * n + i];
+        cc[3] = A.S[i] * alpha1; cc[4] = A.S[n + i]; cc[5] = A.S[2 * n + i];
+        cc[6] = A.iu[i]; cc[7] = A.rho0[i];
+        if (A.first) {  // warp-start reset (solver.py:344-346): u0 = u, u_bar = u, v_bar = v
+          ub[j] = u[j]; vb0[j] = v0[j]; vb1[j] = v1[j]; cc[8] = u[j];
+        } else {
+          ub[j] = A.sub[i]; vb0[j] = A.svb[i]; vb1[j] = A.svb[n + i]; cc[8] = A.uo[i];
+        }
+      }
+      const int ry = ty * PY + j;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) S.c[k][ry][lane] = cc[k];
+    }
+  }
+  const double sq = A.sigma_q * A.alpha0, heps = A.heps;
+  const double lam = A.lam, alpha0 = A.alpha0, theta = A.theta;
+  const int tyd = ty + 1 < kTR ? ty + 1 : ty;
+  for (int it = 0; it < A.iters; ++it) {
+    S.ub[ty][lane] = ub[0];
+    S.vb0[ty][lane] = vb0[0];
+    S.vb1[ty][lane] = vb1[0];
+    __syncthreads();
+    double fx0[PY], fx1[PY], fx2[PY], fy0[PY], fy1[PY], fy2[PY];
+    double pmax = 0.0, qmax = 0.0;
+#pragma unroll
+    for (int j = 0; j < PY; ++j) {
+      const int ry = ty * PY + j;
+      const double a = S.c[0][ry][lane], b = S.c[1][ry][lane], c = S.c[2][ry][lane];
+      const double sp = S.c[3][ry][lane];
+      // forward differences (rasters.py:144-155), zero where the edge leaves the mask
+      const double ubx = shfl_dn(ub[j]), vbx0 = shfl_dn(vb0[j]), vbx1 = shfl_dn(vb1[j]);
+      double uby, vby0, vby1;
+      if (j + 1 < PY) {
+        uby = ub[j + 1]; vby0 = vb0[j + 1]; vby1 = vb1[j + 1];
+      } else {
+        uby = S.ub[tyd][lane]; vby0 = S.vb0[tyd][lane]; vby1 = S.vb1[tyd][lane];
+      }
+      const double gxx = ex[j] ? ubx - ub[j] : 0.0, gyy = ey[j] ? uby - ub[j] : 0.0;
+      const double g00 = ex[j] ? vbx0 - vb0[j] : 0.0, g01 = ey[j] ? vby0 - vb0[j] : 0.0;
+      const double g10 = ex[j] ? vbx1 - vb1[j] : 0.0, g11 = ey[j] ? vby1 - vb1[j] : 0.0;
+      dual_update_exact<double>(a, b, c, sp, sq, gxx, gyy, g00, g01, g10, g11, vb0[j], vb1[j],
+                                p0[j], p1[j], q0[j], q1[j], q2[j], q3[j], heps);
+      fx0[j] = ex[j] ? a * p0[j] + b * p1[j] : 0.0;
+      fy0[j] = ey[j] ? b * p0[j] + c * p1[j] : 0.0;
+      fx1[j] = ex[j] ? q0[j] : 0.0;
+      fy1[j] = ey[j] ? q1[j] : 0.0;
+      fx2[j] = ex[j] ? q2[j] : 0.0;
+      fy2[j] = ey[j] ? q3[j] : 0.0;
+      if (DIAG && inner[j]) {
+        pmax = fmax(pmax, sqrt(p0[j] * p0[j] + p1[j] * p1[j]));
+        qmax = fmax(qmax, sqrt(((q0[j] * q0[j] + q1[j] * q1[j]) + q2[j] * q2[j]) + q3[j] * q3[j]));
+      }
+    }
+    S.fy[0][ty][lane] = fy0[PY - 1];
+    S.fy[1][ty][lane] = fy1[PY - 1];
+    S.fy[2][ty][lane] = fy2[PY - 1];
+    if (DIAG) {
+      pmax = warp_max(pmax);
+      qmax = warp_max(qmax);
+      if (lane == 0 && A.diag_p) {
+        atomic_max_nonneg(A.diag_p + it, (float)pmax);
+        atomic_max_nonneg(A.diag_q + it, (float)qmax);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < PY; ++j) {
+      const int ry = ty * PY + j;
+      // backward divergence (rasters.py:158-172); the column left of / row above
+      // the tile feed only halo pixels
+      const double lx0 = shfl_up(fx0[j]), lx1 = shfl_up(fx1[j]), lx2 = shfl_up(fx2[j]);
+      double uy0, uy1, uy2;
+      if (j > 0) {
+        uy0 = fy0[j - 1]; uy1 = fy1[j - 1]; uy2 = fy2[j - 1];
+      } else if (ty > 0) {
+        uy0 = S.fy[0][ty - 1][lane]; uy1 = S.fy[1][ty - 1][lane]; uy2 = S.fy[2][ty - 1][lane];
+      } else {
+        uy0 = uy1 = uy2 = 0.0;
+      }
+      const double dvv = ((fx0[j] - lx0) + fy0[j]) - uy0;
+      const double d0 = ((fx1[j] - lx1) + fy1[j]) - uy1;
+      const double d1 = ((fx2[j] - lx2) + fy2[j]) - uy2;
+      const double tu = S.c[4][ry][lane], tv = S.c[5][ry][lane], g = S.c[6][ry][lane];
+      const double rh = S.c[7][ry][lane], uo = S.c[8][ry][lane];
+      primal_update_exact<double>(dvv, d0, d1, tu, tv, g, rh, uo, p0[j], p1[j], lam, alpha0,
+                                  alpha1, theta, u[j], v0[j], v1[j], ub[j], vb0[j], vb1[j]);
+    }
+  }
+  double adu = 0.0, amax = 0.0;
+#pragma unroll
+  for (int j = 0; j < PY; ++j) {
+    const int ry = ty * PY + j;
+    const size_t i = idx[j];
+    const bool st = inner[j] && m[j];
+    const double uo = S.c[8][ry][lane];
+    if (A.fin && st) {  // clip / accumulate (solver.py:356-360) on the interior
+      const double du = fmin(fmax(u[j] - uo, -A.du_max), A.du_max);
+      u[j] = uo + du;
+      amax = fmax(amax, fabs(du));
+      const double2 dd = reinterpret_cast<const double2*>(A.dirs)[i];
+      double2 wv = reinterpret_cast<double2*>(A.wv)[i];
+      wv.x = wv.x + du * dd.x;
+      wv.y = wv.y + du * dd.y;
+      reinterpret_cast<double2*>(A.wv)[i] = wv;
+      adu += fabs(du);
+    }
+    if (!st) continue;
+    if (A.first) A.uo[i] = uo;
+    A.du[i] = u[j];
+    A.dv[i] = v0[j]; A.dv[n + i] = v1[j];
+    A.dp[i] = p0[j]; A.dp[n + i] = p1[j];
+    A.dq[i] = q0[j]; A.dq[n + i] = q1[j]; A.dq[2 * n + i] = q2[j]; A.dq[3 * n + i] = q3[j];
+    if (!A.fin) {  // u_bar / v_bar are reset at the next warp's start: dead after its last cycle
+      A.dub[i] = ub[j];
+      A.dvb[i] = vb0[j]; A.dvb[n + i] = vb1[j];
+    }
+  }
+  if (DIAG && A.fin && A.diag_du) {
+    __shared__ double s_sum[kTR], s_max[kTR];
+    const double mx = warp_max(amax), sm = warp_sum(adu);
+    if (lane == 0) { s_sum[ty] = sm; s_max[ty] = mx; }
+    __syncthreads();
+    if (lane == 0 && ty == 0) {
+      double t = 0.0, mm = 0.0;
+      for (int k = 0; k < kTR; ++k) { t += s_sum[k]; mm = fmax(mm, s_max[k]); }
+      A.partials[tile_id] = t;
+      atomic_max_nonneg(A.diag_du, (float)mm);
+    }
+  }
+}
+
+template <int R, int PY, int kTR, bool DIAG>
+int launch_tile(const B64& A, cudaStream_t st) {
+  constexpr int TH = kTR * PY;
+  constexpr int OW = kW - 2 * R, OH = TH - 2 * R;
+  const int ntx = (A.w + OW - 1) / OW, nty = (A.h + OH - 1) / OH;
+  // with a work list: a 1-D grid of every tile (CTAs past the list's count exit)
+  const dim3 blk(kW, kTR), grd = A.tiles ? dim3(ntx * nty) : dim3(ntx, nty);
+  const size_t dyn = sizeof(SmemT<kTR, PY>);
+  static std::atomic<unsigned long long> attr{0};
+  once_per_device(attr, [&] {
+    cudaFuncSetAttribute(k64_tile<R, PY, kTR, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)dyn);
+  });
+  k64_tile<R, PY, kTR, DIAG><<<grd, blk, dyn, st>>>(A);
+  return launch_status();
+}
+
+int tile_py() {
+  static const int v = [] {
+    const char* e = getenv("FSB_PD64_PY");
+    return e && e[0] == '2' ? 2 : 1;
+  }();
+  return v;
+}
+
+// thread rows per CTA: 16 for one pixel per thread; FSB_PD64_PY=2 stacks two
+// pixels per thread on 8 thread rows (same 32 x 16 tile, 2 CTAs / SM) or, with
+// FSB_PD64_PY=2t, on 16 thread rows (32 x 32 tile, 1 CTA / SM)
+int tile_rows() {
+  static const int v = [] {
+    const char* e = getenv("FSB_PD64_PY");
+    return e && e[0] == '2' && e[1] != 't' ? 8 : 16;
+  }();
+  return v;
+}
+
+template <int R>
+int launch_r(const B64& A, cudaStream_t st) {
+  const bool diag = A.diag_p || A.diag_du;
+  if (tile_py() == 2 && tile_rows() == 8)
+    return diag ? launch_tile<R, 2, 8, true>(A, st) : launch_tile<R, 2, 8, false>(A, st);
+  if (tile_py() == 2)
+    return diag ? launch_tile<R, 2, 16, true>(A, st) : launch_tile<R, 2, 16, false>(A, st);
+  return diag ? launch_tile<R, 1, 16, true>(A, st) : launch_tile<R, 1, 16, false>(A, st);
+}
+
+}  // namespace
+
+size_t pd64_tile_count(int w, int h, int halo) {
+  const int TH = tile_rows() * tile_py();
+  const int OW = kW - 2 * halo, OH = TH - 2 * halo;
+  return (size_t)((w + OW - 1) / OW) * ((h + OH - 1) / OH);
+}
+
+int tile_list_internal(const uint8_t* mask, int w, int h, int TW, int TH, int* tiles,
+                       cudaStream_t st);
+
+int pd64_tile_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles,
+                        cudaStream_t st) {
+  return tile_list_internal(mask, w, h, kW - 2 * halo, tile_rows() * tile_py() - 2 * halo, tiles,
+                            st);
+}
+
+int pd64_tile_launch(const B64& A, int halo, cudaStream_t st) {
+  if (A.iters < 1 || A.iters > halo) return FSB_EINVAL;
+  switch (halo) {
+    case 1: return launch_r<1>(A, st);
+    case 2: return launch_r<2>(A, st);
+    case 3: return launch_r<3>(A, st);
+    case 5: return launch_r<5>(A, st);
+    default: return FSB_EINVAL;
+  }
+}
+
+}  // namespace fsb

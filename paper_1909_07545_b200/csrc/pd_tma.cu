@@ -531,12 +531,17 @@ __global__ void k_tile_compact(int* tiles, int ntiles) {
 
 }  // namespace
 
-int pd_tma_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles, cudaStream_t st) {
-  const int TW = kEW - 2 * halo, TH = kEH - 2 * halo;
+// Generic form: tiles of TW x TH interior pixels on a row-major tile grid.
+int tile_list_internal(const uint8_t* mask, int w, int h, int TW, int TH, int* tiles,
+                       cudaStream_t st) {
   const int ntx = (w + TW - 1) / TW, nty = (h + TH - 1) / TH;
   k_tile_flags<<<ntx * nty, 256, 0, st>>>(mask, w, h, TW, TH, ntx, tiles);
   k_tile_compact<<<1, 1024, 0, st>>>(tiles, ntx * nty);
   return launch_status();
+}
+
+int pd_tma_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles, cudaStream_t st) {
+  return tile_list_internal(mask, w, h, kEW - 2 * halo, kEH - 2 * halo, tiles, st);
 }
 
 bool pd_tma_maps(TmaMaps* maps, const float* state_a, const float* state_b, const float* consts,

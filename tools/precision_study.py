@@ -20,12 +20,28 @@ f32 = lambda a: np.asarray(a, np.float32).astype(np.float64)  # noqa: E731
 
 def run(i0, i1, rig, prm, mode):
     orig_cycle, orig_lin, orig_level = O.pd_cycle, O.linearize, O.level_solve
+    orig_T, orig_st = O.edge_tensor, O.step_sizes
 
     def cycle(s, *a, **k):
         s = orig_cycle(s, *a, **k)
         if "state" in mode:
             s = O.PDState(*(f32(getattr(s, f)) for f in ("u", "v", "p", "q", "u_bar", "v_bar")))
+        if "pq" in mode:  # only the duals stored as float32
+            s = O.PDState(u=s.u, v=s.v, p=f32(s.p), q=f32(s.q), u_bar=s.u_bar, v_bar=s.v_bar)
+        if "vv" in mode:  # only the second-order primal v, v_bar as float32
+            s = O.PDState(u=s.u, v=f32(s.v), p=s.p, q=s.q, u_bar=s.u_bar, v_bar=f32(s.v_bar))
         return s
+
+    def tensor(*a, **k):
+        T = orig_T(*a, **k)
+        return f32(T) if "consts" in mode else T
+
+    def steps(*a, **k):
+        st = orig_st(*a, **k)
+        if "consts" in mode:
+            st = O.Steps(sigma_p=f32(st.sigma_p), sigma_q=st.sigma_q, tau_u=f32(st.tau_u),
+                         tau_v=f32(st.tau_v))
+        return st
 
     def lin(i0_, i1_, traj, tok, mask, w):
         if "w" in mode:
@@ -37,10 +53,12 @@ def run(i0, i1, rig, prm, mode):
         return out
 
     O.pd_cycle, O.linearize = cycle, lin
+    O.edge_tensor, O.step_sizes = tensor, steps
     try:
         return O.pyramid_solve(i0, i1, rig, prm)
     finally:
         O.pd_cycle, O.linearize = orig_cycle, orig_lin
+        O.edge_tensor, O.step_sizes = orig_T, orig_st
 
 
 def main():
