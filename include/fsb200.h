@@ -93,6 +93,8 @@ typedef struct fsb_diag {
   float* max_q_norm;    /* one per primal-dual iteration, all levels  */
   float* max_du;        /* one per warp iteration, all levels         */
   double* mean_abs_du;  /* one per warp iteration, all levels         */
+  double* max_du_f64;   /* float64 path: max |du| per warp in float64 (the reference's
+                           du_max + 1e-15 bound, test_acceptance.py:249-258); NULL = max_du */
 } fsb_diag;
 
 /* ---------------------------------------------------------------- geometry */

@@ -63,7 +63,8 @@ class FsbParams(C.Structure):
 
 class FsbDiag(C.Structure):
     _fields_ = [("max_p_norm", C.c_void_p), ("max_q_norm", C.c_void_p),
-                ("max_du", C.c_void_p), ("mean_abs_du", C.c_void_p)]
+                ("max_du", C.c_void_p), ("mean_abs_du", C.c_void_p),
+                ("max_du_f64", C.c_void_p)]
 
 
 class FsbLevel(C.Structure):

@@ -322,7 +322,7 @@ __global__ void k64_primal(L64 L, double lam, double alpha0, double alpha1, doub
 
 // solver.py:356-365
 template <bool kDiag>
-__global__ void k64_finish(L64 L, double du_max, float* dmax) {
+__global__ void k64_finish(L64 L, double du_max, float* dmax, double* dmax64) {
   int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
   double adu = 0.0;
   if (x < L.w && y < L.h) {
@@ -349,7 +349,8 @@ __global__ void k64_finish(L64 L, double du_max, float* dmax) {
       const int nw = (blockDim.x * blockDim.y) >> 5;
       for (int k = 0; k < nw; ++k) { t += ssum[k]; m = fmax(m, smax[k]); }
       L.partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
-      atomic_max_nonneg(dmax, (float)m);
+      if (dmax64) atomic_max_nonneg(dmax64, m);
+      else atomic_max_nonneg(dmax, (float)m);
     }
   }
 }
@@ -537,7 +538,7 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
   const int N = prm->warp_iters, K = prm->pd_iters;
   dim3 blk(kBX, kBY), grd = grid2d(L.w, L.h, blk);
   const bool dpq = diag && diag->max_p_norm && diag->max_q_norm;
-  const bool ddu = diag && diag->max_du && diag->mean_abs_du;
+  const bool ddu = diag && (diag->max_du || diag->max_du_f64) && diag->mean_abs_du;
   // latency-bound small levels: 5 cycles per launch when those tiles fit
   // two resident CTAs per SM (C3: 64^2, 128^2), else R = 2 (throughput)
   int halo = L.u2 ? pd64_halo() : 0;
@@ -605,12 +606,14 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
       A.fin = k + it == K;  // the warp's last cycles: fused clip / accumulate
       A.du_max = prm->du_max;
       A.dirs = L.dirs; A.wv = L.wv;
-      A.diag_du = (A.fin && ddu) ? diag->max_du + warp_off + wi : nullptr;
+      A.diag_du = (A.fin && ddu && diag->max_du) ? diag->max_du + warp_off + wi : nullptr;
+      A.diag_du64 = (A.fin && ddu && diag->max_du_f64) ? diag->max_du_f64 + warp_off + wi : nullptr;
+      if (A.diag_du64) A.diag_du = nullptr;
       A.partials = L.partials;
       A.ecode = listed ? L.ecode : nullptr;
       A.tiles = listed ? L.tiles : nullptr;
       A.prefetch = pd64_prefetch();
-      if (listed && A.diag_du)  // tiles off the work list keep a zero partial sum
+      if (listed && (A.diag_du || A.diag_du64))  // tiles off the work list keep a zero partial sum
         cudaMemsetAsync(L.partials, 0, pd64_tiles(L.w, L.h, halo) * sizeof(double), st);
       rc = pd64_launch(A, halo, st);
       if (rc) return rc;
@@ -645,12 +648,14 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
       k64_primal<<<grd, blk, 0, st>>>(L, prm->lam, prm->alpha0, prm->alpha1, prm->theta);
     }
     if (ddu) {
-      k64_finish<true><<<grd, blk, 0, st>>>(L, prm->du_max, diag->max_du + warp_off + wi);
+      k64_finish<true><<<grd, blk, 0, st>>>(
+          L, prm->du_max, diag->max_du ? diag->max_du + warp_off + wi : nullptr,
+          diag->max_du_f64 ? diag->max_du_f64 + warp_off + wi : nullptr);
       rc = mean_finish_internal(L.partials, (int)(grd.x * grd.y), L.mask, n,
                                 diag->mean_abs_du + warp_off + wi, st);
       if (rc) return rc;
     } else {
-      k64_finish<false><<<grd, blk, 0, st>>>(L, prm->du_max, nullptr);
+      k64_finish<false><<<grd, blk, 0, st>>>(L, prm->du_max, nullptr, nullptr);
     }
   }
   if (L.u != L0.u) {  // the level result back into the primary set (u carries on, v is output)
@@ -705,6 +710,7 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
     if (diag->max_p_norm) cudaMemsetAsync(diag->max_p_norm, 0, npd * sizeof(float), st);
     if (diag->max_q_norm) cudaMemsetAsync(diag->max_q_norm, 0, npd * sizeof(float), st);
     if (diag->max_du) cudaMemsetAsync(diag->max_du, 0, nw * sizeof(float), st);
+    if (diag->max_du_f64) cudaMemsetAsync(diag->max_du_f64, 0, nw * sizeof(double), st);
   }
   rc = fov_mask_internal(&r.cam0, P.mask0, P.iters + 0, st);
   if (rc) return rc;

@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kTX * TY, MINB) k64_block(const B64 A) {
       A.wv[2 * i + 1] = A.wv[2 * i + 1] + du * A.dirs[2 * i + 1];
       adu = fabs(du);
     }
-    if (DIAG && A.diag_du) {
+    if (DIAG && (A.diag_du || A.diag_du64)) {
       __shared__ double s_sum[TY], s_max[TY];
       const double mx = warp_max(adu), sm = warp_sum(adu);
       if (tx == 0) { s_sum[ty] = sm; s_max[ty] = mx; }
@@ -162,7 +162,8 @@ __global__ void __launch_bounds__(kTX * TY, MINB) k64_block(const B64 A) {
         double t = 0.0, mm = 0.0;
         for (int k = 0; k < TY; ++k) { t += s_sum[k]; mm = fmax(mm, s_max[k]); }
         A.partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
-        atomic_max_nonneg(A.diag_du, (float)mm);
+        if (A.diag_du64) atomic_max_nonneg(A.diag_du64, mm);
+        else atomic_max_nonneg(A.diag_du, (float)mm);
       }
     }
   }
@@ -202,7 +203,7 @@ bool pd64_const_regs() {
 
 template <int R>
 int launch64(const B64& A, cudaStream_t st) {
-  const bool diag = A.diag_p || A.diag_du;
+  const bool diag = A.diag_p || A.diag_du || A.diag_du64;
   if (pd64_const_regs())  // FSB_PD64_CONST=regs: constants in registers (spills)
     return diag ? launch64v<R, kTY, true, false, 2>(A, st) : launch64v<R, kTY, false, false, 2>(A, st);
   return diag ? launch64v<R, kTY, true, true, 2>(A, st) : launch64v<R, kTY, false, true, 2>(A, st);

@@ -29,6 +29,7 @@ struct B64 {
   double du_max;
   const double* dirs; double* wv;
   float* diag_du; double* partials;  // max |du| and per-tile sums of |du| (nullptr = off)
+  double* diag_du64;                 // max |du| in float64 (when set, instead of diag_du)
   // k64_pipe only: per-pixel edge codes (bit0 mask, bit1 x-edge, bit2 y-edge) and
   // the level's work list (tiles[0] = count, tiles[1 + k] = tile id; nullptr = all)
   const uint32_t* ecode;

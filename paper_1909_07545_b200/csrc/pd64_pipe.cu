@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kW * TH, 1) k64_pipe(const B64 A) {
   const bool inner_xy = lane >= R && lane < kW - R && ty >= R && ty < TH - R;
   const int tyd = ty + 1 < TH ? ty + 1 : ty;
   double fin_sum = 0.0;
-  float fin_max = 0.f;
+  double fin_max = 0.0;
 
   int k = blockIdx.x;
   if (k < cnt) stage<R, TH>(S, A, A.tiles ? A.tiles[1 + k] : k, ntx);
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kW * TH, 1) k64_pipe(const B64 A) {
       reinterpret_cast<double2*>(A.wv)[i] = wv;
       if (DIAG) {
         fin_sum += fabs(du);
-        fin_max = fmaxf(fin_max, (float)fabs(du));
+        fin_max = fmax(fin_max, fabs(du));
       }
     }
     if (st) {
@@ -214,22 +214,22 @@ __global__ void __launch_bounds__(kW * TH, 1) k64_pipe(const B64 A) {
         A.dvb[i] = vb0; A.dvb[n + i] = vb1;
       }
     }
-    if (DIAG && A.fin && A.diag_du) {  // per-tile sum of |du| (fixed order), global max
+    if (DIAG && A.fin && (A.diag_du || A.diag_du64)) {  // per-tile sum of |du| (fixed order), global max
       __shared__ double s_sum[TH];
-      __shared__ float s_max[TH];
+      __shared__ double s_max[TH];
       const double sm = warp_sum(fin_sum);
-      const float mx = warp_max(fin_max);
+      const double mx = warp_max(fin_max);
       if (lane == 0) { s_sum[ty] = sm; s_max[ty] = mx; }
       __syncthreads();
       if (lane == 0 && ty == 0) {
-        double t = 0.0;
-        float mm = 0.f;
-        for (int r = 0; r < TH; ++r) { t += s_sum[r]; mm = fmaxf(mm, s_max[r]); }
+        double t = 0.0, mm = 0.0;
+        for (int r = 0; r < TH; ++r) { t += s_sum[r]; mm = fmax(mm, s_max[r]); }
         A.partials[tile] = t;
-        atomic_max_nonneg(A.diag_du, mm);
+        if (A.diag_du64) atomic_max_nonneg(A.diag_du64, mm);
+        else atomic_max_nonneg(A.diag_du, (float)mm);
       }
       fin_sum = 0.0;
-      fin_max = 0.f;
+      fin_max = 0.0;
     }
   }
   cp_wait_all();
@@ -277,7 +277,7 @@ int pipe_th() {
 
 template <int R, int TH>
 int launch_th(const B64& A, cudaStream_t st) {
-  const bool diag = A.diag_p || A.diag_du;
+  const bool diag = A.diag_p || A.diag_du || A.diag_du64;
   return diag ? launch_pipe<R, TH, true>(A, st) : launch_pipe<R, TH, false>(A, st);
 }
 

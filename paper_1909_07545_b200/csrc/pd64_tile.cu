@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(con
     }
     // no solve-mask pixel in the interior: nothing to update or store
     if (!__syncthreads_or(any)) {
-      if (A.fin && DIAG && A.diag_du && lane == 0 && ty == 0) A.partials[tile_id] = 0.0;
+      if (A.fin && DIAG && (A.diag_du || A.diag_du64) && lane == 0 && ty == 0) A.partials[tile_id] = 0.0;
       return;
     }
 #pragma unroll
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(con
       A.dvb[i] = vb0[j]; A.dvb[n + i] = vb1[j];
     }
   }
-  if (DIAG && A.fin && A.diag_du) {
+  if (DIAG && A.fin && (A.diag_du || A.diag_du64)) {
     __shared__ double s_sum[kTR], s_max[kTR];
     const double mx = warp_max(amax), sm = warp_sum(adu);
     if (lane == 0) { s_sum[ty] = sm; s_max[ty] = mx; }
@@ -313,7 +313,8 @@ __global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(con
       double t = 0.0, mm = 0.0;
       for (int k = 0; k < kTR; ++k) { t += s_sum[k]; mm = fmax(mm, s_max[k]); }
       A.partials[tile_id] = t;
-      atomic_max_nonneg(A.diag_du, (float)mm);
+      if (A.diag_du64) atomic_max_nonneg(A.diag_du64, mm);
+        else atomic_max_nonneg(A.diag_du, (float)mm);
     }
   }
 }
@@ -356,7 +357,7 @@ int tile_rows() {
 
 template <int R>
 int launch_r(const B64& A, cudaStream_t st) {
-  const bool diag = A.diag_p || A.diag_du;
+  const bool diag = A.diag_p || A.diag_du || A.diag_du64;
   if (tile_py() == 2 && tile_rows() == 8)
     return diag ? launch_tile<R, 2, 8, true>(A, st) : launch_tile<R, 2, 8, false>(A, st);
   if (tile_py() == 2)

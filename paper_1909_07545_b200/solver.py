@@ -438,10 +438,14 @@ class Solver:
             npd, nw = C.c_int64(), C.c_int64()
             L.fsb_diag_counts(self.H, self.W, C.byref(self.ps), C.byref(npd), C.byref(nw))
             self.d_p = E((npd.value,), torch.float32); self.d_q = E((npd.value,), torch.float32)
-            self.d_du = E((nw.value,), torch.float32)
+            # max |du| per warp: float64 on the float64 path (the reference's
+            # du_max + 1e-15 bound holds exactly), float32 on the float32 path
+            self.d_du = E((nw.value,), torch.float64 if precision == "fp64" else torch.float32)
             self.d_mean = E((nw.value,), torch.float64)
+            f64 = precision == "fp64"
             self.diag = _ext.FsbDiag(_dev.ptr(self.d_p), _dev.ptr(self.d_q),
-                                     _dev.ptr(self.d_du), _dev.ptr(self.d_mean))
+                                     None if f64 else _dev.ptr(self.d_du), _dev.ptr(self.d_mean),
+                                     _dev.ptr(self.d_du) if f64 else None)
         self._traj = None
         self._host = None
         self._out_pool: list = []  # pinned output sets (see _out_set)
