@@ -335,6 +335,20 @@ int fsb_solve_pyramid_f64(const fsb_rig* rig, const fsb_params* prm, const doubl
                           double* u, double* w, double* v, uint8_t* mask, double* i1c,
                           const fsb_diag* diag, void* stream);
 
+/* Warp prologue of the float64 path (solver.py:332-346 + image_derivative_along
+ * 192-202) on one level, for the per-stage gate: i1w = B(I1, x + w), dirs =
+ * B(traj, x + w) renormalised, I_u, rho0. All (h,w[,2]) f64 / u8 device arrays;
+ * i1w and dirs are 0 where invalid (i1w_ok, dir_ok), i1w / dirs / iu / rho0 are 0
+ * off the mask. kind 0: masked-gather kernels (k64_sample / k64_linearize, the
+ * large levels); kind 1: NaN-encoded texel kernels (sample64.cu, levels up to
+ * 256^2). scratch: fsb_warp_linearize_f64_scratch_bytes, 32-byte aligned. */
+size_t fsb_warp_linearize_f64_scratch_bytes(int32_t h, int32_t w);
+int fsb_warp_linearize_f64(int32_t h, int32_t w, const double* i0, const double* i1,
+                           const uint8_t* mask, const double* traj, const uint8_t* traj_ok,
+                           const double* wv, double* i1w, uint8_t* i1w_ok, double* dirs,
+                           uint8_t* dir_ok, double* iu, double* rho0, void* scratch,
+                           size_t scratch_bytes, int32_t kind, void* stream);
+
 /* Live kernel timing for the roofline (bench.py): a phase timer records, on
  * the solve stream, three CUDA events per warp iteration of one pyramid level
  * (`level` 0 = finest, up to `max_warps` warps): before the warp's sampling

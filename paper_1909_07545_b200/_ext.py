@@ -8,11 +8,14 @@ CPU fallback anywhere in the package.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libfsb200.so"
+# FSB_LIB=checked loads the checked debug build (build.py --checked)
+LIB_PATH = Path(__file__).resolve().parent / (
+    "libfsb200_checked.so" if os.environ.get("FSB_LIB") == "checked" else "libfsb200.so")
 
 FSB_OK = 0
 FSB_EINVAL = -1
@@ -33,6 +36,7 @@ EXPORTED = (
     "fsb_pd_iterate", "fsb_thresholding_step", "fsb_warp_finish", "fsb_solve_level", "fsb_diag_counts",
     "fsb_solve_pyramid_workspace_bytes", "fsb_solve_pyramid",
     "fsb_solve_pyramid_f64_workspace_bytes", "fsb_solve_pyramid_f64", "fsb_render", "fsb_graph_create", "fsb_graph_create_f64", "fsb_graph_launch", "fsb_graph_destroy",
+    "fsb_warp_linearize_f64_scratch_bytes", "fsb_warp_linearize_f64",
     "fsb_phase_timer_create", "fsb_phase_timer_read", "fsb_phase_timer_destroy",
     "fsb_solve_pyramid_f64_timed",
     "fsb_ground_truth", "fsb_error_report", "fsb_error_report_scratch_bytes", "fsb_version",
@@ -159,6 +163,8 @@ def lib() -> C.CDLL:
             "fsb_graph_create_f64": (C.c_int, [P(FsbRig), P(FsbParams), vp, vp, vp, vp, vp, sz,
                                                vp, vp, vp, vp, vp, P(FsbDiag), vp,
                                                P(C.c_void_p), P(C.c_int64)]),
+            "fsb_warp_linearize_f64_scratch_bytes": (sz, [i32, i32]),
+            "fsb_warp_linearize_f64": (C.c_int, [i32, i32] + [vp] * 12 + [sz, i32, vp]),
             "fsb_phase_timer_create": (C.c_int, [i32, i32, P(C.c_void_p)]),
             "fsb_phase_timer_read": (C.c_int, [vp, P(C.c_double), P(C.c_double), P(C.c_int32),
                                                P(C.c_int32), P(C.c_int32), P(C.c_int32)]),

@@ -20,6 +20,10 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "_build"
 LIB = PKG / "libfsb200.so"
+# checked build (-DFSB_CHECKED: NaN-poisoned shared memory + index asserts), loaded
+# instead of LIB when FSB_LIB=checked
+BUILD_CHECKED = PKG / "_build_checked"
+LIB_CHECKED = PKG / "libfsb200_checked.so"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
@@ -61,15 +65,18 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False,
+          checked: bool = False) -> Path:
+    bdir, lib = (BUILD_CHECKED, LIB_CHECKED) if checked else (BUILD, LIB)
+    bdir.mkdir(exist_ok=True)
     objs, jobs = [], []
     for src, extra in UNITS:
         s = CSRC / src
-        o = BUILD / (s.stem + ".o")
+        o = bdir / (s.stem + ".o")
         objs.append(o)
         if force or _stale(o, [s, *HEADERS, Path(__file__)]):
-            cmd = [nvcc(), *ARCH, *COMMON, *extra, "-c", str(s), "-o", str(o)]
+            cmd = [nvcc(), *ARCH, *COMMON, *extra, *(["-DFSB_CHECKED"] if checked else []),
+                   "-c", str(s), "-o", str(o)]
             if ptxas_verbose:
                 cmd += ["-Xptxas", "-v"]
             if verbose:
@@ -81,12 +88,12 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
         with ThreadPoolExecutor(workers) as ex:
             for f in [ex.submit(subprocess.run, cmd, check=True) for cmd in jobs]:
                 f.result()
-    if force or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"]
+    if force or _stale(lib, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(lib), *map(str, objs), "-lcudart"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 def main(argv=None) -> int:
@@ -94,8 +101,10 @@ def main(argv=None) -> int:
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--ptxas", action="store_true", help="print ptxas register/smem usage")
+    ap.add_argument("--checked", action="store_true",
+                    help="build libfsb200_checked.so (NaN-poisoned shared memory, index asserts)")
     a = ap.parse_args(argv)
-    out = build(force=a.force, verbose=a.verbose, ptxas_verbose=a.ptxas)
+    out = build(force=a.force, verbose=a.verbose, ptxas_verbose=a.ptxas, checked=a.checked)
     print(out)
     return 0
 

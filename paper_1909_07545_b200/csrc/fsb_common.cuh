@@ -15,6 +15,35 @@
 
 #include "../../include/fsb200.h"
 
+#ifdef FSB_CHECKED
+#include <assert.h>
+#endif
+
+namespace fsb {
+// Checked build (python -m paper_1909_07545_b200.build --checked ->
+// libfsb200_checked.so, loaded with FSB_LIB=checked): the hot kernels fill
+// their dynamic shared memory with NaN before first use and assert their
+// global indices. A read of a shared location no thread wrote for it (a
+// missing barrier, a wrong exchange index) then surfaces as NaN in the
+// results, which the parity tests reject. This is the round-2 substitute for
+// compute-sanitizer, which the GPU pool refuses (profiles/r02_sanitizer_*).
+#ifdef FSB_CHECKED
+__device__ __forceinline__ void poison_dynamic_smem(void* base) {
+  uint32_t bytes;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(bytes));
+  const unsigned nt = blockDim.x * blockDim.y * blockDim.z;
+  const unsigned t = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  uint32_t* q = reinterpret_cast<uint32_t*>(base);
+  for (unsigned k = t; k < bytes / 4; k += nt) q[k] = 0x7ff80000u;  // NaN as f32 and (pairs) f64
+  __syncthreads();
+}
+#define FSB_CHECK(cond) assert(cond)
+#else
+__device__ __forceinline__ void poison_dynamic_smem(void*) {}
+#define FSB_CHECK(cond) ((void)0)
+#endif
+}  // namespace fsb
+
 #define FSB_INLINE __device__ __forceinline__
 
 namespace fsb {

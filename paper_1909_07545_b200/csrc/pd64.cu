@@ -355,6 +355,16 @@ __global__ void k64_finish(L64 L, double du_max, float* dmax, double* dmax64) {
   }
 }
 
+// NaN-encoded sampled image -> (value or 0, validity), the masked-gather convention.
+__global__ void k64_nan_split(double* v, uint8_t* ok, size_t n) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = v[i];
+  const bool k = !isnan(x);
+  ok[i] = k;
+  v[i] = k ? x : 0.0;
+}
+
 __global__ void k64_and_mask(const uint8_t* a, const uint8_t* b, size_t n, uint8_t* o) {
   size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) o[i] = a[i] && b[i];
@@ -825,6 +835,50 @@ int fsb_solve_pyramid_f64(const fsb_rig* rig, const fsb_params* prm, const doubl
                           const fsb_diag* diag, void* stream) {
   return solve_pyramid64(rig, prm, i0, i1, traj_dirs, traj_ok, workspace, workspace_bytes, u, w,
                          v, mask, i1c, diag, as_stream(stream));
+}
+
+size_t fsb_warp_linearize_f64_scratch_bytes(int32_t h, int32_t w) {
+  return (size_t)h * w * sizeof(double4) + 256;
+}
+
+int fsb_warp_linearize_f64(int32_t h, int32_t w, const double* i0, const double* i1,
+                           const uint8_t* mask, const double* traj, const uint8_t* traj_ok,
+                           const double* wv, double* i1w, uint8_t* i1w_ok, double* dirs,
+                           uint8_t* dir_ok, double* iu, double* rho0, void* scratch,
+                           size_t scratch_bytes, int32_t kind, void* stream) {
+  if (h < 1 || w < 1 || !i0 || !i1 || !mask || !traj || !traj_ok || !wv || !i1w || !i1w_ok ||
+      !dirs || !dir_ok || !iu || !rho0 || !scratch ||
+      scratch_bytes < fsb_warp_linearize_f64_scratch_bytes(h, w) || (kind != 0 && kind != 1))
+    return FSB_EINVAL;
+  cudaStream_t st = as_stream(stream);
+  const size_t n = (size_t)h * w;
+  if (kind == 1) {  // NaN-encoded texels (sample64.cu)
+    if (reinterpret_cast<uintptr_t>(scratch) & 31) return FSB_EINVAL;
+    double4* tex = reinterpret_cast<double4*>(scratch);
+    int rc = pack64_internal(i1, mask, traj, traj_ok, h, w, tex, st);
+    if (rc) return rc;
+    P64 PL;
+    PL.h = h; PL.w = w; PL.i0 = i0; PL.mask = mask; PL.tex = tex; PL.wv = wv;
+    PL.i1wn = i1w; PL.dirs = dirs; PL.dir_ok = dir_ok; PL.iu = iu; PL.rho0 = rho0;
+    rc = sample_nan64_internal(PL, kBX, kBY, st);
+    if (rc) return rc;
+    rc = linearize_nan64_internal(PL, kBX, kBY, st);
+    if (rc) return rc;
+    k64_nan_split<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(i1w, i1w_ok, n);
+    return launch_status();
+  }
+  L64 L;  // masked-gather kernels (k64_sample / k64_linearize) with all-16-valid flags
+  memset(&L, 0, sizeof(L));
+  L.h = h; L.w = w; L.n = n;
+  L.i0 = i0; L.i1 = i1; L.mask = mask; L.traj = traj; L.traj_ok = traj_ok;
+  L.wv = const_cast<double*>(wv); L.i1w = i1w; L.i1w_ok = i1w_ok; L.dirs = dirs;
+  L.dir_ok = dir_ok; L.iu = iu; L.rho0 = rho0;
+  L.full16 = reinterpret_cast<uint8_t*>(scratch);
+  dim3 blk(kBX, kBY), grd = grid2d(w, h, blk);
+  k64_full16<<<grd, blk, 0, st>>>(L);
+  k64_sample<<<grd, blk, 0, st>>>(L);
+  k64_linearize<<<grd, blk, 0, st>>>(L, false);
+  return launch_status();
 }
 
 int fsb_phase_timer_create(int32_t level, int32_t max_warps, fsb_phase_timer** out) {

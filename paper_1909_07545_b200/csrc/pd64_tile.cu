@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(con
   constexpr int OW = kW - 2 * R, OH = TH - 2 * R;
   extern __shared__ double s_raw[];
   SmemT<kTR, PY>& S = *reinterpret_cast<SmemT<kTR, PY>*>(s_raw);
+  poison_dynamic_smem(s_raw);  // checked build only
   const int lane = threadIdx.x, ty = threadIdx.y;
   const size_t n = A.n;
   const int W = A.w, H = A.h;
@@ -136,6 +137,7 @@ __global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(con
       u[j] = ub[j] = v0[j] = v1[j] = vb0[j] = vb1[j] = p0[j] = p1[j] = 0.0;
       q0[j] = q1[j] = q2[j] = q3[j] = 0.0;
       if (in) {
+        FSB_CHECK(i < n);
         code = A.ecode[i];
         u[j] = A.su[i];
         v0[j] = A.sv[i]; v1[j] = A.sv[n + i];

@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_level_cluster(const ClusterArgs A) 
   __shared__ float s_redm[32];
   __shared__ double s_psum[kMaxWarps];  // this CTA's sum |du| per warp iteration
   __shared__ unsigned s_cnt;            // this CTA's mask pixels
+  poison_dynamic_smem(s_dyn);           // checked build only (before any DSMEM reader)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int rl = warp / A.wr;                    // row within the band
   const int c0 = (warp % A.wr) * 64 + 2 * lane;  // first column of this pair

@@ -106,8 +106,11 @@ __global__ void __launch_bounds__(kNW * 32, 1)
   constexpr int TW = kEW - 2 * R, TH = kEH - 2 * R, NW = kNW, PY = kPY, EH = kEH;
   constexpr unsigned FULL = 0xffffffffu;
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned staging base, formed as an offset from the shared array
+  // itself (not through a uintptr_t round trip) so the compiler keeps the
+  // shared address space: LDS / STS instead of generic LD / ST.
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  poison_dynamic_smem(smem_raw);  // checked build only (before the mbarrier lives there)
   float* st = reinterpret_cast<float*>(base);  // [12 + 10][EH][64]
   const float* cs = st + kStatePlanes * kPlane;
   f2(*s_top)[3][32] = reinterpret_cast<f2(*)[3][32]>(base + kTileBytes);

@@ -335,6 +335,30 @@ def image_derivative_along(dirs, i1w, i1w_valid, mask):
     return iu, ok & valid
 
 
+def warp_linearize64(i0, i1, mask, traj_dirs, traj_valid, w, kind: int = 0):
+    """The float64 path's warp prologue on one level (solver.py:332-346 with
+    image_derivative_along 192-202): returns (i1w, i1w_ok, dirs, dir_ok, I_u, rho0)
+    as host arrays. kind 0 = masked-gather kernels (large levels), 1 = NaN-encoded
+    texel kernels (levels up to 256^2). i1w / dirs / I_u / rho0 are 0 where invalid
+    and off the mask."""
+    L = _ext.lib()
+    m = np.asarray(mask, dtype=bool)
+    h, wd = m.shape
+    up = lambda a, dt=torch.float64: _dev.upload(np.asarray(a), dt)  # noqa: E731
+    d_i0, d_i1 = up(i0), up(i1)
+    d_m, d_t = up(m, torch.uint8), up(traj_dirs)
+    d_tok, d_w = up(np.asarray(traj_valid, dtype=bool), torch.uint8), up(w)
+    i1w = _dev.empty((h, wd), torch.float64); dirs = _dev.empty((h, wd, 2), torch.float64)
+    iu = _dev.empty((h, wd), torch.float64); rho0 = _dev.empty((h, wd), torch.float64)
+    wok = _dev.empty((h, wd), torch.uint8); dok = _dev.empty((h, wd), torch.uint8)
+    s = _dev.scratch(L.fsb_warp_linearize_f64_scratch_bytes(h, wd))
+    _ext.check(L.fsb_warp_linearize_f64(h, wd, *[_dev.ptr(t) for t in (
+        d_i0, d_i1, d_m, d_t, d_tok, d_w, i1w, wok, dirs, dok, iu, rho0, s)], s.numel(),
+        int(kind), _dev.stream_ptr()), "warp_linearize64")
+    return (_dev.download(i1w), _dev.download(wok, bool), _dev.download(dirs),
+            _dev.download(dok, bool), _dev.download(iu), _dev.download(rho0))
+
+
 def solve_level(i0, i1, traj_dirs, traj_valid, params: SolverParams, mask, init: WarpState,
                 diagnostics: Diagnostics | None = None, *,
                 blocked: bool = True) -> tuple[WarpState, SolverState]:

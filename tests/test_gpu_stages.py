@@ -228,3 +228,34 @@ def test_thresholding():
     assert np.isclose(thresholding_step(2.0, 0.4, 2.0, 0.25, 1.0), 1.8, atol=1e-12)
     assert float(thresholding_step(1.3, 0.0, 2.0, 0.25, 1.0)) == 1.3
     assert float(thresholding_step(1.3, 0.7, 0.0, 0.25, 1.0)) == 1.3
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("amp", [0.0, 1.5, 6.0])
+def test_warp_linearize_stage_gate_fp64(kind, amp):
+    """SURVEY §8(c) per-stage gate of K5 on the float64 path: i1w, dirs, I_u and
+    rho0 each within 1e-6 of the oracle (oracle/fs_oracle.linearize =
+    solver.py:332-346 + 192-202) with validity identical, for a zero, a small
+    and a large random warp field (the large one drives stencils across the mask
+    edge into every fallback branch), with both prologue kernels (kind 0 masked
+    gathers, kind 1 NaN-encoded texels)."""
+    from paper_1909_07545_b200.solver import warp_linearize64
+    g = load_golden("level_solve")
+    h, w = g["mask"].shape
+    rng = np.random.default_rng(int(10 * amp) + kind)
+    wv = amp * rng.standard_normal((h, w, 2))
+    got = warp_linearize64(g["i0"], g["i1"], g["mask"], g["dirs"], g["tok"], wv, kind)
+    ref = O.linearize(g["i0"], g["i1"], g["dirs"], g["tok"], g["mask"], wv)
+    m = g["mask"]
+    i1w, wok, dirs, dok, iu, rho0 = got
+    ri1w, rwok, rdirs, rdok, riu, rrho0 = ref
+    np.testing.assert_array_equal(wok & m, rwok & m)
+    np.testing.assert_array_equal(dok, rdok)
+    assert np.max(np.abs(np.where(m & rwok, i1w - ri1w, 0.0))) <= 1e-6
+    assert np.max(np.abs(dirs - rdirs)) <= 1e-6
+    assert np.max(np.abs(iu - riu)) <= 1e-6
+    assert np.max(np.abs(rho0 - rrho0)) <= 1e-6
+    # the gate is met with orders of margin: same operation order as the oracle
+    assert max(np.max(np.abs(iu - riu)), np.max(np.abs(dirs - rdirs))) <= 1e-12
+    if amp > 0:  # the field really exercises partial stencils
+        assert (rwok & m).sum() < m.sum() or (rdok != m).any()
