@@ -164,7 +164,7 @@ def lib() -> C.CDLL:
                                                vp, vp, vp, vp, vp, P(FsbDiag), vp,
                                                P(C.c_void_p), P(C.c_int64)]),
             "fsb_warp_linearize_f64_scratch_bytes": (sz, [i32, i32]),
-            "fsb_warp_linearize_f64": (C.c_int, [i32, i32] + [vp] * 12 + [sz, i32, vp]),
+            "fsb_warp_linearize_f64": (C.c_int, [i32, i32] + [vp] * 13 + [sz, i32, vp]),
             "fsb_phase_timer_create": (C.c_int, [i32, i32, P(C.c_void_p)]),
             "fsb_phase_timer_read": (C.c_int, [vp, P(C.c_double), P(C.c_double), P(C.c_int32),
                                                P(C.c_int32), P(C.c_int32), P(C.c_int32)]),

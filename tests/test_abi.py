@@ -87,3 +87,23 @@ def test_product_never_imports_oracle():
     pkg = ROOT / "paper_1909_07545_b200"
     for f in pkg.rglob("*.py"):
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", f.read_text(), re.M), f
+
+
+def test_binding_arity_matches_header():
+    """Every ctypes signature in _ext.py takes as many arguments as the C
+    declaration in include/fsb200.h (a short binding passes garbage for the
+    missing trailing arguments)."""
+    from paper_1909_07545_b200 import _ext
+    L = _ext.lib()
+    text = (ROOT / "include" / "fsb200.h").read_text()
+    decls = re.findall(r"^\s*(?:int|size_t|const char\*)\s+(fsb_\w+)\(([^;]*)\);", text,
+                       re.M | re.S)
+    assert len(decls) == len(header_symbols())
+    bad = []
+    for name, args in decls:
+        args = " ".join(args.split())
+        n = 0 if args in ("", "void") else args.count(",") + 1
+        f = getattr(L, name)
+        if f.argtypes is None or len(f.argtypes) != n:
+            bad.append((name, n, None if f.argtypes is None else len(f.argtypes)))
+    assert not bad, bad
