@@ -557,8 +557,9 @@ def _graph_fps(eng, K, warmup, stream, flush, world, dist) -> tuple[float, objec
     return float(t_all.item()) / 1e3, clk
 
 
-def _e2e(solve, h0, h1, K, warmup, world, dist) -> float:
-    """Seconds for K calls of the public API on host float64 arrays (max over ranks)."""
+def _e2e(solve, h0, h1, K, warmup, world, dist) -> tuple[float, list]:
+    """Seconds for K calls of the public API on host float64 arrays (max over
+    ranks), and the per-call milliseconds of this rank."""
     import torch
     for _ in range(max(warmup, 5)):  # engine build, graph capture, pinned pools
         res = solve(h0, h1)
@@ -566,14 +567,17 @@ def _e2e(solve, h0, h1, K, warmup, world, dist) -> float:
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    calls = []
     t0 = time.perf_counter()
     for _ in range(K):
-        res = solve(h0, h1)
+        t1 = time.perf_counter()
+        res = solve(h0, h1)  # returns after its D2H: the call is synchronous
+        calls.append((time.perf_counter() - t1) * 1e3)
     torch.cuda.synchronize()
     te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    return float(te.item())
+    return float(te.item()), calls
 
 
 def run_b200(a) -> None:
@@ -623,8 +627,11 @@ def run_b200(a) -> None:
 
     e2e = None
     if not a.no_e2e:
-        te = _e2e(lambda p, q: solve_pyramid(p, q, rig, prm), x0, x1, K, a.warmup, world, dist)
+        te, calls = _e2e(lambda p, q: solve_pyramid(p, q, rig, prm), x0, x1, K, a.warmup,
+                         world, dist)
         e2e = {"value": world * K / te, "unit": "frames/s",
+               "ms_per_call": {"min": min(calls), "median": statistics.median(calls),
+                               "max": max(calls)},
                "h2d_bytes_per_step": 2 * H * W * 8,
                "d2h_bytes_per_step": H * W * (8 + 16 + 16 + 1 + 8),
                "api": "paper_1909_07545_b200.solve_pyramid (float64 host arrays in, "
@@ -650,8 +657,8 @@ def run_b200(a) -> None:
                     e32.u.cpu().numpy(), e32.mask.cpu().numpy().astype(bool))
                     if name == "c3" else None)}
         if not a.no_e2e:
-            te = _e2e(lambda p, q: solve_pyramid(p, q, rig, prm, precision="fp32"), x0, x1,
-                      K, a.warmup, 1, None)
+            te, _ = _e2e(lambda p, q: solve_pyramid(p, q, rig, prm, precision="fp32"), x0, x1,
+                         K, a.warmup, 1, None)
             fp32["e2e"] = {"value": K / te, "unit": "frames/s",
                            "h2d_bytes_per_step": 2 * H * W * 4,
                            "d2h_bytes_per_step": H * W * (8 + 16 + 16 + 1 + 8)}

@@ -493,7 +493,17 @@ int pd64_prefetch() {
   return v;
 }
 
-int pd64_launch(const B64& A, int halo, cudaStream_t st) {
+int pd64_launch(const B64& A0, int halo, cudaStream_t st) {
+  static const int zero = [] {  // FSB_PD64_ZERO=1: timing experiment, load/store only
+    const char* e = getenv("FSB_PD64_ZERO");
+    return e && e[0] == '1';
+  }();
+  B64 A = A0;
+  if (zero && halo <= 3) {
+    A.iters = 0;
+    if (pd64_kernel_for(halo) == K64_TILEL || pd64_kernel_for(halo) == K64_TILE)
+      return pd64_tile_launch_unchecked(A, halo, st);
+  }
   switch (pd64_kernel_for(halo)) {
     case K64_PIPE: return pd64_pipe_launch(A, halo, st);
     case K64_TILE: case K64_TILEL: return pd64_tile_launch(A, halo, st);
@@ -555,6 +565,18 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
   if (halo == 2 && getenv("FSB_PD64") == nullptr) {
     if (pd64_tile_count(L.w, L.h, 5) <= 2 * 148) halo = 5;
     else if (pd64_tile_count(L.w, L.h, 3) <= 2 * 148) halo = 3;
+  }
+  if (halo > 0) {  // FSB_PD64_HALO_L="w:R,w:R" overrides per level width (tuning)
+    const char* e = getenv("FSB_PD64_HALO_L");
+    for (const char* c = e; c && *c;) {
+      const int lw = atoi(c);
+      const char* colon = strchr(c, ':');
+      if (!colon) break;
+      const int r = atoi(colon + 1);
+      if (lw == L.w && (r == 1 || r == 2 || r == 3 || r == 5)) halo = r;
+      c = strchr(colon, ',');
+      if (c) ++c;
+    }
   }
   const int kern = halo > 0 ? pd64_kernel_for(halo) : -1;
   const bool listed = kern == K64_PIPE || kern == K64_TILEL;
@@ -741,23 +763,6 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
     rc = downsample64_internal(P.lvl_i1[l - 1], P.lvl_mask[l - 1], fh, fw, P.lvl_i1[l],
                                P.lvl_mask[l], ch, cw, st);
     if (rc) return rc;
-  }
-  // FSB_L2PERSIST=1 (experiment): keep the per-level tensor / step planes
-  // (P.T, P.S: contiguous, 48 B/px) L2-persisting for the frame
-  static const bool l2p = [] {
-    const char* e = getenv("FSB_L2PERSIST");
-    return e && e[0] == '1';
-  }();
-  if (l2p) {
-    const size_t bytes = 6 * n0 * sizeof(double);
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes);
-    cudaStreamAttrValue av = {};
-    av.accessPolicyWindow.base_ptr = P.T;
-    av.accessPolicyWindow.num_bytes = bytes;
-    av.accessPolicyWindow.hitRatio = 1.0f;
-    av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &av);
   }
   int64_t pd_off = 0, warp_off = 0;
   int cur = 0, prev_h = 0, prev_w = 0;

@@ -42,6 +42,7 @@ int pd64_block_launch(const B64& A, int halo, cudaStream_t st);
 size_t pd64_block_tiles(int w, int h, int halo);
 // The issue-lean tile kernel (pd64_tile.cu): same arguments and semantics.
 int pd64_tile_launch(const B64& A, int halo, cudaStream_t st);
+int pd64_tile_launch_unchecked(const B64& A, int halo, cudaStream_t st);  // iters 0: timing
 size_t pd64_tile_count(int w, int h, int halo);
 int pd64_tile_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles, cudaStream_t st);
 // The persistent, cp.async-pipelined kernel (pd64_pipe.cu), halo 2 or 3.

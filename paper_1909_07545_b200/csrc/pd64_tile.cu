@@ -384,6 +384,14 @@ int pd64_tile_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles,
                             st);
 }
 
+int pd64_tile_launch_unchecked(const B64& A, int halo, cudaStream_t st) {
+  switch (halo) {
+    case 2: return launch_r<2>(A, st);
+    case 3: return launch_r<3>(A, st);
+    default: return FSB_EINVAL;
+  }
+}
+
 int pd64_tile_launch(const B64& A, int halo, cudaStream_t st) {
   if (A.iters < 1 || A.iters > halo) return FSB_EINVAL;
   switch (halo) {

@@ -44,3 +44,20 @@ for _ in range(10):
 torch.cuda.synchronize()
 print(prec, {k: round(v * 100, 3) for k, v in T.items()}, "ms/call; full API", round(full, 2),
       "ms/call; eng.solve", round((time.perf_counter() - t0) * 100, 2), "ms/call")
+
+# where does the API call spend its time beyond eng.solve?
+import paper_1909_07545_b200.solver as SV
+made = []
+orig_init = SV.Solver.__init__
+def counting_init(self, *a, **k):
+    made.append(1)
+    return orig_init(self, *a, **k)
+SV.Solver.__init__ = counting_init
+pools = []
+ts = []
+for _ in range(10):
+    t = time.perf_counter()
+    r = solve_pyramid(i0, i1, rig, prm, precision=prec)
+    ts.append(round((time.perf_counter() - t) * 1e3, 2))
+    pools.append([len(e._out_pool) for v in SV._CACHE.values() for e in v])
+print("per-call ms", ts, "engines built", len(made), "pool sizes", pools[-1], "cache keys", len(SV._CACHE))
