@@ -485,12 +485,16 @@ int pd64_kernel_for(int halo) {
   const int k = pd64_kernel_choice();
   return k == K64_PIPE && halo != 2 && halo != 3 ? K64_TILEL : k;
 }
-int pd64_prefetch() {
+// Persistent, phase-staggered k64_tile on the halo-2 (large) levels: 2 CTAs per
+// SM stride over the work list and the second half starts 2 us late, so an SM's
+// two CTAs keep opposite phases (C3 1024^2: 16.5 -> 15.9 ms). The small levels
+// (halo 3 / 5, one wave) keep one tile per CTA. FSB_PD64_PERSIST=<ns> (0 = off).
+int pd64_persist(int halo) {
   static const int v = [] {
-    const char* e = getenv("FSB_PD64_PF");
-    return e ? atoi(e) : 0;
+    const char* e = getenv("FSB_PD64_PERSIST");
+    return e ? atoi(e) : 2000;
   }();
-  return v;
+  return halo == 2 ? v : 0;
 }
 
 int pd64_launch(const B64& A0, int halo, cudaStream_t st) {
@@ -644,7 +648,7 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
       A.partials = L.partials;
       A.ecode = listed ? L.ecode : nullptr;
       A.tiles = listed ? L.tiles : nullptr;
-      A.prefetch = pd64_prefetch();
+      A.persist = pd64_persist(halo);
       if (listed && (A.diag_du || A.diag_du64))  // tiles off the work list keep a zero partial sum
         cudaMemsetAsync(L.partials, 0, pd64_tiles(L.w, L.h, halo) * sizeof(double), st);
       rc = pd64_launch(A, halo, st);

@@ -34,7 +34,7 @@ struct B64 {
   // the level's work list (tiles[0] = count, tiles[1 + k] = tile id; nullptr = all)
   const uint32_t* ecode;
   const int* tiles;
-  int prefetch;  // k64_tile with a work list: L2-prefetch the tile this many list entries ahead (0 = off)
+  int persist;   // k64_tile with a work list: persistent 2 CTAs / SM, second half staggered by this many ns (0 = one tile per CTA)
 };
 
 // `iters` (<= halo, halo in 1..3 or 5) cycles from the src set into the dst set.

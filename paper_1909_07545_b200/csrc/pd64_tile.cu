@@ -48,76 +48,34 @@ struct SmemT {
   double c[9][TH][kW];                              // a b c sp tu tv g rho0 u_omega
 };
 
+int sm_count() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return v;
+}
+
 FSB_INLINE double shfl_dn(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 FSB_INLINE double shfl_up(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
 
-// Base pointer of staging plane l (0..20) of the source set and constants.
-FSB_INLINE const double* plane_ptr(const B64& A, int l) {
-  const size_t n = A.n;
-  switch (l) {
-    case 0: return A.su;
-    case 1: return A.sv;
-    case 2: return A.sv + n;
-    case 3: return A.sp;
-    case 4: return A.sp + n;
-    case 5: case 6: case 7: case 8: return A.sq + (l - 5) * n;
-    case 9: case 10: case 11: return A.T + (l - 9) * n;
-    case 12: case 13: case 14: return A.S + (l - 12) * n;
-    case 15: return A.iu;
-    case 16: return A.rho0;
-    case 17: return A.sub;
-    case 18: return A.svb;
-    case 19: return A.svb + n;
-    default: return A.uo;
-  }
-}
-
+// One tile (bx, by) of the level: load, `iters` cycles, epilogue, stores.
 template <int R, int PY, int kTR, bool DIAG>
-__global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(const B64 A) {
+FSB_INLINE void tile_work(const B64& A, SmemT<kTR, PY>& S, int bx, int by, int tile_id) {
   constexpr int TH = kTR * PY;
   constexpr int OW = kW - 2 * R, OH = TH - 2 * R;
-  extern __shared__ double s_raw[];
-  SmemT<kTR, PY>& S = *reinterpret_cast<SmemT<kTR, PY>*>(s_raw);
-  poison_dynamic_smem(s_raw);  // checked build only
   const int lane = threadIdx.x, ty = threadIdx.y;
   const size_t n = A.n;
   const int W = A.w, H = A.h;
-  const int ntx = (W + OW - 1) / OW;
-  int bx = blockIdx.x, by = blockIdx.y;
-  if (A.tiles) {  // 1-D grid over the level's work list of tiles holding mask pixels
-    const int cnt = A.tiles[0];
-    if ((int)blockIdx.x >= cnt) return;
-    const int t = A.tiles[1 + blockIdx.x];
-    bx = t % ntx;
-    by = t / ntx;
-    // L2 prefetch of the tile one resident wave ahead (its CTA starts about one
-    // CTA lifetime from now): lane l < 21 fetches staging plane l of its row
-    const int k2 = (int)blockIdx.x + A.prefetch;
-    if (A.prefetch > 0 && k2 < cnt && lane < 21 + 1 && !(A.first && lane >= 17 && lane < 21)) {
-      const int t2 = A.tiles[1 + k2];
-      const int px0 = max((t2 % ntx) * OW - R, 0), py = (t2 / ntx) * OH - R + ty * PY;
-      const int px1 = min(px0 + kW, W) - 1;
-#pragma unroll
-      for (int j = 0; j < PY; ++j) {
-        if ((unsigned)(py + j) < (unsigned)H) {
-          const size_t r = (size_t)(py + j) * W;
-          const char* b0 = lane < 21 ? reinterpret_cast<const char*>(plane_ptr(A, lane) + r)
-                                     : reinterpret_cast<const char*>(A.ecode + r);
-          const size_t es = lane < 21 ? 8 : 4;
-          for (size_t o = (size_t)px0 * es & ~size_t(127); o <= (size_t)px1 * es; o += 128)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(b0 + o));
-        }
-      }
-    }
-  }
   const int gx = bx * OW - R + lane;
   const int gy0 = by * OH - R + ty * PY;
-  const int tile_id = by * ntx + bx;
 
   double u[PY], ub[PY], v0[PY], v1[PY], vb0[PY], vb1[PY], p0[PY], p1[PY];
   double q0[PY], q1[PY], q2[PY], q3[PY];
   bool m[PY], ex[PY], ey[PY], inner[PY];
-  size_t idx[PY];
+  uint32_t idx[PY];
   const double alpha1 = A.alpha1;
   if (A.ecode) {
     // Speculative loads: the work list guarantees mask pixels in the interior,
@@ -125,32 +83,41 @@ __global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(con
     // in-image pixel loads unconditionally — one memory round trip, no
     // dependency on the mask.
 #pragma unroll
+    // 32-bit pixel offsets from kernel-uniform plane pointers: one address
+    // instruction per plane. Out-of-image threads read pixel 0 (finite values)
+    // and get edge code 0, so nothing they compute reaches an in-image pixel.
+    const double* __restrict__ sv1 = A.sv + n;
+    const double* __restrict__ sp1 = A.sp + n;
+    const double* __restrict__ sq1 = A.sq + n;
+    const double* __restrict__ sq2 = A.sq + 2 * n;
+    const double* __restrict__ sq3 = A.sq + 3 * n;
+    const double* __restrict__ t1 = A.T + n;
+    const double* __restrict__ t2 = A.T + 2 * n;
+    const double* __restrict__ s1 = A.S + n;
+    const double* __restrict__ s2 = A.S + 2 * n;
+    const double* __restrict__ svb1 = A.svb + n;
+#pragma unroll
     for (int j = 0; j < PY; ++j) {
       const int gy = gy0 + j;
       const bool in = (unsigned)gx < (unsigned)W && (unsigned)gy < (unsigned)H;
-      const size_t i = in ? (size_t)gy * W + gx : 0;
+      const uint32_t i = in ? (uint32_t)gy * (uint32_t)W + (uint32_t)gx : 0u;
+      FSB_CHECK(i < n);
       idx[j] = i;
       const int ry = ty * PY + j;
       inner[j] = lane >= R && lane < kW - R && ry >= R && ry < TH - R && in;
-      double cc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-      uint32_t code = 0;
-      u[j] = ub[j] = v0[j] = v1[j] = vb0[j] = vb1[j] = p0[j] = p1[j] = 0.0;
-      q0[j] = q1[j] = q2[j] = q3[j] = 0.0;
-      if (in) {
-        FSB_CHECK(i < n);
-        code = A.ecode[i];
-        u[j] = A.su[i];
-        v0[j] = A.sv[i]; v1[j] = A.sv[n + i];
-        p0[j] = A.sp[i]; p1[j] = A.sp[n + i];
-        q0[j] = A.sq[i]; q1[j] = A.sq[n + i]; q2[j] = A.sq[2 * n + i]; q3[j] = A.sq[3 * n + i];
-        cc[0] = A.T[i]; cc[1] = A.T[n + i]; cc[2] = A.T[2 * n + i];
-        cc[3] = A.S[i] * alpha1; cc[4] = A.S[n + i]; cc[5] = A.S[2 * n + i];
-        cc[6] = A.iu[i]; cc[7] = A.rho0[i];
-        if (A.first) {
-          ub[j] = u[j]; vb0[j] = v0[j]; vb1[j] = v1[j]; cc[8] = u[j];
-        } else {
-          ub[j] = A.sub[i]; vb0[j] = A.svb[i]; vb1[j] = A.svb[n + i]; cc[8] = A.uo[i];
-        }
+      const uint32_t code = in ? A.ecode[i] : 0u;
+      u[j] = A.su[i];
+      v0[j] = A.sv[i]; v1[j] = sv1[i];
+      p0[j] = A.sp[i]; p1[j] = sp1[i];
+      q0[j] = A.sq[i]; q1[j] = sq1[i]; q2[j] = sq2[i]; q3[j] = sq3[i];
+      double cc[9];
+      cc[0] = A.T[i]; cc[1] = t1[i]; cc[2] = t2[i];
+      cc[3] = A.S[i] * alpha1; cc[4] = s1[i]; cc[5] = s2[i];
+      cc[6] = A.iu[i]; cc[7] = A.rho0[i];
+      if (A.first) {
+        ub[j] = u[j]; vb0[j] = v0[j]; vb1[j] = v1[j]; cc[8] = u[j];
+      } else {
+        ub[j] = A.sub[i]; vb0[j] = A.svb[i]; vb1[j] = svb1[i]; cc[8] = A.uo[i];
       }
       m[j] = code & 1u;
       ex[j] = code & 2u;
@@ -165,7 +132,7 @@ __global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(con
       const int gy = gy0 + j;
       const bool in = (unsigned)gx < (unsigned)W && (unsigned)gy < (unsigned)H;
       const size_t i = in ? (size_t)gy * W + gx : 0;
-      idx[j] = i;
+      idx[j] = (uint32_t)i;
       m[j] = in && A.mask[i];
       ex[j] = m[j] && gx + 1 < W && A.mask[i + 1];
       ey[j] = m[j] && gy + 1 < H && A.mask[i + W];
@@ -281,7 +248,7 @@ __global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(con
 #pragma unroll
   for (int j = 0; j < PY; ++j) {
     const int ry = ty * PY + j;
-    const size_t i = idx[j];
+    const uint32_t i = idx[j];
     const bool st = inner[j] && m[j];
     const double uo = S.c[8][ry][lane];
     if (A.fin && st) {  // clip / accumulate (solver.py:356-360) on the interior
@@ -298,12 +265,13 @@ __global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(con
     if (!st) continue;
     if (A.first) A.uo[i] = uo;
     A.du[i] = u[j];
-    A.dv[i] = v0[j]; A.dv[n + i] = v1[j];
-    A.dp[i] = p0[j]; A.dp[n + i] = p1[j];
-    A.dq[i] = q0[j]; A.dq[n + i] = q1[j]; A.dq[2 * n + i] = q2[j]; A.dq[3 * n + i] = q3[j];
+    A.dv[i] = v0[j]; (A.dv + n)[i] = v1[j];
+    A.dp[i] = p0[j]; (A.dp + n)[i] = p1[j];
+    A.dq[i] = q0[j]; (A.dq + n)[i] = q1[j]; (A.dq + 2 * n)[i] = q2[j];
+    (A.dq + 3 * n)[i] = q3[j];
     if (!A.fin) {  // u_bar / v_bar are reset at the next warp's start: dead after its last cycle
       A.dub[i] = ub[j];
-      A.dvb[i] = vb0[j]; A.dvb[n + i] = vb1[j];
+      A.dvb[i] = vb0[j]; (A.dvb + n)[i] = vb1[j];
     }
   }
   if (DIAG && A.fin && (A.diag_du || A.diag_du64)) {
@@ -322,12 +290,39 @@ __global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(con
 }
 
 template <int R, int PY, int kTR, bool DIAG>
+__global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(const B64 A) {
+  constexpr int TH = kTR * PY;
+  constexpr int OW = kW - 2 * R, OH = TH - 2 * R;
+  extern __shared__ double s_raw[];
+  SmemT<kTR, PY>& S = *reinterpret_cast<SmemT<kTR, PY>*>(s_raw);
+  poison_dynamic_smem(s_raw);  // checked build only
+  const int ntx = (A.w + OW - 1) / OW;
+  if (!A.tiles) {  // 2-D grid over every tile
+    tile_work<R, PY, kTR, DIAG>(A, S, blockIdx.x, blockIdx.y, blockIdx.y * ntx + blockIdx.x);
+    return;
+  }
+  // 1-D grid over the level's work list. With A.persist the grid is 2 CTAs per
+  // SM striding over the list, and the second half of the CTAs starts
+  // A.persist ns late, so an SM's two CTAs keep opposite phases (one loading
+  // while the other cycles) instead of loading in step.
+  const int cnt = A.tiles[0];
+  const int stride = A.persist ? (int)gridDim.x : cnt;
+  if (A.persist && blockIdx.x >= gridDim.x / 2) __nanosleep((unsigned)A.persist);
+  for (int k = blockIdx.x; k < cnt; k += stride) {
+    const int t = A.tiles[1 + k];
+    tile_work<R, PY, kTR, DIAG>(A, S, t % ntx, t / ntx, t);
+    if (A.persist) __syncthreads();  // shared tile buffers are reused by the next tile
+  }
+}
+
+template <int R, int PY, int kTR, bool DIAG>
 int launch_tile(const B64& A, cudaStream_t st) {
   constexpr int TH = kTR * PY;
   constexpr int OW = kW - 2 * R, OH = TH - 2 * R;
   const int ntx = (A.w + OW - 1) / OW, nty = (A.h + OH - 1) / OH;
   // with a work list: a 1-D grid of every tile (CTAs past the list's count exit)
-  const dim3 blk(kW, kTR), grd = A.tiles ? dim3(ntx * nty) : dim3(ntx, nty);
+  const dim3 blk(kW, kTR),
+      grd = A.tiles ? dim3(A.persist ? 2 * sm_count() : ntx * nty) : dim3(ntx, nty);
   const size_t dyn = sizeof(SmemT<kTR, PY>);
   static std::atomic<unsigned long long> attr{0};
   once_per_device(attr, [&] {
