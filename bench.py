@@ -493,6 +493,8 @@ def pd64_roofline(eng, prm) -> tuple[dict, dict]:
     traffic, traffic_src = profiled_traffic("*_pd64_ncu.txt")
     pd = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
           "frac": achieved / peak, "traffic": traffic,
+          # the real DRAM fraction: ncu bytes of one launch over the live launch time
+          "dram_frac": (traffic / (us_launch * 1e-6) / 1e9 / peak) if traffic else None,
           "kernel": (f"float64 primal-dual launch at the finest level ({W}x{H}), "
                      f"{cycles:g} PD cycles per launch"),
           "algorithmic_bytes_per_launch": bytes_launch,

@@ -6,8 +6,10 @@ mapping path (solver.py:36-452): `SolverParams`, `StereoResult`, `WarpState`,
 `primal_dual_iterate`, `compute_tensor`, `precondition_steps`,
 `image_derivative_along`, `warp_image`, `thresholding_step`,
 `calibrate_second_image`. Host arrays in (float64, any layout the reference
-accepts), host arrays out (float64 / bool) — every pixel of work runs in
-libfsb200's sm_100a kernels.
+accepts), host arrays out (float64 / bool) — every pixel of the solve runs in
+libfsb200's sm_100a kernels. `energy`, `apply_tensor` and `sqrt_tensor` are
+host-side evaluation helpers kept for the reference's tests (solver.py:164-178,
+455-473); they are not on the solve path.
 
 `Solver` is the device-resident engine underneath `solve_pyramid`: it owns the
 workspace for one (rig, params) pair, can capture the whole frame into a CUDA
