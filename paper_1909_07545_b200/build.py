@@ -41,7 +41,6 @@ UNITS = [
     ("pd64.cu", ["-fmad=false"]),
     ("pd64_block.cu", ["-fmad=false"]),
     ("pd64_tile.cu", []),
-    ("pd64_pipe.cu", []),
     ("sample64.cu", ["-fmad=false"]),
     ("solver.cu", []),
     ("synth.cu", ["-fmad=false"]),

@@ -92,7 +92,7 @@ struct L64 {
   double *u2, *ub2, *v2, *vb2, *p2, *q2;
   // per-pixel flags: bit0 all 16 bicubic taps in mask, bit1 all in traj_ok (nullptr = off)
   uint8_t* full16;
-  // k64_pipe: per-pixel edge codes and the level's tile work list
+  // k64_tile: per-pixel edge codes and the level's tile work list
   uint32_t* ecode;
   int* tiles;
   double4* tex;  // NaN-encoded packed texels of the level (sample64.cu)
@@ -467,24 +467,21 @@ fsb_camera scaled(const fsb_camera& c, int h, int w) {  // camera.py:66-77
 
 // FSB_PD64=plain runs the one-cycle-per-launch kernels (reference for the
 // blocked kernel in tests/tools); default: blocked, halo 2.
-// Blocked PD kernel choice. FSB_PD64K=block: the round-1 k64_block; =tile:
-// k64_tile everywhere; default (pipe): k64_pipe on levels that run halo 2 / 3
-// (the large ones), k64_tile on the small levels (halo 5).
-enum { K64_BLOCK = 0, K64_TILE = 1, K64_PIPE = 2, K64_TILEL = 3 };
+// Blocked PD kernel choice. Default: k64_tile over the level's work list of
+// mask tiles (K64_TILEL). FSB_PD64K=tile: k64_tile over every tile (masked
+// gathers, no work list); =block: the round-1 k64_block (pd64_block.cu). The
+// persistent cp.async-pipelined variants measured slower.
+enum { K64_BLOCK = 0, K64_TILE = 1, K64_TILEL = 3 };
 int pd64_kernel_choice() {
   static const int v = [] {
     const char* e = getenv("FSB_PD64K");
     if (e && strcmp(e, "block") == 0) return (int)K64_BLOCK;
     if (e && strcmp(e, "tile") == 0) return (int)K64_TILE;
-    if (e && strcmp(e, "pipe") == 0) return (int)K64_PIPE;
     return (int)K64_TILEL;
   }();
   return v;
 }
-int pd64_kernel_for(int halo) {
-  const int k = pd64_kernel_choice();
-  return k == K64_PIPE && halo != 2 && halo != 3 ? K64_TILEL : k;
-}
+int pd64_kernel_for(int) { return pd64_kernel_choice(); }
 // Persistent, phase-staggered k64_tile on the halo-2 (large) levels: 2 CTAs per
 // SM stride over the work list and the second half starts 2 us late, so an SM's
 // two CTAs keep opposite phases (C3 1024^2: 16.5 -> 15.9 ms). The small levels
@@ -509,7 +506,6 @@ int pd64_launch(const B64& A0, int halo, cudaStream_t st) {
       return pd64_tile_launch_unchecked(A, halo, st);
   }
   switch (pd64_kernel_for(halo)) {
-    case K64_PIPE: return pd64_pipe_launch(A, halo, st);
     case K64_TILE: case K64_TILEL: return pd64_tile_launch(A, halo, st);
     default: return pd64_block_launch(A, halo, st);
   }
@@ -517,7 +513,6 @@ int pd64_launch(const B64& A0, int halo, cudaStream_t st) {
 
 size_t pd64_tiles(int w, int h, int halo) {
   switch (pd64_kernel_for(halo)) {
-    case K64_PIPE: return pd64_pipe_count(w, h, halo);
     case K64_TILE: case K64_TILEL: return pd64_tile_count(w, h, halo);
     default: return pd64_block_tiles(w, h, halo);
   }
@@ -583,12 +578,11 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
     }
   }
   const int kern = halo > 0 ? pd64_kernel_for(halo) : -1;
-  const bool listed = kern == K64_PIPE || kern == K64_TILEL;
+  const bool listed = kern == K64_TILEL;
   if (listed) {  // per-level edge codes and tile work list
     rc = pd64_edge_codes(L.mask, L.w, L.h, L.ecode, st);
     if (rc) return rc;
-    rc = kern == K64_PIPE ? pd64_pipe_tile_list(L.mask, L.w, L.h, halo, L.tiles, st)
-                          : pd64_tile_tile_list(L.mask, L.w, L.h, halo, L.tiles, st);
+    rc = pd64_tile_tile_list(L.mask, L.w, L.h, halo, L.tiles, st);
     if (rc) return rc;
   }
   // Warp prologue: the NaN-encoded texel kernels (sample64.cu) on levels up to

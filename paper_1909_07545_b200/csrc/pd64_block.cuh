@@ -30,7 +30,7 @@ struct B64 {
   const double* dirs; double* wv;
   float* diag_du; double* partials;  // max |du| and per-tile sums of |du| (nullptr = off)
   double* diag_du64;                 // max |du| in float64 (when set, instead of diag_du)
-  // k64_pipe only: per-pixel edge codes (bit0 mask, bit1 x-edge, bit2 y-edge) and
+  // k64_tile with a work list: per-pixel edge codes (bit0 mask, bit1 x-edge, bit2 y-edge) and
   // the level's work list (tiles[0] = count, tiles[1 + k] = tile id; nullptr = all)
   const uint32_t* ecode;
   const int* tiles;
@@ -45,11 +45,7 @@ int pd64_tile_launch(const B64& A, int halo, cudaStream_t st);
 int pd64_tile_launch_unchecked(const B64& A, int halo, cudaStream_t st);  // iters 0: timing
 size_t pd64_tile_count(int w, int h, int halo);
 int pd64_tile_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles, cudaStream_t st);
-// The persistent, cp.async-pipelined kernel (pd64_pipe.cu), halo 2 or 3.
-int pd64_pipe_launch(const B64& A, int halo, cudaStream_t st);
-size_t pd64_pipe_count(int w, int h, int halo);
-int pd64_pipe_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles,
-                        cudaStream_t st);
+// Per-level edge codes (bit0 mask, bit1 x-edge, bit2 y-edge; pd64_tile.cu).
 int pd64_edge_codes(const uint8_t* mask, int w, int h, uint32_t* code, cudaStream_t st);
 
 }  // namespace fsb
