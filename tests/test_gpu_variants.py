@@ -1,0 +1,61 @@
+"""The float64 path's kernel variants agree (each switch is read once per
+process, so every variant runs in a child process on the golden pair and on a
+C1 frame): the default (k64_tile over the per-level work list, phase-staggered
+persistent schedule, NaN-texel prologue on small levels) against
+  * the non-persistent schedule (FSB_PD64_PERSIST=0)      -> bit-identical,
+  * k64_tile over every tile with masked loads (FSB_PD64K=tile) -> bit-identical,
+  * the masked-gather prologue everywhere (FSB_PRO64=old) -> <= 1e-10 px,
+  * the round-1 k64_block, no FMA (FSB_PD64K=block)       -> <= 1e-8 px.
+Scheduling and load strategy must not change a single bit of the answer."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+from conftest import load_golden
+import test_gpu_solve as T
+import bench
+from paper_1909_07545_b200 import synth as S
+from paper_1909_07545_b200.solver import solve_pyramid
+g = load_golden("pyramid_solve")
+r = solve_pyramid(g["i0"], g["i1"], T._rig(g), T._params(g))
+rig1, prm1 = bench.product_rig("c1"), bench.product_params("c1")
+sc = S.default_scene()
+i0 = S.render(sc, rig1.cam0, supersample=1)[0]
+i1 = S.render(sc, rig1.cam1, pose=rig1.pose, supersample=1)[0]
+r1 = solve_pyramid(i0, i1, rig1, prm1)
+np.savez(sys.argv[2], u=r.u, w=r.w, v=r.v, u1=r1.u, w1=r1.w)
+"""
+
+
+def _run(tmp_path, name, env_extra):
+    out = tmp_path / f"{name}.npz"
+    env = dict(os.environ, **env_extra)
+    subprocess.run([sys.executable, "-c", _CHILD, str(ROOT), str(out)], env=env, check=True,
+                   timeout=900)
+    with np.load(out) as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.mark.parametrize("name,env,tol", [
+    ("persist0", {"FSB_PD64_PERSIST": "0"}, 0.0),
+    ("alltiles", {"FSB_PD64K": "tile"}, 0.0),
+    ("prologue_old", {"FSB_PRO64": "old"}, 1e-10),
+    ("block", {"FSB_PD64K": "block"}, 1e-8),
+])
+def test_float64_kernel_variants_agree(tmp_path, name, env, tol):
+    base = _run(tmp_path, "default", {})
+    var = _run(tmp_path, name, env)
+    for k in base:
+        d = float(np.max(np.abs(base[k] - var[k])))
+        assert d <= tol, (name, k, d)
