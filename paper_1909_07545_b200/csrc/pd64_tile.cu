@@ -316,11 +316,14 @@ __global__ void __launch_bounds__(kW * kTR, kTR * PY <= 16 ? 2 : 1) k64_tile(con
 }
 
 template <int R, int PY, int kTR, bool DIAG>
-int launch_tile(const B64& A, cudaStream_t st) {
+int launch_tile(const B64& A0, cudaStream_t st) {
   constexpr int TH = kTR * PY;
   constexpr int OW = kW - 2 * R, OH = TH - 2 * R;
+  B64 A = A0;
+  if (kTR * PY > 16) A.persist = 0;  // the staggered schedule needs 2 CTAs per SM
   const int ntx = (A.w + OW - 1) / OW, nty = (A.h + OH - 1) / OH;
-  // with a work list: a 1-D grid of every tile (CTAs past the list's count exit)
+  // with a work list: a 1-D grid of every tile (CTAs past the list's count exit),
+  // or 2 persistent CTAs per SM
   const dim3 blk(kW, kTR),
       grd = A.tiles ? dim3(A.persist ? 2 * sm_count() : ntx * nty) : dim3(ntx, nty);
   const size_t dyn = sizeof(SmemT<kTR, PY>);
@@ -344,21 +347,43 @@ int tile_py() {
 // thread rows per CTA: 16 for one pixel per thread; FSB_PD64_PY=2 stacks two
 // pixels per thread on 8 thread rows (same 32 x 16 tile, 2 CTAs / SM) or, with
 // FSB_PD64_PY=2t, on 16 thread rows (32 x 32 tile, 1 CTA / SM)
-int tile_rows() {
-  static const int v = [] {
+// Thread rows per CTA (one pixel per thread): 16 (2 CTAs / SM; the large,
+// DRAM-streaming levels, with the staggered persistent schedule) or 32 (1 CTA
+// / SM, 32 x 32 tiles). 32 rows pay off on levels of 128^2 < n <= 256^2: their
+// 32 x 32 tiles fit one wave at R = 5, so a warp takes 2 PD launches instead of
+// 4 (C3 256^2: 2.39 -> 2.13 ms); elsewhere 16 rows measured better.
+// FSB_PD64_ROWS_L="w:rows,..." overrides per level width; FSB_PD64_PY=2 stacks
+// two pixels per thread on 8 rows.
+int tile_rows(int w, int h) {
+  static const int py2 = [] {
     const char* e = getenv("FSB_PD64_PY");
-    return e && e[0] == '2' && e[1] != 't' ? 8 : 16;
+    return e && e[0] == '2' ? (e[1] == 't' ? 16 : 8) : 0;
   }();
-  return v;
+  if (py2) return py2;
+  const char* e = getenv("FSB_PD64_ROWS_L");
+  for (const char* c = e; c && *c;) {
+    const int lw = atoi(c);
+    const char* colon = strchr(c, ':');
+    if (!colon) break;
+    const int r = atoi(colon + 1);
+    if (lw == w && (r == 16 || r == 32)) return r;
+    c = strchr(colon, ',');
+    if (c) ++c;
+  }
+  const size_t n = (size_t)w * h;
+  return n > 128 * 128 && n <= 256 * 256 ? 32 : 16;
 }
 
 template <int R>
 int launch_r(const B64& A, cudaStream_t st) {
   const bool diag = A.diag_p || A.diag_du || A.diag_du64;
-  if (tile_py() == 2 && tile_rows() == 8)
+  const int rows = tile_rows(A.w, A.h);
+  if (tile_py() == 2 && rows == 8)
     return diag ? launch_tile<R, 2, 8, true>(A, st) : launch_tile<R, 2, 8, false>(A, st);
   if (tile_py() == 2)
     return diag ? launch_tile<R, 2, 16, true>(A, st) : launch_tile<R, 2, 16, false>(A, st);
+  if (rows == 32)
+    return diag ? launch_tile<R, 1, 32, true>(A, st) : launch_tile<R, 1, 32, false>(A, st);
   return diag ? launch_tile<R, 1, 16, true>(A, st) : launch_tile<R, 1, 16, false>(A, st);
 }
 
@@ -383,7 +408,7 @@ int pd64_edge_codes(const uint8_t* mask, int w, int h, uint32_t* code, cudaStrea
 }
 
 size_t pd64_tile_count(int w, int h, int halo) {
-  const int TH = tile_rows() * tile_py();
+  const int TH = tile_rows(w, h) * tile_py();
   const int OW = kW - 2 * halo, OH = TH - 2 * halo;
   return (size_t)((w + OW - 1) / OW) * ((h + OH - 1) / OH);
 }
@@ -393,7 +418,7 @@ int tile_list_internal(const uint8_t* mask, int w, int h, int TW, int TH, int* t
 
 int pd64_tile_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles,
                         cudaStream_t st) {
-  return tile_list_internal(mask, w, h, kW - 2 * halo, tile_rows() * tile_py() - 2 * halo, tiles,
+  return tile_list_internal(mask, w, h, kW - 2 * halo, tile_rows(w, h) * tile_py() - 2 * halo, tiles,
                             st);
 }
 
