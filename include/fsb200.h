@@ -378,7 +378,7 @@ int fsb_graph_create(const fsb_rig* rig, const fsb_params* prm, const float* i0,
                      void* workspace, size_t workspace_bytes, float* u, float* w, float* v,
                      uint8_t* mask, float* i1c, const fsb_diag* diag, void* stream,
                      fsb_graph** graph, int64_t* n_kernels);
-/* The same for the float64 parity path (fsb_solve_pyramid_f64's arguments). */
+/* The same for the float64 path (fsb_solve_pyramid_f64's arguments). */
 int fsb_graph_create_f64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
                          const double* i1, const double* const* traj_dirs,
                          const uint8_t* const* traj_ok, void* workspace, size_t workspace_bytes,

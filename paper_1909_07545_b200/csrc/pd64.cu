@@ -1,12 +1,15 @@
-// fp64 parity path: the whole solve_pyramid frame in float64 storage and
-// arithmetic (compiled with -fmad=false, IEEE division / sqrt, the reference's
-// operation order), one primal-dual cycle per launch.
+// The float64 path — the drop-in default and the credited path: the whole
+// solve_pyramid frame in float64 storage and arithmetic. Geometry, setup and
+// the samplers are compiled with -fmad=false (NumPy's rounding order); the
+// primal-dual cycles run in k64_tile (pd64_tile.cu, FMA contraction, IEEE
+// division / sqrt). The one-cycle-per-launch kernels below (k64_dual /
+// k64_primal / k64_finish) remain as the FSB_PD64=plain cross-check.
 //
-// The fp32 path (TMA-fed temporally blocked kernels) is the production path.
-// At the reference defaults (N=50 warps) the problem is at its conditioning
-// limit: ANY fp32 rounding moves the p99 disparity by ~2e-2 px against the
-// fp64 reference (profiles/r01_precision_study.txt). This path reproduces the
-// reference to round-off at every N, so parity can be shown at N=50 too.
+// Why float64: at the reference defaults (N=50 warps) the problem is at its
+// conditioning limit — ANY float32 rounding of the state or the constants moves
+// the p99 disparity past 1e-2 px against the reference
+// (profiles/r01_precision_study.txt). This path reproduces the
+// reference to round-off at every N (C3: p99 3.3e-6 px).
 //
 // Reference: solver.py:306-452 (solve_level, solve_pyramid) with the stages of
 // solver.py:279-303 and :332-365; rasters.py:57-141 (bicubic).

@@ -1,4 +1,5 @@
-// Temporally blocked primal-dual cycles for the float64 parity path.
+// Temporally blocked primal-dual cycles for the float64 path (round-1 kernel,
+// FSB_PD64K=block; the default is k64_tile, pd64_tile.cu).
 //
 // k64_dual + k64_primal (pd64.cu) run one cycle per launch pair and move the
 // whole fp64 state through HBM twice per cycle. This kernel keeps a 32 x 16

@@ -5,7 +5,7 @@ The renderer (input generator) is checked against the reference's own renders
 GPU-rendered inputs at the sizes the oracle finishes in seconds (C1 at full
 size; C2 geometry at full size), and at the headline 1024^2 size (C3) through
 size-independent invariants, the per-level trajectory fields against the oracle
-and the fp32 path against the fp64 parity path.
+and the fp32 / fp64 paths against the oracle.
 """
 
 import numpy as np
@@ -230,7 +230,7 @@ def test_n50_parity_on_acceptance_geometry():
 
 
 def test_fp64_path_reproduces_oracle_to_roundoff():
-    """The float64 parity path on the golden pair and on C1: disparity and warp
+    """The float64 path on the golden pair and on C1: disparity and warp
     agree with the fp64 oracle to ~1e-9 (same algorithm, same operation order)."""
     import json
     from conftest import load_golden
