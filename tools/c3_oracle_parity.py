@@ -18,7 +18,7 @@ rig = StereoRig(cam, cam, RelativePose.from_displacement((0.08, 0.02, 0.03),
                                                          rotvec=(0.01, 0.03, -0.02)))
 prm = SolverParams()
 i0, i1 = _render_pair(rig, ss=1)
-r32 = solve_pyramid(i0, i1, rig, prm)
+r32 = solve_pyramid(i0, i1, rig, prm, precision="fp32")
 r64 = solve_pyramid(i0, i1, rig, prm, precision="fp64")
 t0 = time.time()
 sol = O.pyramid_solve(i0, i1, rig, prm)

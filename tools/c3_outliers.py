@@ -11,7 +11,7 @@ cam = UnifiedCamera(width=1024, height=1024, fx=455.0, fy=455.0, cx=511.5, cy=51
 rig = StereoRig(cam, cam, RelativePose.from_displacement((0.08, 0.02, 0.03), rotvec=(0.01, 0.03, -0.02)))
 prm = SolverParams()
 i0, i1 = _render_pair(rig, ss=1)
-r32 = solve_pyramid(i0, i1, rig, prm); r64 = solve_pyramid(i0, i1, rig, prm, precision="fp64")
+r32 = solve_pyramid(i0, i1, rig, prm, precision="fp32"); r64 = solve_pyramid(i0, i1, rig, prm, precision="fp64")
 e = np.abs(r32.u - r64.u); e[~r64.mask] = 0
 ys, xs = np.nonzero(e > 1.0)
 print("px > 1:", len(ys), "px > 0.1:", int((e > 0.1).sum()), "of", int(r64.mask.sum()))

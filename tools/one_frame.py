@@ -10,7 +10,7 @@ from paper_1909_07545_b200.solver import Solver
 
 rig, prm, desc, ss = bench.workload(sys.argv[1] if len(sys.argv) > 1 else "c3")
 sc = S.default_scene()
-eng = Solver(rig, prm)
+eng = Solver(rig, prm, precision="fp32")
 eng.i0.copy_(S.render_device(sc, rig.cam0, supersample=ss)[0])
 eng.i1.copy_(S.render_device(sc, rig.cam1, pose=rig.pose, supersample=ss)[0])
 for _ in range(int(sys.argv[2]) if len(sys.argv) > 2 else 2):

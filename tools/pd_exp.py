@@ -8,7 +8,7 @@ from paper_1909_07545_b200 import _dev, _ext, synth as S
 from paper_1909_07545_b200.solver import Solver, _Level
 from paper_1909_07545_b200.fields import trajectory_field_device, translation_only_rig
 rig, prm, desc, ss = bench.workload("c3")
-eng = Solver(rig, prm)
+eng = Solver(rig, prm, precision="fp32")
 sc = S.default_scene()
 i0 = S.render_device(sc, rig.cam0, supersample=ss)[0]
 eng.i0.copy_(i0); eng.i1.copy_(S.render_device(sc, rig.cam1, pose=rig.pose, supersample=ss)[0]); eng.run()
