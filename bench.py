@@ -136,7 +136,8 @@ def config_of(name: str, world: int) -> dict:
            "pixel_iters_per_frame": pixel_iters_per_frame(name),
            "params": params_dict(name),
            "inputs": ("tests/golden/c3_pair.npz (reference synth.render, float32)"
-                      if name == "c3" else "GPU ray-cast default_scene (synth.cu)"),
+                      if name == "c3" else "default_scene render (B200 arm: synth.cu; "
+                      "reference arm: the reference renderer)"),
            "l2": "flushed (256 MiB write) between timed steps",
            "parallelism": f"frame-partitioned x{world}, no data-path collective"}
     return cfg
@@ -311,12 +312,38 @@ def _reference_module():
         return None
 
 
+def reference_pair(name: str):
+    """Input pair of a workload for the CPU arms: C3 from its fixture; other
+    workloads rendered by the reference's own renderer (baseline/_ref), float32."""
+    if name == "c3":
+        return load_c3_pair()
+    mods = _reference_module()
+    if mods is None:
+        raise SystemExit(f"--impl reference --workload {name} needs the reference renderer "
+                         "(tools/install_reference.sh)")
+    camera, _ = mods
+    from fisheyestereo import synth
+    spec = WORKLOADS[name]
+
+    def cam(d):
+        kw = {k: v for k, v in d.items() if k != "model"}
+        return (camera.UnifiedCamera(**kw) if d["model"] == "unified"
+                else camera.PolynomialFisheyeCamera(**kw))
+    c0 = cam(spec["cam0"])
+    c1 = cam(spec["cam1"]) if spec["cam1"] else c0
+    pose = camera.RelativePose.from_displacement(spec["center"], rotvec=spec["rotvec"])
+    sc = synth.default_scene()
+    i0 = synth.render(sc, c0, supersample=spec["ss"])[0]
+    i1 = synth.render(sc, c1, pose=pose, supersample=spec["ss"])[0]
+    return np.asarray(i0, np.float32), np.asarray(i1, np.float32)
+
+
 def _cpu_frame(job) -> float:
     """Worker: solve one whole frame on the host; returns wall seconds.
-    job = (kind, workload name, warp_iters override or None)."""
-    kind, name, n_warps = job
+    job = (kind, workload name, warp_iters override or None, input pair or None)."""
+    kind, name, n_warps, pair = job
     _single_thread_env()
-    i0, i1 = (a.astype(np.float64) for a in load_c3_pair())
+    i0, i1 = (a.astype(np.float64) for a in (pair if pair is not None else load_c3_pair()))
     spec = WORKLOADS[name]
     prm = params_dict(name)
     if n_warps is not None:
@@ -349,18 +376,21 @@ def _cpu_frame(job) -> float:
     return time.perf_counter() - t0
 
 
-def cpu_wave(kind: str, name: str, procs: int, warps=None) -> list:
+def cpu_wave(kind: str, name: str, procs: int, warps=None, pair=None) -> list:
     """One wave of whole-frame CPU solves, one process per core; per-process seconds."""
     import multiprocessing as mp
-    jobs = [(kind, name, warps[i % len(warps)] if warps else None) for i in range(procs)]
+    jobs = [(kind, name, warps[i % len(warps)] if warps else None, pair) for i in range(procs)]
     ctx = mp.get_context("spawn")
     with ctx.Pool(procs) as pool:
         return pool.map(_cpu_frame, jobs, chunksize=1)
 
 
 def cpu_procs() -> int:
-    """All host cores, bounded by memory (a C3 frame peaks below 2 GB per process)."""
-    return max(1, min(cpu_cores(), mem_available_bytes() // (2 << 30)))
+    """All host cores, bounded by memory (a C3 frame peaks below 2 GB per process);
+    FSB_REF_PROCS caps it (tests)."""
+    n = max(1, min(cpu_cores(), mem_available_bytes() // (2 << 30)))
+    cap = os.environ.get("FSB_REF_PROCS")
+    return min(n, max(1, int(cap))) if cap else n
 
 
 def cpu_baseline_sample(name: str) -> dict:
@@ -390,19 +420,21 @@ def run_reference(a) -> None:
     """CPU reference arm: rank 0 only; one wave of whole frames on all host cores."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
-    if a.workload != "c3":
-        raise SystemExit("--impl reference runs the C3 pair (tests/golden/c3_pair.npz)")
+    if a.workload == "c4":
+        raise SystemExit("--impl reference times single frames (c1, c2, c3, c5)")
     kind = "reference" if _reference_module() is not None else "port"
     procs = cpu_procs()
+    pair = None if a.workload == "c3" else reference_pair(a.workload)
     t0 = time.perf_counter()
-    secs = cpu_wave(kind, a.workload, procs)
+    secs = cpu_wave(kind, a.workload, procs, pair=pair)
     wave = time.perf_counter() - t0
     fps = procs / wave
     ppf = pixel_iters_per_frame(a.workload)
     impl = ("fisheyestereo.solve_pyramid, the unmodified reference package "
             "(baseline/_ref)" if kind == "reference" else
             "oracle/fs_oracle.pyramid_solve (pinned port; baseline/_ref absent)")
-    sample = (f"{impl}: one wave of {procs} whole C3 frames, one single-threaded process "
+    sample = (f"{impl}: one wave of {procs} whole {a.workload.upper()} frames, one "
+              f"single-threaded process "
               f"per host core ({cpu_model()}); per-frame {min(secs):.0f}-{max(secs):.0f} s, "
               f"wave {wave:.0f} s. --steps/--warmup are not applied: a frame is minutes "
               f"of NumPy with no warm-up state")
@@ -410,7 +442,7 @@ def run_reference(a) -> None:
     line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
             "n_gpus": world, "steps": 1, "warmup": 0, "ms_per_step": wave * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference-rendered C3 pair, float32 values)",
+            "data": f"synthetic (reference-rendered {a.workload.upper()} pair, float32 values)",
             "config": config_of(a.workload, world),
             "mpix_iter_per_s": fps * ppf / 1e6,
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": procs, "kind": kind,

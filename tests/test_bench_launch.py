@@ -64,3 +64,26 @@ def test_reference_arm_imports_no_product_code():
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                          timeout=120, cwd=ROOT)
     assert out.returncode == 0 and out.stdout.strip() == "ok", out.stderr[-2000:]
+
+
+@pytest.mark.skipif(not (ROOT / "baseline" / "_ref" / "fisheyestereo").exists(),
+                    reason="reference not installed in baseline/_ref")
+def test_reference_arm_line_on_c1():
+    """The reference arm end to end on a small workload (C1, 2 processes): one
+    JSON line with the contract's keys, the unmodified reference as the
+    implementation, the same config object as the B200 arm, and no product
+    package import (the workers run in spawned processes)."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    env = dict(os.environ, FSB_REF_PROCS="2")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                          "--workload", "c1"], capture_output=True, text=True, timeout=900,
+                         env=env, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["unit"] == "frames/s" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] == 2
+    assert d["config"] == bench.config_of("c1", 1)
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
