@@ -17,6 +17,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <vector>
+
 #include "pd_math.cuh"
 #include "pd64_block.cuh"
 
@@ -59,6 +61,7 @@ int pack64_internal(const double* i1, const uint8_t* mask, const double* traj,
                     const uint8_t* tok, int h, int w, double4* tex, cudaStream_t st);
 int sample_nan64_internal(const P64& L, int bx, int by, cudaStream_t st);
 int linearize_nan64_internal(const P64& L, int bx, int by, cudaStream_t st);
+bool side_stream_for(cudaStream_t main, cudaStream_t* side, cudaEvent_t** ev);  // solver.cu
 
 }  // namespace fsb
 
@@ -400,12 +403,15 @@ struct Plan64 {
   uint8_t *lvl_mask[kMaxLevels], *traj_ok[kMaxLevels];
   void* traj_scratch; size_t traj_bytes;
   void* setup_scratch; size_t setup_bytes;
-  double *T, *S, *u[2], *wv[2], *ub, *v, *vb, *p, *q, *uo, *iu, *rho0, *i1w, *dirs, *partials;
+  double *u[2], *wv[2], *ub, *v, *vb, *p, *q, *uo, *iu, *rho0, *i1w, *dirs, *partials;
   double *u2, *ub2, *v2, *vb2, *p2, *q2;
-  uint8_t *i1w_ok, *dir_ok, *full16;
-  uint32_t* ecode;
-  int* tiles;
-  double4* tex;
+  uint8_t *i1w_ok, *dir_ok;
+  // per-level setup products (filled ahead on the side stream)
+  double *Tl[kMaxLevels], *Sl[kMaxLevels];
+  uint8_t* f16l[kMaxLevels];
+  uint32_t* ecl[kMaxLevels];
+  int* tll[kMaxLevels];
+  double4* texl[kMaxLevels];
   size_t bytes;
 };
 
@@ -439,7 +445,6 @@ int plan64(const fsb_rig* rig, const fsb_params* prm, void* base, Plan64& P) {
   P.traj_scratch = c.take<char>(P.traj_bytes);
   P.setup_bytes = level_setup_scratch_internal(H, W);
   P.setup_scratch = c.take<char>(P.setup_bytes);
-  P.T = c.take<double>(3 * n0); P.S = c.take<double>(3 * n0);
   for (int k = 0; k < 2; ++k) { P.u[k] = c.take<double>(n0); P.wv[k] = c.take<double>(2 * n0); }
   P.ub = c.take<double>(n0); P.v = c.take<double>(2 * n0); P.vb = c.take<double>(2 * n0);
   P.p = c.take<double>(2 * n0); P.q = c.take<double>(4 * n0);
@@ -450,10 +455,13 @@ int plan64(const fsb_rig* rig, const fsb_params* prm, void* base, Plan64& P) {
   P.u2 = c.take<double>(n0); P.ub2 = c.take<double>(n0);
   P.v2 = c.take<double>(2 * n0); P.vb2 = c.take<double>(2 * n0);
   P.p2 = c.take<double>(2 * n0); P.q2 = c.take<double>(4 * n0);
-  P.full16 = c.take<uint8_t>(n0);
-  P.ecode = c.take<uint32_t>(n0);
-  P.tex = c.take<double4>(n0);
-  P.tiles = c.take<int>(partial_count(H, W) + 1);
+  for (int l = 0; l < n; ++l) {
+    const int lh = P.shapes[2 * l], lw = P.shapes[2 * l + 1];
+    const size_t np = (size_t)lh * lw;
+    P.Tl[l] = c.take<double>(3 * np); P.Sl[l] = c.take<double>(3 * np);
+    P.f16l[l] = c.take<uint8_t>(np); P.ecl[l] = c.take<uint32_t>(np);
+    P.tll[l] = c.take<int>(partial_count(lh, lw) + 1); P.texl[l] = c.take<double4>(np);
+  }
   P.bytes = c.off;
   return FSB_OK;
 }
@@ -536,14 +544,87 @@ L64 swapped(const L64& L) {
   return o;
 }
 
-int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, int64_t pd_off,
-                  int64_t warp_off, void* scratch, size_t scratch_bytes, cudaStream_t st,
-                  fsb_phase_timer* tm = nullptr) {
-  L64 L = L0;  // L's state pointers follow the ping-pong of the blocked cycles
-  const size_t n = L.n;
+// Per-level kernel configuration (deterministic from the level size and the
+// tuning environment, so the side-stream setup and the solve agree).
+struct LevelCfg64 {
+  int halo, kern;
+  bool listed, pro_nan;
+};
+
+LevelCfg64 level_cfg64(const L64& L) {
+  LevelCfg64 c;
+  // latency-bound small levels: 5 cycles per launch when those tiles fit
+  // two resident CTAs per SM (C3: 64^2, 128^2), else R = 2 (throughput)
+  int halo = L.u2 ? pd64_halo() : 0;
+  if (halo == 2 && getenv("FSB_PD64") == nullptr) {
+    if (pd64_tile_count(L.w, L.h, 5) <= 2 * 148) halo = 5;
+    else if (pd64_tile_count(L.w, L.h, 3) <= 2 * 148) halo = 3;
+  }
+  if (halo > 0) {  // FSB_PD64_HALO_L="w:R,w:R" overrides per level width (tuning)
+    const char* e = getenv("FSB_PD64_HALO_L");
+    for (const char* p = e; p && *p;) {
+      const int lw = atoi(p);
+      const char* colon = strchr(p, ':');
+      if (!colon) break;
+      const int r = atoi(colon + 1);
+      if (lw == L.w && (r == 1 || r == 2 || r == 3 || r == 5)) halo = r;
+      p = strchr(colon, ',');
+      if (p) ++p;
+    }
+  }
+  c.halo = halo;
+  c.kern = halo > 0 ? pd64_kernel_for(halo) : -1;
+  c.listed = c.kern == K64_TILEL;
+  // Warp prologue: the NaN-encoded texel kernels (sample64.cu) on levels up to
+  // 256^2, where the masked-gather chains of k64_sample / k64_linearize are
+  // latency floors (C3: 64^2 -0.18 ms, 128^2 -0.34 ms per frame); on larger
+  // levels the 32-byte texels cost more DRAM traffic than they save
+  // (1024^2 +0.8 ms). FSB_PRO64=old / new forces one kind everywhere.
+  static const int pro_mode = [] {
+    const char* e = getenv("FSB_PRO64");
+    return e && strcmp(e, "old") == 0 ? 0 : (e && strcmp(e, "new") == 0 ? 2 : 1);
+  }();
+  c.pro_nan =
+      halo > 0 && (pro_mode == 2 || (pro_mode == 1 && (size_t)L.w * L.h <= 256 * 256));
+  return c;
+}
+
+// Level setup that depends only on the pyramid and the rig (solver.py:319-321
+// and the gather / tile tables): runs ahead on the side stream.
+int level_prepare64(const L64& L, const fsb_params* prm, const LevelCfg64& c, void* scratch,
+                    size_t scratch_bytes, cudaStream_t st) {
   int rc = level_setup64_internal(L.i0, L.mask, L.h, L.w, prm, L.T, L.S, scratch, scratch_bytes,
                                   st);
   if (rc) return rc;
+  if (c.listed) {  // per-level edge codes and tile work list
+    rc = pd64_edge_codes(L.mask, L.w, L.h, L.ecode, st);
+    if (rc) return rc;
+    rc = pd64_tile_tile_list(L.mask, L.w, L.h, c.halo, L.tiles, st);
+    if (rc) return rc;
+  }
+  if (c.pro_nan) {
+    rc = pack64_internal(L.i1, L.mask, L.traj, L.traj_ok, L.h, L.w, L.tex, st);
+    if (rc) return rc;
+  } else if (L.full16) {  // all-16-taps-valid flags of the masked-gather sampler
+    dim3 b(kBX, kBY);
+    k64_full16<<<grid2d(L.w, L.h, b), b, 0, st>>>(L);
+  }
+  return launch_status();
+}
+
+int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, int64_t pd_off,
+                  int64_t warp_off, void* scratch, size_t scratch_bytes, cudaStream_t st,
+                  fsb_phase_timer* tm = nullptr, bool prepared = false) {
+  L64 L = L0;  // L's state pointers follow the ping-pong of the blocked cycles
+  const size_t n = L.n;
+  const LevelCfg64 cfg = level_cfg64(L);
+  const int halo = cfg.halo, kern = cfg.kern;
+  const bool listed = cfg.listed, pro_nan = cfg.pro_nan;
+  int rc = FSB_OK;
+  if (!prepared) {
+    rc = level_prepare64(L, prm, cfg, scratch, scratch_bytes, st);
+    if (rc) return rc;
+  }
   cudaMemsetAsync(L.v, 0, 2 * n * sizeof(double), st);
   cudaMemsetAsync(L.vb, 0, 2 * n * sizeof(double), st);
   cudaMemsetAsync(L.p, 0, 2 * n * sizeof(double), st);
@@ -561,54 +642,9 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
   dim3 blk(kBX, kBY), grd = grid2d(L.w, L.h, blk);
   const bool dpq = diag && diag->max_p_norm && diag->max_q_norm;
   const bool ddu = diag && (diag->max_du || diag->max_du_f64) && diag->mean_abs_du;
-  // latency-bound small levels: 5 cycles per launch when those tiles fit
-  // two resident CTAs per SM (C3: 64^2, 128^2), else R = 2 (throughput)
-  int halo = L.u2 ? pd64_halo() : 0;
-  if (halo == 2 && getenv("FSB_PD64") == nullptr) {
-    if (pd64_tile_count(L.w, L.h, 5) <= 2 * 148) halo = 5;
-    else if (pd64_tile_count(L.w, L.h, 3) <= 2 * 148) halo = 3;
-  }
-  if (halo > 0) {  // FSB_PD64_HALO_L="w:R,w:R" overrides per level width (tuning)
-    const char* e = getenv("FSB_PD64_HALO_L");
-    for (const char* c = e; c && *c;) {
-      const int lw = atoi(c);
-      const char* colon = strchr(c, ':');
-      if (!colon) break;
-      const int r = atoi(colon + 1);
-      if (lw == L.w && (r == 1 || r == 2 || r == 3 || r == 5)) halo = r;
-      c = strchr(colon, ',');
-      if (c) ++c;
-    }
-  }
-  const int kern = halo > 0 ? pd64_kernel_for(halo) : -1;
-  const bool listed = kern == K64_TILEL;
-  if (listed) {  // per-level edge codes and tile work list
-    rc = pd64_edge_codes(L.mask, L.w, L.h, L.ecode, st);
-    if (rc) return rc;
-    rc = pd64_tile_tile_list(L.mask, L.w, L.h, halo, L.tiles, st);
-    if (rc) return rc;
-  }
-  // Warp prologue: the NaN-encoded texel kernels (sample64.cu) on levels up to
-  // 256^2, where the masked-gather chains of k64_sample / k64_linearize are
-  // latency floors (C3: 64^2 -0.18 ms, 128^2 -0.34 ms per frame); on larger
-  // levels the 32-byte texels cost more DRAM traffic than they save
-  // (1024^2 +0.8 ms). FSB_PRO64=old / new forces one kind everywhere.
-  static const int pro_mode = [] {
-    const char* e = getenv("FSB_PRO64");
-    return e && strcmp(e, "old") == 0 ? 0 : (e && strcmp(e, "new") == 0 ? 2 : 1);
-  }();
-  const bool pro_nan =
-      halo > 0 && (pro_mode == 2 || (pro_mode == 1 && (size_t)L.w * L.h <= 256 * 256));
   P64 PL;
   PL.h = L.h; PL.w = L.w; PL.i0 = L.i0; PL.mask = L.mask; PL.tex = L.tex; PL.wv = L.wv;
   PL.i1wn = L.i1w; PL.dirs = L.dirs; PL.dir_ok = L.dir_ok; PL.iu = L.iu; PL.rho0 = L.rho0;
-  if (pro_nan) {
-    rc = pack64_internal(L.i1, L.mask, L.traj, L.traj_ok, L.h, L.w, L.tex, st);
-    if (rc) return rc;
-  } else if (L.full16) {  // all-16-taps-valid flags of the masked-gather sampler
-    dim3 b(kBX, kBY);
-    k64_full16<<<grid2d(L.w, L.h, b), b, 0, st>>>(L);
-  }
   for (int wi = 0; wi < N; ++wi) {
     const bool timed = tm && wi < tm->cap;
     if (timed) cudaEventRecord(tm->ev[3 * wi], st);
@@ -745,6 +781,29 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
     if (diag->max_du) cudaMemsetAsync(diag->max_du, 0, nw * sizeof(float), st);
     if (diag->max_du_f64) cudaMemsetAsync(diag->max_du_f64, 0, nw * sizeof(double), st);
   }
+  // Side stream (shared with the float32 driver, solver.cu side_ctx): the
+  // trajectory fields of every level (rig only) start there at once; after the
+  // pyramids, every level's setup runs there coarse to fine with one event per
+  // level, which the level's solve on the caller's stream waits for. The small
+  // levels leave most SMs idle, so the finer levels' setup fills them.
+  // FSB_OVERLAP=0 keeps everything on the caller's stream.
+  cudaStream_t ss = st;
+  cudaEvent_t* ev = nullptr;
+  const bool side = !tm && side_stream_for(st, &ss, &ev);
+  if (!side) ss = st;
+  if (side) {
+    cudaEventRecord(ev[0], st);
+    cudaStreamWaitEvent(ss, ev[0], 0);
+  }
+  if (!traj_dirs) {
+    for (int l = P.nlev - 1; l >= 0; --l) {
+      const int h = P.shapes[2 * l], w = P.shapes[2 * l + 1];
+      fsb_camera cl = scaled(r.cam0, h, w);
+      rc = trajectory_field64_internal(&cl, t_res, prm->epsilon_scale, 1.0, P.traj[l],
+                                       P.traj_ok[l], P.traj_scratch, P.traj_bytes, ss);
+      if (rc) return rc;
+    }
+  }
   rc = fov_mask_internal(&r.cam0, P.mask0, P.iters + 0, st);
   if (rc) return rc;
   rc = fov_mask_internal(&r.cam1, P.mask1, P.iters + 1, st);
@@ -765,6 +824,34 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
                                P.lvl_mask[l], ch, cw, st);
     if (rc) return rc;
   }
+  // the level views (coarse -> fine index k) and their setup, on the side stream
+  std::vector<L64> lv(P.nlev);
+  for (int k = 0; k < P.nlev; ++k) {
+    const int l = P.nlev - 1 - k;
+    const int h = P.shapes[2 * l], w = P.shapes[2 * l + 1];
+    L64& L = lv[k];
+    memset(&L, 0, sizeof(L));
+    L.h = h; L.w = w; L.n = (size_t)h * w;
+    L.i0 = P.lvl_i0[l]; L.i1 = P.lvl_i1[l]; L.mask = P.lvl_mask[l];
+    L.traj = traj_dirs ? traj_dirs[k] : P.traj[l];
+    L.traj_ok = traj_dirs ? traj_okv[k] : P.traj_ok[l];
+    L.T = P.Tl[l]; L.S = P.Sl[l];
+    L.ub = P.ub; L.v = P.v; L.vb = P.vb; L.p = P.p; L.q = P.q;
+    L.u2 = P.u2; L.ub2 = P.ub2; L.v2 = P.v2; L.vb2 = P.vb2; L.p2 = P.p2; L.q2 = P.q2;
+    L.full16 = P.f16l[l];
+    L.ecode = P.ecl[l]; L.tiles = P.tll[l]; L.tex = P.texl[l];
+    L.uo = P.uo; L.iu = P.iu; L.rho0 = P.rho0; L.i1w = P.i1w; L.i1w_ok = P.i1w_ok;
+    L.dirs = P.dirs; L.dir_ok = P.dir_ok; L.partials = P.partials;
+  }
+  if (side) {
+    cudaEventRecord(ev[kMaxLevels + 1], st);  // pyramids done
+    cudaStreamWaitEvent(ss, ev[kMaxLevels + 1], 0);
+    for (int k = 0; k < P.nlev; ++k) {
+      rc = level_prepare64(lv[k], prm, level_cfg64(lv[k]), P.setup_scratch, P.setup_bytes, ss);
+      if (rc) return rc;
+      cudaEventRecord(ev[1 + k], ss);
+    }
+  }
   int64_t pd_off = 0, warp_off = 0;
   int cur = 0, prev_h = 0, prev_w = 0;
   const uint8_t* prev_mask = nullptr;
@@ -773,19 +860,6 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
     const int h = P.shapes[2 * l], w = P.shapes[2 * l + 1];
     const size_t np = (size_t)h * w;
     const LevelRange nvtx_range("fsb64 level %dx%d", w, h);  // NVTX range per level
-    const double* traj;
-    const uint8_t* tok;
-    if (traj_dirs) {
-      traj = traj_dirs[k];
-      tok = traj_okv[k];
-    } else {
-      fsb_camera cl = scaled(r.cam0, h, w);
-      rc = trajectory_field64_internal(&cl, t_res, prm->epsilon_scale, 1.0, P.traj[l],
-                                       P.traj_ok[l], P.traj_scratch, P.traj_bytes, st);
-      if (rc) return rc;
-      traj = P.traj[l];
-      tok = P.traj_ok[l];
-    }
     double* u = P.u[cur];
     double* wv = P.wv[cur];
     if (k == 0) {
@@ -796,19 +870,12 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
                                P.lvl_mask[l], h, w, u, wv, st);
       if (rc) return rc;
     }
-    L64 L;
-    L.h = h; L.w = w; L.n = np;
-    L.i0 = P.lvl_i0[l]; L.i1 = P.lvl_i1[l]; L.mask = P.lvl_mask[l];
-    L.traj = traj; L.traj_ok = tok;
-    L.T = P.T; L.S = P.S;
-    L.u = u; L.ub = P.ub; L.v = P.v; L.vb = P.vb; L.p = P.p; L.q = P.q;
-    L.u2 = P.u2; L.ub2 = P.ub2; L.v2 = P.v2; L.vb2 = P.vb2; L.p2 = P.p2; L.q2 = P.q2;
-    L.full16 = P.full16;
-    L.ecode = P.ecode; L.tiles = P.tiles; L.tex = P.tex;
-    L.wv = wv; L.uo = P.uo; L.iu = P.iu; L.rho0 = P.rho0; L.i1w = P.i1w; L.i1w_ok = P.i1w_ok;
-    L.dirs = P.dirs; L.dir_ok = P.dir_ok; L.partials = P.partials;
+    L64 L = lv[k];
+    L.u = u;
+    L.wv = wv;
+    if (side) cudaStreamWaitEvent(st, ev[1 + k], 0);  // join: this level's setup done
     rc = solve_level64(L, prm, diag, pd_off, warp_off, P.setup_scratch, P.setup_bytes, st,
-                       tm && tm->level == l ? tm : nullptr);
+                       tm && tm->level == l ? tm : nullptr, side);
     if (rc) return rc;
     pd_off += (int64_t)N * K;
     warp_off += N;

@@ -504,6 +504,16 @@ SideCtx* side_ctx(cudaStream_t main) {
 
 }  // namespace
 
+// The caller stream's side stream and its events (kMaxLevels + 2), for the
+// float64 driver (pd64.cu); false when FSB_OVERLAP=0 or on failure.
+bool side_stream_for(cudaStream_t main, cudaStream_t* side, cudaEvent_t** ev) {
+  SideCtx* c = side_ctx(main);
+  if (!c) return false;
+  *side = c->side;
+  *ev = c->ev;
+  return true;
+}
+
 int solve_pyramid_internal(const fsb_rig* rig, const fsb_params* prm, const float* i0,
                            const float* i1, const float* const* traj_dirs,
                            const uint8_t* const* traj_okv, void* ws, size_t ws_bytes, float* u_out,

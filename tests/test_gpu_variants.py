@@ -3,6 +3,7 @@ process, so every variant runs in a child process on the golden pair and on a
 C1 frame): the default (k64_tile over the per-level work list, phase-staggered
 persistent schedule, NaN-texel prologue on small levels) against
   * the non-persistent schedule (FSB_PD64_PERSIST=0)      -> bit-identical,
+  * per-level setup on the caller's stream (FSB_OVERLAP=0) -> bit-identical,
   * k64_tile over every tile with masked loads (FSB_PD64K=tile) -> bit-identical,
   * the masked-gather prologue everywhere (FSB_PRO64=old) -> <= 1e-10 px,
   * the round-1 k64_block, no FMA (FSB_PD64K=block)       -> <= 1e-8 px.
@@ -49,6 +50,7 @@ def _run(tmp_path, name, env_extra):
 
 @pytest.mark.parametrize("name,env,tol", [
     ("persist0", {"FSB_PD64_PERSIST": "0"}, 0.0),
+    ("no_overlap", {"FSB_OVERLAP": "0"}, 0.0),
     ("alltiles", {"FSB_PD64K": "tile"}, 0.0),
     ("prologue_old", {"FSB_PRO64": "old"}, 1e-10),
     ("block", {"FSB_PD64K": "block"}, 1e-8),
