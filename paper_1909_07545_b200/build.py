@@ -41,6 +41,8 @@ UNITS = [
     ("pd64.cu", ["-fmad=false"]),
     ("pd64_block.cu", ["-fmad=false"]),
     ("pd64_tile.cu", []),
+    ("pd64_tma.cu", []),
+    ("pd64_ctile.cu", []),
     ("sample64.cu", ["-fmad=false"]),
     ("solver.cu", []),
     ("synth.cu", ["-fmad=false"]),

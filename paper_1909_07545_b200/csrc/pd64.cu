@@ -403,11 +403,16 @@ struct Plan64 {
   uint8_t *lvl_mask[kMaxLevels], *traj_ok[kMaxLevels];
   void* traj_scratch; size_t traj_bytes;
   void* setup_scratch; size_t setup_bytes;
-  double *u[2], *wv[2], *ub, *v, *vb, *p, *q, *uo, *iu, *rho0, *i1w, *dirs, *partials;
-  double *u2, *ub2, *v2, *vb2, *p2, *q2;
+  // the two primal-dual state sets, each one block of 12 planes of the level's
+  // size (u, v x2, p x2, q x4, u_bar, v_bar x2: the 3-D TMA box of k64_tma)
+  double *setA, *setB;
+  double* carry_u;  // the finished level's u, read by the next level's upsample
+  double *wv[2], *i1w, *dirs, *partials;
   uint8_t *i1w_ok, *dir_ok;
-  // per-level setup products (filled ahead on the side stream)
-  double *Tl[kMaxLevels], *Sl[kMaxLevels];
+  // per-level setup products (filled ahead on the side stream); cst: one block
+  // of 10 planes per level — tensor a, b, c, steps sigma_p, tau_u, tau_v, I_u,
+  // rho0, u_omega, edge code (k64_tma's constant box)
+  double* cst[kMaxLevels];
   uint8_t* f16l[kMaxLevels];
   uint32_t* ecl[kMaxLevels];
   int* tll[kMaxLevels];
@@ -417,7 +422,8 @@ struct Plan64 {
 
 size_t partial_count(int h, int w) {  // k64_finish blocks or blocked-kernel tiles (halo <= 5)
   const size_t blocks = (size_t)((w + kBX - 1) / kBX) * ((h + kBY - 1) / kBY);
-  const size_t tiles = pd64_block_tiles(w, h, 5);
+  size_t tiles = pd64_block_tiles(w, h, 5);
+  if (pd64_ctile_partials(w, h) > tiles) tiles = pd64_ctile_partials(w, h);
   return (blocks > tiles ? blocks : tiles) + 64;
 }
 
@@ -445,20 +451,16 @@ int plan64(const fsb_rig* rig, const fsb_params* prm, void* base, Plan64& P) {
   P.traj_scratch = c.take<char>(P.traj_bytes);
   P.setup_bytes = level_setup_scratch_internal(H, W);
   P.setup_scratch = c.take<char>(P.setup_bytes);
-  for (int k = 0; k < 2; ++k) { P.u[k] = c.take<double>(n0); P.wv[k] = c.take<double>(2 * n0); }
-  P.ub = c.take<double>(n0); P.v = c.take<double>(2 * n0); P.vb = c.take<double>(2 * n0);
-  P.p = c.take<double>(2 * n0); P.q = c.take<double>(4 * n0);
-  P.uo = c.take<double>(n0); P.iu = c.take<double>(n0); P.rho0 = c.take<double>(n0);
+  for (int k = 0; k < 2; ++k) P.wv[k] = c.take<double>(2 * n0);
+  P.setA = c.take<double>(12 * n0); P.setB = c.take<double>(12 * n0);
+  P.carry_u = c.take<double>(n0);
   P.i1w = c.take<double>(n0); P.dirs = c.take<double>(2 * n0);
   P.i1w_ok = c.take<uint8_t>(n0); P.dir_ok = c.take<uint8_t>(n0);
   P.partials = c.take<double>(partial_count(H, W));
-  P.u2 = c.take<double>(n0); P.ub2 = c.take<double>(n0);
-  P.v2 = c.take<double>(2 * n0); P.vb2 = c.take<double>(2 * n0);
-  P.p2 = c.take<double>(2 * n0); P.q2 = c.take<double>(4 * n0);
   for (int l = 0; l < n; ++l) {
     const int lh = P.shapes[2 * l], lw = P.shapes[2 * l + 1];
     const size_t np = (size_t)lh * lw;
-    P.Tl[l] = c.take<double>(3 * np); P.Sl[l] = c.take<double>(3 * np);
+    P.cst[l] = c.take<double>(10 * np);
     P.f16l[l] = c.take<uint8_t>(np); P.ecl[l] = c.take<uint32_t>(np);
     P.tll[l] = c.take<int>(partial_count(lh, lw) + 1); P.texl[l] = c.take<double4>(np);
   }
@@ -479,20 +481,28 @@ fsb_camera scaled(const fsb_camera& c, int h, int w) {  // camera.py:66-77
 // FSB_PD64=plain runs the one-cycle-per-launch kernels (reference for the
 // blocked kernel in tests/tools); default: blocked, halo 2.
 // Blocked PD kernel choice. Default: k64_tile over the level's work list of
-// mask tiles (K64_TILEL). FSB_PD64K=tile: k64_tile over every tile (masked
-// gathers, no work list); =block: the round-1 k64_block (pd64_block.cu). The
-// persistent cp.async-pipelined variants measured slower.
-enum { K64_BLOCK = 0, K64_TILE = 1, K64_TILEL = 3 };
+// mask tiles (K64_TILEL), and on the halo-2 levels whose layout allows it the
+// TMA-fed k64_tma (K64_TMA, pd64_tma.cu) over the same list. FSB_PD64K=tilel:
+// k64_tile everywhere; =tile: k64_tile over every tile (masked gathers, no work
+// list); =block: the round-1 k64_block (pd64_block.cu). The persistent
+// cp.async-pipelined variants measured slower.
+enum { K64_BLOCK = 0, K64_TILE = 1, K64_TILEL = 3, K64_TMA = 4, K64_CTILE = 5 };
 int pd64_kernel_choice() {
   static const int v = [] {
     const char* e = getenv("FSB_PD64K");
     if (e && strcmp(e, "block") == 0) return (int)K64_BLOCK;
     if (e && strcmp(e, "tile") == 0) return (int)K64_TILE;
-    return (int)K64_TILEL;
+    if (e && strcmp(e, "tilel") == 0) return (int)K64_TILEL;
+    if (e && strcmp(e, "tma") == 0) return (int)K64_TMA;
+    return (int)K64_CTILE;
   }();
   return v;
 }
-int pd64_kernel_for(int) { return pd64_kernel_choice(); }
+int pd64_kernel_for(int) {
+  const int k = pd64_kernel_choice();
+  // k64_tma / k64_ctile are picked per level (level_cfg64)
+  return k == K64_TMA || k == K64_CTILE ? (int)K64_TILEL : k;
+}
 // Persistent, phase-staggered k64_tile on the halo-2 (large) levels: 2 CTAs per
 // SM stride over the work list and the second half starts 2 us late, so an SM's
 // two CTAs keep opposite phases (C3 1024^2: 16.5 -> 15.9 ms). The small levels
@@ -551,6 +561,20 @@ struct LevelCfg64 {
   bool listed, pro_nan;
 };
 
+// k64_tma's layout: each state set and the constants one block of planes
+// (pd64_block.cuh)
+bool tma_layout64(const L64& L) {
+  const size_t n = L.n;
+  auto set_ok = [n](const double* u, const double* v, const double* p, const double* q,
+                    const double* ub, const double* vb) {
+    return u && v == u + n && p == u + 3 * n && q == u + 5 * n && ub == u + 9 * n &&
+           vb == u + 10 * n;
+  };
+  return set_ok(L.u, L.v, L.p, L.q, L.ub, L.vb) && set_ok(L.u2, L.v2, L.p2, L.q2, L.ub2, L.vb2) &&
+         L.T && L.S == L.T + 3 * n && L.iu == L.T + 6 * n && L.rho0 == L.T + 7 * n &&
+         L.uo == L.T + 8 * n;
+}
+
 LevelCfg64 level_cfg64(const L64& L) {
   LevelCfg64 c;
   // latency-bound small levels: 5 cycles per launch when those tiles fit
@@ -574,7 +598,23 @@ LevelCfg64 level_cfg64(const L64& L) {
   }
   c.halo = halo;
   c.kern = halo > 0 ? pd64_kernel_for(halo) : -1;
-  c.listed = c.kern == K64_TILEL;
+  // k64_ctile on levels above 512^2 (C3 1024^2: 16.0 -> 14.4 ms per frame); at
+  // 512^2 it measured level with k64_tile. FSB_CTILE_MIN=<pixels> moves the cut.
+  static const size_t ctile_min = [] {
+    const char* e = getenv("FSB_CTILE_MIN");
+    return e ? (size_t)atoll(e) : (size_t)512 * 512 + 1;
+  }();
+  const int choice = pd64_kernel_choice();
+  if (c.kern == K64_TILEL && halo == 2 && choice == K64_CTILE && tma_layout64(L) &&
+      (size_t)L.w * L.h >= ctile_min && pd64_ctile_usable(L.w, L.h)) {
+    c.kern = K64_CTILE;
+    c.halo = pd64_ctile_halo();
+  } else if (c.kern == K64_TILEL && halo == 2 && choice == K64_TMA && tma_layout64(L) &&
+             pd64_tma_usable(L.w, L.h) &&
+             pd64_tma_tile_count(L.w, L.h) == pd64_tile_count(L.w, L.h, 2)) {
+    c.kern = K64_TMA;
+  }
+  c.listed = c.kern == K64_TILEL || c.kern == K64_TMA || c.kern == K64_CTILE;
   // Warp prologue: the NaN-encoded texel kernels (sample64.cu) on levels up to
   // 256^2, where the masked-gather chains of k64_sample / k64_linearize are
   // latency floors (C3: 64^2 -0.18 ms, 128^2 -0.34 ms per frame); on larger
@@ -597,9 +637,13 @@ int level_prepare64(const L64& L, const fsb_params* prm, const LevelCfg64& c, vo
                                   st);
   if (rc) return rc;
   if (c.listed) {  // per-level edge codes and tile work list
-    rc = pd64_edge_codes(L.mask, L.w, L.h, L.ecode, st);
+    // k64_tma / k64_ctile: edge codes also as the 10th constant plane
+    const bool tma = c.kern == K64_TMA || c.kern == K64_CTILE;
+    rc = pd64_edge_codes(L.mask, L.w, L.h, L.ecode, tma ? L.T + 9 * L.n : nullptr, st);
     if (rc) return rc;
-    rc = pd64_tile_tile_list(L.mask, L.w, L.h, c.halo, L.tiles, st);
+    if (c.kern == K64_CTILE) rc = pd64_ctile_list(L.mask, L.w, L.h, L.tiles, st);
+    else if (c.kern == K64_TMA) rc = pd64_tma_tile_list(L.mask, L.w, L.h, L.tiles, st);
+    else rc = pd64_tile_tile_list(L.mask, L.w, L.h, c.halo, L.tiles, st);
     if (rc) return rc;
   }
   if (c.pro_nan) {
@@ -642,6 +686,15 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
   dim3 blk(kBX, kBY), grd = grid2d(L.w, L.h, blk);
   const bool dpq = diag && diag->max_p_norm && diag->max_q_norm;
   const bool ddu = diag && (diag->max_du || diag->max_du_f64) && diag->mean_abs_du;
+  Tma64Level tmaps;  // k64_tma's / k64_ctile's tensor maps: set 0 = L0's primary set
+  Ctile64Maps cmaps;
+  if (kern == K64_TMA && !pd64_tma_level_maps(&tmaps, L0.u, L0.u2, L0.T, L0.w, L0.h))
+    return FSB_EINVAL;
+  if (kern == K64_CTILE && !pd64_ctile_maps(&cmaps, L0.u, L0.u2, L0.T, L0.w, L0.h))
+    return FSB_EINVAL;
+  // per-tile partial sums of |du| (DIAG): count of the kernel's tile / CTA slots
+  const size_t nparts =
+      kern == K64_CTILE ? pd64_ctile_partials(L.w, L.h) : pd64_tiles(L.w, L.h, halo);
   P64 PL;
   PL.h = L.h; PL.w = L.w; PL.i0 = L.i0; PL.mask = L.mask; PL.tex = L.tex; PL.wv = L.wv;
   PL.i1wn = L.i1w; PL.dirs = L.dirs; PL.dir_ok = L.dir_ok; PL.iu = L.iu; PL.rho0 = L.rho0;
@@ -683,14 +736,17 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
       A.tiles = listed ? L.tiles : nullptr;
       A.persist = pd64_persist(halo);
       if (listed && (A.diag_du || A.diag_du64))  // tiles off the work list keep a zero partial sum
-        cudaMemsetAsync(L.partials, 0, pd64_tiles(L.w, L.h, halo) * sizeof(double), st);
-      rc = pd64_launch(A, halo, st);
+        cudaMemsetAsync(L.partials, 0, nparts * sizeof(double), st);
+      const int src = L.u == L0.u ? 0 : 1;
+      rc = kern == K64_CTILE ? pd64_ctile_launch(A, cmaps, src, st)
+           : kern == K64_TMA ? pd64_tma_launch(A, tmaps, src, st)
+                             : pd64_launch(A, halo, st);
       if (rc) return rc;
       ++pd_launches;
       L = swapped(L);
       k += it;
       if (k == K && ddu) {
-        rc = mean_finish_internal(L.partials, (int)pd64_tiles(L.w, L.h, halo), L.mask, n,
+        rc = mean_finish_internal(L.partials, (int)nparts, L.mask, n,
                                   diag->mean_abs_du + warp_off + wi, st);
         if (rc) return rc;
       }
@@ -835,12 +891,16 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
     L.i0 = P.lvl_i0[l]; L.i1 = P.lvl_i1[l]; L.mask = P.lvl_mask[l];
     L.traj = traj_dirs ? traj_dirs[k] : P.traj[l];
     L.traj_ok = traj_dirs ? traj_okv[k] : P.traj_ok[l];
-    L.T = P.Tl[l]; L.S = P.Sl[l];
-    L.ub = P.ub; L.v = P.v; L.vb = P.vb; L.p = P.p; L.q = P.q;
-    L.u2 = P.u2; L.ub2 = P.ub2; L.v2 = P.v2; L.vb2 = P.vb2; L.p2 = P.p2; L.q2 = P.q2;
+    const size_t np = L.n;
+    L.T = P.cst[l]; L.S = P.cst[l] + 3 * np;
+    L.iu = P.cst[l] + 6 * np; L.rho0 = P.cst[l] + 7 * np; L.uo = P.cst[l] + 8 * np;
+    L.u = P.setA; L.v = P.setA + np; L.p = P.setA + 3 * np; L.q = P.setA + 5 * np;
+    L.ub = P.setA + 9 * np; L.vb = P.setA + 10 * np;
+    L.u2 = P.setB; L.v2 = P.setB + np; L.p2 = P.setB + 3 * np; L.q2 = P.setB + 5 * np;
+    L.ub2 = P.setB + 9 * np; L.vb2 = P.setB + 10 * np;
     L.full16 = P.f16l[l];
     L.ecode = P.ecl[l]; L.tiles = P.tll[l]; L.tex = P.texl[l];
-    L.uo = P.uo; L.iu = P.iu; L.rho0 = P.rho0; L.i1w = P.i1w; L.i1w_ok = P.i1w_ok;
+    L.i1w = P.i1w; L.i1w_ok = P.i1w_ok;
     L.dirs = P.dirs; L.dir_ok = P.dir_ok; L.partials = P.partials;
   }
   if (side) {
@@ -860,18 +920,17 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
     const int h = P.shapes[2 * l], w = P.shapes[2 * l + 1];
     const size_t np = (size_t)h * w;
     const LevelRange nvtx_range("fsb64 level %dx%d", w, h);  // NVTX range per level
-    double* u = P.u[cur];
+    double* u = P.setA;  // plane 0 of the level's state block
     double* wv = P.wv[cur];
     if (k == 0) {
       cudaMemsetAsync(u, 0, np * sizeof(double), st);
       cudaMemsetAsync(wv, 0, 2 * np * sizeof(double), st);
     } else {
-      rc = upsample64_internal(P.u[cur ^ 1], P.wv[cur ^ 1], prev_mask, prev_h, prev_w,
+      rc = upsample64_internal(P.carry_u, P.wv[cur ^ 1], prev_mask, prev_h, prev_w,
                                P.lvl_mask[l], h, w, u, wv, st);
       if (rc) return rc;
     }
     L64 L = lv[k];
-    L.u = u;
     L.wv = wv;
     if (side) cudaStreamWaitEvent(st, ev[1 + k], 0);  // join: this level's setup done
     rc = solve_level64(L, prm, diag, pd_off, warp_off, P.setup_scratch, P.setup_bytes, st,
@@ -880,10 +939,11 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
     pd_off += (int64_t)N * K;
     warp_off += N;
     prev_h = h; prev_w = w; prev_mask = P.lvl_mask[l];
+    if (l > 0) cudaMemcpyAsync(P.carry_u, u, np * sizeof(double), cudaMemcpyDeviceToDevice, st);
     if (l == 0) {
       cudaMemcpyAsync(u_out, u, n0 * sizeof(double), cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(w_out, wv, 2 * n0 * sizeof(double), cudaMemcpyDeviceToDevice, st);
-      k64_interleave<<<(unsigned)((n0 + 255) / 256), 256, 0, st>>>(P.v, n0, v_out);
+      k64_interleave<<<(unsigned)((n0 + 255) / 256), 256, 0, st>>>(P.setA + n0, n0, v_out);
       cudaMemcpyAsync(mask_out, P.solve_mask, n0, cudaMemcpyDeviceToDevice, st);
     }
     cur ^= 1;

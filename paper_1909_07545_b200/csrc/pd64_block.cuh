@@ -1,6 +1,7 @@
 // Launch arguments of the blocked float64 primal-dual kernel (pd64_block.cu).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
@@ -45,7 +46,40 @@ int pd64_tile_launch(const B64& A, int halo, cudaStream_t st);
 int pd64_tile_launch_unchecked(const B64& A, int halo, cudaStream_t st);  // iters 0: timing
 size_t pd64_tile_count(int w, int h, int halo);
 int pd64_tile_tile_list(const uint8_t* mask, int w, int h, int halo, int* tiles, cudaStream_t st);
-// Per-level edge codes (bit0 mask, bit1 x-edge, bit2 y-edge; pd64_tile.cu).
-int pd64_edge_codes(const uint8_t* mask, int w, int h, uint32_t* code, cudaStream_t st);
+// Per-level edge codes (bit0 mask, bit1 x-edge, bit2 y-edge; pd64_tile.cu);
+// with `codef`, also as a float64 plane (the 10th constant plane of k64_tma).
+int pd64_edge_codes(const uint8_t* mask, int w, int h, uint32_t* code, double* codef,
+                    cudaStream_t st);
+
+// The TMA-fed tile kernel (pd64_tma.cu, halo-2 levels). Layout it requires:
+// each state set one block of 12 planes of stride n = h*w in the order u, v0,
+// v1, p0, p1, q0..q3, u_bar, v_bar0, v_bar1 (A.su .. A.svb point into it), the
+// level's constants one block of 10 planes: tensor a b c, sigma_p, tau_u,
+// tau_v, I_u, rho0, u_omega, edge code (float64); w % 4 == 0. Tensor maps:
+// [set][0] all 12 planes, [set][1] the first 9 (the warp's first launch loads
+// no u_bar / v_bar, its last stores none).
+struct Tma64Level {
+  CUtensorMap ld[2][2], st[2][2], cst;
+};
+bool pd64_tma_usable(int w, int h);
+bool pd64_tma_level_maps(Tma64Level* M, const double* set0, const double* set1,
+                         const double* cst, int w, int h);
+int pd64_tma_launch(const B64& A, const Tma64Level& M, int src_set, cudaStream_t st);
+size_t pd64_tma_tile_count(int w, int h);
+int pd64_tma_tile_list(const uint8_t* mask, int w, int h, int* tiles, cudaStream_t st);
+
+// The cluster-tile kernel (pd64_ctile.cu, the large levels): same layout as
+// k64_tma; regions of a cluster of CTAs exchange halos through DSMEM, R
+// (pd64_ctile_halo) cycles per launch. Tensor maps: [set][0] 12 planes, [set][1] 9.
+struct Ctile64Maps {
+  CUtensorMap ld[2][2], cst;
+};
+int pd64_ctile_halo();
+bool pd64_ctile_usable(int w, int h);
+bool pd64_ctile_maps(Ctile64Maps* M, const double* set0, const double* set1, const double* cst,
+                     int w, int h);
+size_t pd64_ctile_partials(int w, int h);  // per-CTA partial sums of |du| (regions x CTAs)
+int pd64_ctile_list(const uint8_t* mask, int w, int h, int* tiles, cudaStream_t st);
+int pd64_ctile_launch(const B64& A, const Ctile64Maps& M, int src_set, cudaStream_t st);
 
 }  // namespace fsb

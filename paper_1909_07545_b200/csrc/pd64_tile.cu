@@ -390,20 +390,23 @@ int launch_r(const B64& A, cudaStream_t st) {
 // Edge code per pixel of a level: bit0 mask, bit1 x-edge in the mask
 // (m(x) & m(x+1)), bit2 y-edge (m(y) & m(y+1)) — rasters.py:175-182.
 __global__ void k64_edge_codes(const uint8_t* __restrict__ m, int w, int h,
-                               uint32_t* __restrict__ code) {
+                               uint32_t* __restrict__ code, double* __restrict__ codef) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
   if (x >= w) return;
   const size_t i = (size_t)y * w + x;
   const bool mm = m[i];
   const bool ex = mm && x + 1 < w && m[i + 1];
   const bool ey = mm && y + 1 < h && m[i + w];
-  code[i] = (mm ? 1u : 0u) | (ex ? 2u : 0u) | (ey ? 4u : 0u);
+  const uint32_t c = (mm ? 1u : 0u) | (ex ? 2u : 0u) | (ey ? 4u : 0u);
+  code[i] = c;
+  if (codef) codef[i] = (double)c;
 }
 
 }  // namespace
 
-int pd64_edge_codes(const uint8_t* mask, int w, int h, uint32_t* code, cudaStream_t st) {
-  k64_edge_codes<<<dim3((w + 127) / 128, h), 128, 0, st>>>(mask, w, h, code);
+int pd64_edge_codes(const uint8_t* mask, int w, int h, uint32_t* code, double* codef,
+                    cudaStream_t st) {
+  k64_edge_codes<<<dim3((w + 127) / 128, h), 128, 0, st>>>(mask, w, h, code, codef);
   return launch_status();
 }
 

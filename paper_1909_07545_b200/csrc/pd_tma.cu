@@ -19,6 +19,7 @@
 
 #include "pd_args.cuh"
 #include "pd_math.cuh"
+#include "tma.cuh"
 
 namespace fsb {
 namespace {
@@ -42,38 +43,6 @@ FSB_INLINE float shrink1(float uh, float rh, float g, float tl) {
 }
 FSB_INLINE f2 shrink2(f2 uh, f2 rh, f2 g, f2 tl) {
   return mk2(shrink1(uh.x, rh.x, g.x, tl.x), shrink1(uh.y, rh.y, g.y, tl.y));
-}
-
-FSB_INLINE uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-FSB_INLINE void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-FSB_INLINE void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-FSB_INLINE void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-FSB_INLINE void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
-                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-      : "memory");
 }
 
 #ifndef FSB_ALIGNED_LOAD
@@ -123,7 +92,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_init_fence();
   }
   __syncthreads();
   // The tensor maps are used straight from the __grid_constant__ parameters
@@ -413,26 +382,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
 #undef FSB_ISSUE_TILE
 }
 
-typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiled encoder() {
-  // resolved once; a function-local static is initialised thread-safely, so a
-  // concurrent first caller never sees a half-done lookup (and a spurious
-  // non-TMA fallback)
-  static const EncodeTiled fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      return reinterpret_cast<EncodeTiled>(p);
-    return static_cast<EncodeTiled>(nullptr);
-  }();
-  return fn;
-}
+EncodeTiled encoder() { return tma_encoder(); }
 
 // planes x h x w fp32 block with plane stride n; box 64 x 32 x planes
 bool make_map(CUtensorMap* m, const float* base, int w, int h, int planes, size_t n) {

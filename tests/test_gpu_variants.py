@@ -1,10 +1,15 @@
 """The float64 path's kernel variants agree (each switch is read once per
 process, so every variant runs in a child process on the golden pair and on a
-C1 frame): the default (k64_tile over the per-level work list, phase-staggered
-persistent schedule, NaN-texel prologue on small levels) against
+C1 frame). The default at these sizes (k64_tile over the per-level work lists,
+phase-staggered persistent schedule, NaN-texel prologue on small levels) against
+  * k64_tile everywhere (FSB_PD64K=tilel)                  -> bit-identical,
   * the non-persistent schedule (FSB_PD64_PERSIST=0)      -> bit-identical,
   * per-level setup on the caller's stream (FSB_OVERLAP=0) -> bit-identical,
   * k64_tile over every tile with masked loads (FSB_PD64K=tile) -> bit-identical,
+  * the k64_ctile cluster regions on the halo-2 levels, as the default uses
+    them above 512^2 (FSB_CTILE_MIN=1), in three cluster shapes / halos, and
+    the TMA-fed k64_tma (FSB_PD64K=tma)                   -> <= 1e-10 px (they
+    differ only in where the compiler contracts a multiply-add, ~1e-13 px),
   * the masked-gather prologue everywhere (FSB_PRO64=old) -> <= 1e-10 px,
   * the round-1 k64_block, no FMA (FSB_PD64K=block)       -> <= 1e-8 px.
 Scheduling and load strategy must not change a single bit of the answer."""
@@ -49,6 +54,11 @@ def _run(tmp_path, name, env_extra):
 
 
 @pytest.mark.parametrize("name,env,tol", [
+    ("tilel", {"FSB_PD64K": "tilel"}, 0.0),
+    ("ctile", {"FSB_CTILE_MIN": "1"}, 1e-10),
+    ("ctile_5_4_4", {"FSB_CTILE_MIN": "1", "FSB_CTILE": "5,4,4"}, 1e-10),
+    ("ctile_10_4_4", {"FSB_CTILE_MIN": "1", "FSB_CTILE": "10,4,4"}, 1e-10),
+    ("tma", {"FSB_PD64K": "tma"}, 1e-10),
     ("persist0", {"FSB_PD64_PERSIST": "0"}, 0.0),
     ("no_overlap", {"FSB_OVERLAP": "0"}, 0.0),
     ("alltiles", {"FSB_PD64K": "tile"}, 0.0),
