@@ -332,7 +332,8 @@ CtileCfg ctile_cfg() {
       CtileCfg t{0, 0, 0};
       if (sscanf(e, "%d,%d,%d", &t.R, &t.CX, &t.CY) == 3 &&
           ((t.R == 5 && t.CX == 2 && t.CY == 4) || (t.R == 5 && t.CX == 4 && t.CY == 4) ||
-           (t.R == 10 && t.CX == 4 && t.CY == 4) || (t.R == 4 && t.CX == 2 && t.CY == 4)))
+           (t.R == 10 && t.CX == 4 && t.CY == 4) || (t.R == 4 && t.CX == 2 && t.CY == 4) ||
+           (t.R == 5 && t.CX == 2 && t.CY == 8) || (t.R == 5 && t.CX == 4 && t.CY == 2)))
         d = t;
     }
     return d;
@@ -412,7 +413,9 @@ int pd64_ctile_list(const uint8_t* mask, int w, int h, int* tiles, cudaStream_t 
 int pd64_ctile_launch(const B64& A, const Ctile64Maps& M, int src_set, cudaStream_t st) {
   const CtileCfg c = ctile_cfg();
   if (A.iters < 1 || A.iters > c.R || !A.tiles || (src_set & ~1)) return FSB_EINVAL;
-  if (c.R == 5 && c.CX == 4) return launch_ctile_d<5, 4, 4>(A, M, src_set, st);
+  if (c.R == 5 && c.CX == 4 && c.CY == 4) return launch_ctile_d<5, 4, 4>(A, M, src_set, st);
+  if (c.R == 5 && c.CX == 4 && c.CY == 2) return launch_ctile_d<5, 4, 2>(A, M, src_set, st);
+  if (c.R == 5 && c.CY == 8) return launch_ctile_d<5, 2, 8>(A, M, src_set, st);
   if (c.R == 10) return launch_ctile_d<10, 4, 4>(A, M, src_set, st);
   if (c.R == 4) return launch_ctile_d<4, 2, 4>(A, M, src_set, st);
   return launch_ctile_d<5, 2, 4>(A, M, src_set, st);
