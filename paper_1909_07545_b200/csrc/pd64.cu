@@ -598,11 +598,11 @@ LevelCfg64 level_cfg64(const L64& L) {
   }
   c.halo = halo;
   c.kern = halo > 0 ? pd64_kernel_for(halo) : -1;
-  // k64_ctile on levels above 512^2 (C3 1024^2: 16.0 -> 14.4 ms per frame); at
-  // 512^2 it measured level with k64_tile. FSB_CTILE_MIN=<pixels> moves the cut.
+  // k64_ctile on levels of 512^2 and more (C3 1024^2: 16.0 -> 13.5 ms per
+  // frame, 512^2: 4.64 -> 4.57 ms); FSB_CTILE_MIN=<pixels> moves the cut.
   static const size_t ctile_min = [] {
     const char* e = getenv("FSB_CTILE_MIN");
-    return e ? (size_t)atoll(e) : (size_t)512 * 512 + 1;
+    return e ? (size_t)atoll(e) : (size_t)512 * 512;
   }();
   const int choice = pd64_kernel_choice();
   if (c.kern == K64_TILEL && halo == 2 && choice == K64_CTILE && tma_layout64(L) &&

@@ -52,19 +52,20 @@ int tile_list_internal(const uint8_t* mask, int w, int h, int TW, int TH, int* t
 
 namespace {
 
-constexpr int kW = 32, kH = 16, kBW = kW + 2;  // load box: 2 spare columns for the even start
-constexpr int kPl = kBW * kH;                  // doubles per staged plane
+constexpr int kW = 32, kBW = kW + 2;  // load box: 2 spare columns for the even start
 constexpr int kSt = 12, kSt0 = 9, kCst = 10;
 enum { PU, PV0, PV1, PP0, PP1, PQ0, PQ1, PQ2, PQ3, PUB, PVB0, PVB1 };
 enum { CA, CB, CC, CSP, CTU, CTV, CIU, CRH, CUO, CCODE };
 
 // in-CTA exchange buffers, aliased on the state box once the tile is in registers
+template <int kH>
 struct XchC {
   double ub[kH][kW], vb0[kH][kW], vb1[kH][kW];  // dual step: u_bar, v_bar rows
   double fy[3][kH][kW];                         // primal step: y-fluxes
 };
 // Cross-CTA values, pushed by the neighbour CTA with st.async (double-buffered
 // by cycle parity; each buffer completes one mbarrier phase per 2 cycles).
+template <int kH>
 struct RecvC {
   double dn[2][3][kW];  // dual: row 0 (u_bar, v_bar) of the CTA below
   double rt[2][3][kH];  // dual: column 0 of the CTA to the right
@@ -72,16 +73,19 @@ struct RecvC {
   double lf[2][3][kH];  // primal: column 31 x-fluxes of the CTA to the left
   uint64_t bd[2], bp[2];  // dual / primal mbarriers
 };
+template <int kH>
 struct SmemC {
+  static constexpr int kPl = kBW * kH;  // doubles per staged plane
   double st[kSt][kPl];   // state box | XchC
   double cs[kCst][kPl];  // constant box, read through the cycles
-  RecvC rv;
+  RecvC<kH> rv;
   double red_sum[kH], red_max[kH];
   uint64_t bar;
+  static_assert(sizeof(XchC<kH>) <= sizeof(double) * kSt * kPl, "exchange aliases the state box");
+  static_assert(sizeof(double) * kSt * kPl % 128 == 0, "TMA boxes must stay 128-byte aligned");
 };
-static_assert(sizeof(XchC) <= sizeof(double) * kSt * kPl, "exchange aliases the state box");
-static_assert(sizeof(double) * kSt * kPl % 128 == 0, "TMA boxes must stay 128-byte aligned");
-constexpr size_t kSmemBytes = sizeof(SmemC) + 128;
+template <int kH>
+constexpr size_t smem_bytes() { return sizeof(SmemC<kH>) + 128; }
 
 FSB_INLINE double shfl_dn(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 FSB_INLINE double shfl_up(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
@@ -109,15 +113,18 @@ FSB_INLINE void st_async(uint32_t raddr, double v, uint32_t rbar) {
                : "memory");
 }
 
-template <int R, int CX, int CY, bool DIAG>
-__global__ void __launch_bounds__(kW * kH, 2)
+// kH rows per CTA: 16 (512 threads, 2 CTAs per SM), 8 (256 threads, 4 per SM) or 4
+template <int R, int CX, int CY, int kH, bool DIAG>
+__global__ void __launch_bounds__(kW * kH, 1024 / (kW * kH))
     k64_ctile(const B64 A, const __grid_constant__ CUtensorMap m_ld,
               const __grid_constant__ CUtensorMap m_cst, int nrx) {
   constexpr int NC = CX * CY, RW = CX * kW, RH = CY * kH, IW = RW - 2 * R, IH = RH - 2 * R;
   extern __shared__ unsigned char smem_raw[];
   poison_dynamic_smem(smem_raw);  // checked build only
-  SmemC& S = *reinterpret_cast<SmemC*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
-  XchC& X = *reinterpret_cast<XchC*>(&S.st[0][0]);
+  constexpr int kPl = SmemC<kH>::kPl;
+  SmemC<kH>& S =
+      *reinterpret_cast<SmemC<kH>*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
+  XchC<kH>& X = *reinterpret_cast<XchC<kH>*>(&S.st[0][0]);
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank(), cx = rank % CX, cy = rank / CX;
   const int k = (int)blockIdx.x / NC;  // the cluster's work-list entry
@@ -320,20 +327,24 @@ __global__ void __launch_bounds__(kW * kH, 2)
 }
 
 struct CtileCfg {
-  int R, CX, CY;
+  int R, CX, CY, TH;
 };
 
-// FSB_CTILE="R,CX,CY" (tuning): halo / cycles per launch and cluster shape
+// FSB_CTILE="R,CX,CY[,TH]" (tuning): halo / cycles per launch, cluster shape,
+// rows per CTA
 CtileCfg ctile_cfg() {
   static const CtileCfg c = [] {
-    CtileCfg d{5, 2, 4};
+    CtileCfg d{5, 2, 8, 8};  // 2 x 8 CTAs of 32 x 8: 64 x 64 regions, 4 CTAs per SM
     const char* e = getenv("FSB_CTILE");
     if (e) {
-      CtileCfg t{0, 0, 0};
-      if (sscanf(e, "%d,%d,%d", &t.R, &t.CX, &t.CY) == 3 &&
-          ((t.R == 5 && t.CX == 2 && t.CY == 4) || (t.R == 5 && t.CX == 4 && t.CY == 4) ||
-           (t.R == 10 && t.CX == 4 && t.CY == 4) || (t.R == 4 && t.CX == 2 && t.CY == 4) ||
-           (t.R == 5 && t.CX == 2 && t.CY == 8) || (t.R == 5 && t.CX == 4 && t.CY == 2)))
+      CtileCfg t{0, 0, 0, 16};
+      const int k = sscanf(e, "%d,%d,%d,%d", &t.R, &t.CX, &t.CY, &t.TH);
+      auto is = [&](int r, int cx, int cy, int th) {
+        return t.R == r && t.CX == cx && t.CY == cy && t.TH == th;
+      };
+      if (k >= 3 && (is(5, 2, 4, 16) || is(5, 4, 4, 16) || is(10, 4, 4, 16) || is(4, 2, 4, 16) ||
+                     is(5, 2, 8, 16) || is(5, 4, 2, 16) || is(5, 2, 8, 8) || is(5, 2, 4, 8) ||
+                     is(5, 4, 4, 8) || is(5, 2, 8, 4)))
         d = t;
     }
     return d;
@@ -341,21 +352,22 @@ CtileCfg ctile_cfg() {
   return c;
 }
 
-template <int R, int CX, int CY, bool DIAG>
+template <int R, int CX, int CY, int TH, bool DIAG>
 int launch_ctile(const B64& A, const Ctile64Maps& M, int src, cudaStream_t st) {
-  constexpr int NC = CX * CY, IW = CX * kW - 2 * R, IH = CY * kH - 2 * R;
+  constexpr int NC = CX * CY, IW = CX * kW - 2 * R, IH = CY * TH - 2 * R;
   const int nrx = (A.w + IW - 1) / IW, nry = (A.h + IH - 1) / IH;
-  auto kern = k64_ctile<R, CX, CY, DIAG>;
+  auto kern = k64_ctile<R, CX, CY, TH, DIAG>;
+  constexpr size_t smem = smem_bytes<TH>();
   static std::atomic<unsigned long long> attr{0};
   once_per_device(attr, [&] {
     if (NC > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   });
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3((unsigned)(nrx * nry * NC));
-  cfg.blockDim = dim3(kW, kH);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.blockDim = dim3(kW, TH);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -370,11 +382,11 @@ int launch_ctile(const B64& A, const Ctile64Maps& M, int src, cudaStream_t st) {
   return launch_status();
 }
 
-template <int R, int CX, int CY>
+template <int R, int CX, int CY, int TH>
 int launch_ctile_d(const B64& A, const Ctile64Maps& M, int src, cudaStream_t st) {
   const bool diag = A.diag_p || A.diag_du || A.diag_du64;
-  return diag ? launch_ctile<R, CX, CY, true>(A, M, src, st)
-              : launch_ctile<R, CX, CY, false>(A, M, src, st);
+  return diag ? launch_ctile<R, CX, CY, TH, true>(A, M, src, st)
+              : launch_ctile<R, CX, CY, TH, false>(A, M, src, st);
 }
 
 }  // namespace
@@ -383,42 +395,49 @@ int pd64_ctile_halo() { return ctile_cfg().R; }
 
 bool pd64_ctile_usable(int w, int h) {
   const CtileCfg c = ctile_cfg();
-  return w % 2 == 0 && w >= kBW && h >= kH && w >= c.CX * kW && h >= c.CY * kH &&
+  return w % 2 == 0 && w >= kBW && h >= c.TH && w >= c.CX * kW && h >= c.CY * c.TH &&
          tma_encoder() != nullptr;
 }
 
 bool pd64_ctile_maps(Ctile64Maps* M, const double* set0, const double* set1, const double* cst,
                      int w, int h) {
   if (!pd64_ctile_usable(w, h)) return false;
+  const CtileCfg c = ctile_cfg();
   if (((uintptr_t)set0 | (uintptr_t)set1 | (uintptr_t)cst) & 15) return false;
   const double* sets[2] = {set0, set1};
   for (int k = 0; k < 2; ++k)
-    if (!make_map64(&M->ld[k][0], sets[k], w, h, kSt, kBW, kH, kSt) ||
-        !make_map64(&M->ld[k][1], sets[k], w, h, kSt, kBW, kH, kSt0))
+    if (!make_map64(&M->ld[k][0], sets[k], w, h, kSt, kBW, c.TH, kSt) ||
+        !make_map64(&M->ld[k][1], sets[k], w, h, kSt, kBW, c.TH, kSt0))
       return false;
-  return make_map64(&M->cst, cst, w, h, kCst, kBW, kH, kCst);
+  return make_map64(&M->cst, cst, w, h, kCst, kBW, c.TH, kCst);
 }
 
 size_t pd64_ctile_partials(int w, int h) {
   const CtileCfg c = ctile_cfg();
-  const int IW = c.CX * kW - 2 * c.R, IH = c.CY * kH - 2 * c.R;
+  const int IW = c.CX * kW - 2 * c.R, IH = c.CY * c.TH - 2 * c.R;
   return (size_t)((w + IW - 1) / IW) * ((h + IH - 1) / IH) * c.CX * c.CY;
 }
 
 int pd64_ctile_list(const uint8_t* mask, int w, int h, int* tiles, cudaStream_t st) {
   const CtileCfg c = ctile_cfg();
-  return tile_list_internal(mask, w, h, c.CX * kW - 2 * c.R, c.CY * kH - 2 * c.R, tiles, st);
+  return tile_list_internal(mask, w, h, c.CX * kW - 2 * c.R, c.CY * c.TH - 2 * c.R, tiles, st);
 }
 
 int pd64_ctile_launch(const B64& A, const Ctile64Maps& M, int src_set, cudaStream_t st) {
   const CtileCfg c = ctile_cfg();
   if (A.iters < 1 || A.iters > c.R || !A.tiles || (src_set & ~1)) return FSB_EINVAL;
-  if (c.R == 5 && c.CX == 4 && c.CY == 4) return launch_ctile_d<5, 4, 4>(A, M, src_set, st);
-  if (c.R == 5 && c.CX == 4 && c.CY == 2) return launch_ctile_d<5, 4, 2>(A, M, src_set, st);
-  if (c.R == 5 && c.CY == 8) return launch_ctile_d<5, 2, 8>(A, M, src_set, st);
-  if (c.R == 10) return launch_ctile_d<10, 4, 4>(A, M, src_set, st);
-  if (c.R == 4) return launch_ctile_d<4, 2, 4>(A, M, src_set, st);
-  return launch_ctile_d<5, 2, 4>(A, M, src_set, st);
+  if (c.TH == 4) return launch_ctile_d<5, 2, 8, 4>(A, M, src_set, st);
+  if (c.TH == 8) {
+    if (c.CX == 4) return launch_ctile_d<5, 4, 4, 8>(A, M, src_set, st);
+    if (c.CY == 8) return launch_ctile_d<5, 2, 8, 8>(A, M, src_set, st);
+    return launch_ctile_d<5, 2, 4, 8>(A, M, src_set, st);
+  }
+  if (c.R == 5 && c.CX == 4 && c.CY == 4) return launch_ctile_d<5, 4, 4, 16>(A, M, src_set, st);
+  if (c.R == 5 && c.CX == 4 && c.CY == 2) return launch_ctile_d<5, 4, 2, 16>(A, M, src_set, st);
+  if (c.R == 5 && c.CY == 8) return launch_ctile_d<5, 2, 8, 16>(A, M, src_set, st);
+  if (c.R == 10) return launch_ctile_d<10, 4, 4, 16>(A, M, src_set, st);
+  if (c.R == 4) return launch_ctile_d<4, 2, 4, 16>(A, M, src_set, st);
+  return launch_ctile_d<5, 2, 4, 16>(A, M, src_set, st);
 }
 
 }  // namespace fsb

@@ -7,7 +7,7 @@ phase-staggered persistent schedule, NaN-texel prologue on small levels) against
   * per-level setup on the caller's stream (FSB_OVERLAP=0) -> bit-identical,
   * k64_tile over every tile with masked loads (FSB_PD64K=tile) -> bit-identical,
   * the k64_ctile cluster regions on the halo-2 levels, as the default uses
-    them above 512^2 (FSB_CTILE_MIN=1), in three cluster shapes / halos, and
+    them from 512^2 up (FSB_CTILE_MIN=1), in four cluster shapes / halos, and
     the TMA-fed k64_tma (FSB_PD64K=tma)                   -> <= 1e-10 px (they
     differ only in where the compiler contracts a multiply-add, ~1e-13 px),
   * the masked-gather prologue everywhere (FSB_PRO64=old) -> <= 1e-10 px,
@@ -56,6 +56,7 @@ def _run(tmp_path, name, env_extra):
 @pytest.mark.parametrize("name,env,tol", [
     ("tilel", {"FSB_PD64K": "tilel"}, 0.0),
     ("ctile", {"FSB_CTILE_MIN": "1"}, 1e-10),
+    ("ctile_5_2_4_16", {"FSB_CTILE_MIN": "1", "FSB_CTILE": "5,2,4,16"}, 1e-10),
     ("ctile_5_4_4", {"FSB_CTILE_MIN": "1", "FSB_CTILE": "5,4,4"}, 1e-10),
     ("ctile_10_4_4", {"FSB_CTILE_MIN": "1", "FSB_CTILE": "10,4,4"}, 1e-10),
     ("tma", {"FSB_PD64K": "tma"}, 1e-10),
