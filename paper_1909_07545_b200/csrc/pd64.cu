@@ -605,7 +605,7 @@ LevelCfg64 level_cfg64(const L64& L) {
     return e ? (size_t)atoll(e) : (size_t)512 * 512;
   }();
   const int choice = pd64_kernel_choice();
-  if (c.kern == K64_TILEL && halo == 2 && choice == K64_CTILE && tma_layout64(L) &&
+  if (c.kern == K64_TILEL && halo > 1 && choice == K64_CTILE && tma_layout64(L) &&
       (size_t)L.w * L.h >= ctile_min && pd64_ctile_usable(L.w, L.h)) {
     c.kern = K64_CTILE;
     c.halo = pd64_ctile_halo();
