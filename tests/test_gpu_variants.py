@@ -1,6 +1,7 @@
 """The float64 path's kernel variants agree (each switch is read once per
 process, so every variant runs in a child process on the golden pair and on a
-C1 frame). The default at these sizes (k64_tile over the per-level work lists,
+C1 frame, the C1 frame also with diagnostics: the DIAG kernel variants). The
+default at these sizes (k64_tile over the per-level work lists,
 phase-staggered persistent schedule, NaN-texel prologue on small levels) against
   * k64_tile everywhere (FSB_PD64K=tilel)                  -> bit-identical,
   * the non-persistent schedule (FSB_PD64_PERSIST=0)      -> bit-identical,
@@ -40,7 +41,10 @@ sc = S.default_scene()
 i0 = S.render(sc, rig1.cam0, supersample=1)[0]
 i1 = S.render(sc, rig1.cam1, pose=rig1.pose, supersample=1)[0]
 r1 = solve_pyramid(i0, i1, rig1, prm1)
-np.savez(sys.argv[2], u=r.u, w=r.w, v=r.v, u1=r1.u, w1=r1.w)
+d = solve_pyramid(i0, i1, rig1, prm1, collect_diagnostics=True).diagnostics
+np.savez(sys.argv[2], u=r.u, w=r.w, v=r.v, u1=r1.u, w1=r1.w,
+         d_p=np.array(d.max_p_norm), d_q=np.array(d.max_q_norm), d_du=np.array(d.max_du),
+         d_mean=np.array(d.mean_abs_du))
 """
 
 
@@ -70,5 +74,11 @@ def test_float64_kernel_variants_agree(tmp_path, name, env, tol):
     base = _run(tmp_path, "default", {})
     var = _run(tmp_path, name, env)
     for k in base:
+        if k.startswith("d_"):  # diagnostics (the DIAG kernel variants): max / mean traces
+            if tol == 0.0:
+                assert np.array_equal(base[k], var[k]), (name, k)
+            else:
+                assert np.allclose(base[k], var[k], rtol=1e-6, atol=1e-12), (name, k)
+            continue
         d = float(np.max(np.abs(base[k] - var[k])))
         assert d <= tol, (name, k, d)
