@@ -1,26 +1,27 @@
-// k64_ctile: the float64 primal-dual kernel of the largest levels as cluster
-// tiles — halo exchange through distributed shared memory inside a cluster,
-// redundant halo cycles only at the cluster's border.
+// k64_ctile: the float64 primal-dual kernel of the large levels (512^2 and up)
+// as cluster tiles — halo exchange through distributed shared memory inside a
+// cluster, redundant halo cycles only at the cluster's border.
 //
 // k64_tile / k64_tma run R = 2 cycles per launch on 32 x 16 tiles: every tile
 // recomputes a 2-pixel halo, and a warp's K = 10 cycles cost 5 round trips of
 // the 12 state + 10 constant planes through HBM — the launch is bound by that
 // traffic (profiles/r02_pd64_ncu.txt). Here a cluster of CX x CY CTAs covers
-// one region of (CX 32) x (CY 16) pixels (each CTA one 32 x 16 tile, one pixel
+// one region of (CX 32) x (CY kH) pixels (each CTA one 32 x kH tile, one pixel
 // per thread, state in registers, constants in shared memory) and runs R = 5
 // cycles per launch: a warp is 2 launches instead of 5, and only the region's
-// outer R-pixel border is halo (2 x 4 cluster: 64 x 64 region, 54 x 54
-// interior: 1.40 pixel-cycles per solved pixel-cycle against 1.52).
+// outer R-pixel border is halo. Default: 2 x 8 clusters of 32 x 8 CTAs (256
+// threads, 4 CTAs per SM) — a 64 x 64 region with a 54 x 54 interior, 1.40
+// pixel-cycles per solved pixel-cycle against k64_tile's 1.52.
 //
 // Across a CTA edge the neighbour values of a half-cycle (dual: the u_bar /
-// v_bar row 0 and column 0; primal: the y-fluxes of row 15 and x-fluxes of
-// column 31) are PUSHED into the neighbour CTA's shared memory with st.async,
-// completing bytes on its mbarrier; the receiver waits on that mbarrier, and
-// inside the CTA two __syncthreads per cycle remain. No cluster barrier in the
-// cycles: a release-ordered barrier.cluster costs a MEMBAR.GPU per use, which
-// made a first version with 2 cluster barriers per cycle slower than k64_tile.
-// Receive buffers and mbarriers are double-buffered by cycle parity; a
-// neighbour can run at most one half-cycle ahead, because every push
+// v_bar row 0 and column 0; primal: the y-fluxes of the last row and the
+// x-fluxes of column 31) are PUSHED into the neighbour CTA's shared memory
+// with st.async, completing bytes on its mbarrier; the receiver waits on that
+// mbarrier, and inside the CTA two __syncthreads per cycle remain. No cluster
+// barrier in the cycles: a release-ordered barrier.cluster costs a MEMBAR.GPU
+// per use, which made a first version with 2 cluster barriers per cycle slower
+// than k64_tile. Receive buffers and mbarriers are double-buffered by cycle
+// parity; a neighbour can run at most one half-cycle ahead, because every push
 // direction has a reverse one between the same two CTAs.
 //
 // Loads: two TMA boxes per CTA (state: 12 planes, the warp's first launch 9;
