@@ -43,6 +43,7 @@ UNITS = [
     ("pd64_tile.cu", []),
     ("pd64_tma.cu", []),
     ("pd64_ctile.cu", []),
+    ("pd64_level.cu", []),
     ("sample64.cu", ["-fmad=false"]),
     ("solver.cu", []),
     ("synth.cu", ["-fmad=false"]),

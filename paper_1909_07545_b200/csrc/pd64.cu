@@ -21,6 +21,7 @@
 
 #include "pd_math.cuh"
 #include "pd64_block.cuh"
+#include "sample64.cuh"
 
 namespace fsb {
 
@@ -45,23 +46,16 @@ int level_setup64_internal(const double* i0, const uint8_t* mask, int h, int w,
                            size_t scratch_bytes, cudaStream_t st);
 int mean_finish_internal(const double* partials, int nparts, const uint8_t* mask, size_t n,
                          double* out, cudaStream_t st);
-struct P64 {  // sample64.cu
-  int h, w;
-  const double* i0;
-  const uint8_t* mask;
-  const double4* tex;
-  const double* wv;
-  double* i1wn;
-  double* dirs;
-  uint8_t* dir_ok;
-  double* iu;
-  double* rho0;
-};
 int pack64_internal(const double* i1, const uint8_t* mask, const double* traj,
                     const uint8_t* tok, int h, int w, double4* tex, cudaStream_t st);
 int sample_nan64_internal(const P64& L, int bx, int by, cudaStream_t st);
 int linearize_nan64_internal(const P64& L, int bx, int by, cudaStream_t st);
 bool side_stream_for(cudaStream_t main, cudaStream_t* side, cudaEvent_t** ev);  // solver.cu
+bool pd64_level_fits(int w, int h);  // pd64_level.cu
+int pd64_level_launch(const P64& P, const double* T, const double* S, const uint32_t* ecode,
+                      double* u, double* v, double* wv, double* scratch2, double lam,
+                      double alpha0, double alpha1, double theta, double sigma_q, double heps,
+                      double du_max, int N, int K, cudaStream_t st);
 
 }  // namespace fsb
 
@@ -698,6 +692,20 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
   P64 PL;
   PL.h = L.h; PL.w = L.w; PL.i0 = L.i0; PL.mask = L.mask; PL.tex = L.tex; PL.wv = L.wv;
   PL.i1wn = L.i1w; PL.dirs = L.dirs; PL.dir_ok = L.dir_ok; PL.iu = L.iu; PL.rho0 = L.rho0;
+  // a small level without diagnostics: the whole warp loop in one cluster launch
+  // (k64_level, pd64_level.cu); the sampled-image scratch is 2 level planes of
+  // the finest-level i1w buffer
+  if (pro_nan && listed && !dpq && !ddu && L.u2 && pd64_level_fits(L.w, L.h)) {
+    rc = pd64_level_launch(PL, L.T, L.S, L.ecode, L.u, L.v, L.wv, L.i1w, prm->lam,
+                           prm->alpha0, prm->alpha1, prm->theta, sigma_q_of(prm),
+                           huber_eps_of(prm), prm->du_max, N, K, st);
+    if (rc) return rc;
+    if (tm) {  // phase timer: the level is one launch
+      tm->used = 0;
+      tm->level_h = L.h; tm->level_w = L.w;
+    }
+    return launch_status();
+  }
   for (int wi = 0; wi < N; ++wi) {
     const bool timed = tm && wi < tm->cap;
     if (timed) cudaEventRecord(tm->ev[3 * wi], st);

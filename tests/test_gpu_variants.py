@@ -11,6 +11,8 @@ phase-staggered persistent schedule, NaN-texel prologue on small levels) against
     them from 512^2 up (FSB_CTILE_MIN=1), in four cluster shapes / halos, and
     the TMA-fed k64_tma (FSB_PD64K=tma)                   -> <= 1e-10 px (they
     differ only in where the compiler contracts a multiply-add, ~1e-13 px),
+  * the per-warp launches instead of the whole-level cluster kernel on the
+    levels that fit one cluster (FSB_LEVEL64=0)           -> <= 1e-10 px,
   * the masked-gather prologue everywhere (FSB_PRO64=old) -> <= 1e-10 px,
   * the round-1 k64_block, no FMA (FSB_PD64K=block)       -> <= 1e-8 px.
 Scheduling and load strategy must not change a single bit of the answer."""
@@ -67,6 +69,7 @@ def _run(tmp_path, name, env_extra):
     ("persist0", {"FSB_PD64_PERSIST": "0"}, 0.0),
     ("no_overlap", {"FSB_OVERLAP": "0"}, 0.0),
     ("alltiles", {"FSB_PD64K": "tile"}, 0.0),
+    ("level_off", {"FSB_LEVEL64": "0"}, 1e-10),
     ("prologue_old", {"FSB_PRO64": "old"}, 1e-10),
     ("block", {"FSB_PD64K": "block"}, 1e-8),
 ])
