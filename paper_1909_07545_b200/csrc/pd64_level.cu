@@ -68,6 +68,130 @@ FSB_INLINE void st_async(uint32_t raddr, double v, uint32_t rbar) {
                : "memory");
 }
 
+// A CTA's place in its cluster and the neighbours it exchanges with.
+struct Nbr {
+  int rank, cx_n;  // rank; cluster width in CTAs
+  bool has_r, has_l, has_d, has_u;
+  uint32_t dual_bytes, primal_bytes;  // bytes each exchange phase receives
+};
+template <int kH>
+FSB_INLINE Nbr make_nbr(int rank, int CX, int CY) {
+  Nbr e;
+  const int cx = rank % CX, cy = rank / CX;
+  e.rank = rank; e.cx_n = CX;
+  e.has_r = cx + 1 < CX; e.has_l = cx > 0; e.has_d = cy + 1 < CY; e.has_u = cy > 0;
+  e.dual_bytes = (e.has_d ? 3 * kW * 8 : 0) + (e.has_r ? 3 * kH * 8 : 0);
+  e.primal_bytes = (e.has_u ? 3 * kW * 8 : 0) + (e.has_l ? 3 * kH * 8 : 0);
+  return e;
+}
+struct PdConst {  // per-pixel constants of the cycles
+  double a, b, c, sp, tu, tv, g, rh, uo;
+  bool ex, ey;
+};
+struct PdScal {
+  double sq, heps, lam, alpha0, alpha1, theta;
+};
+
+// K primal-dual cycles (solver.py:279-303) of a warp, starting from the
+// warp-start reset u_bar = u, v_bar = v; in-CTA y-neighbours through shared
+// memory, x-neighbours by shuffle, across CTA edges by st.async pushes counted
+// on the receiver's mbarriers (parity buffers by the running cycle index cyc).
+// Left of column 0 / above row 0 without a neighbour CTA the fluxes are 0 (the
+// image border; at a region border these are halo pixels).
+template <int kH>
+FSB_INLINE void pd_cycles(LvlSmem<kH>& S, const Nbr& E, const PdConst& C, const PdScal& Q, int K,
+                          int& cyc, double& u, double& v0, double& v1, double& p0, double& p1,
+                          double& q0, double& q1, double& q2, double& q3) {
+  const int lane = threadIdx.x, ty = threadIdx.y, tid = ty * kW + lane;
+  const int tyd = ty + 1 < kH ? ty + 1 : ty;
+  const bool ex = C.ex, ey = C.ey;
+  double ub = u, vb0 = v0, vb1 = v1;
+  for (int it = 0; it < K; ++it, ++cyc) {
+    const int par = cyc & 1;
+    const uint32_t ph = (uint32_t)(cyc >> 1) & 1u;
+    S.ub[ty][lane] = ub;
+    S.vb0[ty][lane] = vb0;
+    S.vb1[ty][lane] = vb1;
+    if (ty == 0 && E.has_u) {
+      const int rk = E.rank - E.cx_n;
+      const uint32_t bar = mapa(&S.bd[par], rk);
+      st_async(mapa(&S.dn[par][0][lane], rk), ub, bar);
+      st_async(mapa(&S.dn[par][1][lane], rk), vb0, bar);
+      st_async(mapa(&S.dn[par][2][lane], rk), vb1, bar);
+    }
+    if (lane == 0 && E.has_l) {
+      const int rk = E.rank - 1;
+      const uint32_t bar = mapa(&S.bd[par], rk);
+      st_async(mapa(&S.rt[par][0][ty], rk), ub, bar);
+      st_async(mapa(&S.rt[par][1][ty], rk), vb0, bar);
+      st_async(mapa(&S.rt[par][2][ty], rk), vb1, bar);
+    }
+    if (tid == 0) mbar_expect_tx(&S.bd[par], E.dual_bytes);
+    __syncthreads();
+    // forward differences (rasters.py:144-155), zero where the edge leaves the mask
+    double ubx = shfl_dn(ub), vbx0 = shfl_dn(vb0), vbx1 = shfl_dn(vb1);
+    double uby = S.ub[tyd][lane], vby0 = S.vb0[tyd][lane], vby1 = S.vb1[tyd][lane];
+    if (E.has_r || (ty == kH - 1 && E.has_d)) {  // warp-uniform wait
+      mbar_wait(&S.bd[par], ph);
+      if (lane == kW - 1 && E.has_r) {
+        ubx = S.rt[par][0][ty]; vbx0 = S.rt[par][1][ty]; vbx1 = S.rt[par][2][ty];
+      }
+      if (ty == kH - 1 && E.has_d) {
+        uby = S.dn[par][0][lane]; vby0 = S.dn[par][1][lane]; vby1 = S.dn[par][2][lane];
+      }
+    }
+    const double gxx = ex ? ubx - ub : 0.0, gyy = ey ? uby - ub : 0.0;
+    const double g00 = ex ? vbx0 - vb0 : 0.0, g01 = ey ? vby0 - vb0 : 0.0;
+    const double g10 = ex ? vbx1 - vb1 : 0.0, g11 = ey ? vby1 - vb1 : 0.0;
+    dual_update_exact<double>(C.a, C.b, C.c, C.sp, Q.sq, gxx, gyy, g00, g01, g10, g11, vb0, vb1,
+                              p0, p1, q0, q1, q2, q3, Q.heps);
+    const double fx0 = ex ? C.a * p0 + C.b * p1 : 0.0;
+    const double fy0 = ey ? C.b * p0 + C.c * p1 : 0.0;
+    const double fx1 = ex ? q0 : 0.0, fy1 = ey ? q1 : 0.0;
+    const double fx2 = ex ? q2 : 0.0, fy2 = ey ? q3 : 0.0;
+    S.fy[0][ty][lane] = fy0;
+    S.fy[1][ty][lane] = fy1;
+    S.fy[2][ty][lane] = fy2;
+    if (ty == kH - 1 && E.has_d) {
+      const int rk = E.rank + E.cx_n;
+      const uint32_t bar = mapa(&S.bp[par], rk);
+      st_async(mapa(&S.up[par][0][lane], rk), fy0, bar);
+      st_async(mapa(&S.up[par][1][lane], rk), fy1, bar);
+      st_async(mapa(&S.up[par][2][lane], rk), fy2, bar);
+    }
+    if (lane == kW - 1 && E.has_r) {
+      const int rk = E.rank + 1;
+      const uint32_t bar = mapa(&S.bp[par], rk);
+      st_async(mapa(&S.lf[par][0][ty], rk), fx0, bar);
+      st_async(mapa(&S.lf[par][1][ty], rk), fx1, bar);
+      st_async(mapa(&S.lf[par][2][ty], rk), fx2, bar);
+    }
+    if (tid == 0) mbar_expect_tx(&S.bp[par], E.primal_bytes);
+    __syncthreads();
+    // backward divergence (rasters.py:158-172)
+    double lx0 = shfl_up(fx0), lx1 = shfl_up(fx1), lx2 = shfl_up(fx2);
+    if (lane == 0) lx0 = lx1 = lx2 = 0.0;
+    double uy0 = 0.0, uy1 = 0.0, uy2 = 0.0;
+    if (ty > 0) {
+      uy0 = S.fy[0][ty - 1][lane]; uy1 = S.fy[1][ty - 1][lane]; uy2 = S.fy[2][ty - 1][lane];
+    }
+    if (E.has_l || (ty == 0 && E.has_u)) {
+      mbar_wait(&S.bp[par], ph);
+      if (lane == 0 && E.has_l) {
+        lx0 = S.lf[par][0][ty]; lx1 = S.lf[par][1][ty]; lx2 = S.lf[par][2][ty];
+      }
+      if (ty == 0 && E.has_u) {
+        uy0 = S.up[par][0][lane]; uy1 = S.up[par][1][lane]; uy2 = S.up[par][2][lane];
+      }
+    }
+    const double dvv = ((fx0 - lx0) + fy0) - uy0;
+    const double dd0 = ((fx1 - lx1) + fy1) - uy1;
+    const double dd1 = ((fx2 - lx2) + fy2) - uy2;
+    primal_update_exact<double>(dvv, dd0, dd1, C.tu, C.tv, C.g, C.rh, C.uo, p0, p1, Q.lam,
+                                Q.alpha0, Q.alpha1, Q.theta, u, v0, v1, ub, vb0, vb1);
+  }
+}
+
 struct LvlArgs {
   P64 P;                    // the level's prologue view (tex, i0, mask, h, w)
   const double* T;          // tensor a, b, c planes
@@ -95,9 +219,7 @@ __global__ void __launch_bounds__(kW * kH, 1) k64_level(const LvlArgs A) {
   const int x = cx * kW + lane, y = cy * kH + ty;
   const bool in = x < W && y < H;
   const size_t i = in ? (size_t)y * W + x : 0;
-  const bool has_r = cx + 1 < CX, has_l = cx > 0, has_d = cy + 1 < CY, has_u = cy > 0;
-  const uint32_t dual_bytes = (has_d ? 3 * kW * 8 : 0) + (has_r ? 3 * kH * 8 : 0);
-  const uint32_t primal_bytes = (has_u ? 3 * kW * 8 : 0) + (has_l ? 3 * kH * 8 : 0);
+  const Nbr E = make_nbr<kH>(rank, CX, CY);
   if (tid == 0) {
     for (int j = 0; j < 2; ++j) {
       mbar_init(&S.bd[j], 1);
@@ -115,10 +237,8 @@ __global__ void __launch_bounds__(kW * kH, 1) k64_level(const LvlArgs A) {
   double u = in ? A.u[i] : 0.0, v0 = 0.0, v1 = 0.0, p0 = 0.0, p1 = 0.0;
   double q0 = 0.0, q1 = 0.0, q2 = 0.0, q3 = 0.0;
   double2 wv = in ? reinterpret_cast<const double2*>(A.wv)[i] : make_double2(0.0, 0.0);
-  const double sq = A.sigma_q * A.alpha0, heps = A.heps;
-  const double lam = A.lam, alpha0 = A.alpha0, alpha1 = A.alpha1, theta = A.theta;
+  const PdScal Q{A.sigma_q * A.alpha0, A.heps, A.lam, A.alpha0, A.alpha1, A.theta};
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
-  const int tyd = ty + 1 < kH ? ty + 1 : ty;
   cluster_sync_rel_acq();  // every CTA's mbarriers are initialised
 
   int cyc = 0;  // running cycle index: exchange buffer parity and mbarrier phase
@@ -142,92 +262,8 @@ __global__ void __launch_bounds__(kW * kH, 1) k64_level(const LvlArgs A) {
     }
     // warp-start reset (solver.py:344-346): u0 = u, u_bar = u, v_bar = v
     const double uo = u;
-    double ub = u, vb0 = v0, vb1 = v1;
-    for (int it = 0; it < A.K; ++it, ++cyc) {
-      const int par = cyc & 1;
-      const uint32_t ph = (uint32_t)(cyc >> 1) & 1u;
-      S.ub[ty][lane] = ub;
-      S.vb0[ty][lane] = vb0;
-      S.vb1[ty][lane] = vb1;
-      if (ty == 0 && has_u) {
-        const int rk = rank - CX;
-        const uint32_t bar = mapa(&S.bd[par], rk);
-        st_async(mapa(&S.dn[par][0][lane], rk), ub, bar);
-        st_async(mapa(&S.dn[par][1][lane], rk), vb0, bar);
-        st_async(mapa(&S.dn[par][2][lane], rk), vb1, bar);
-      }
-      if (lane == 0 && has_l) {
-        const int rk = rank - 1;
-        const uint32_t bar = mapa(&S.bd[par], rk);
-        st_async(mapa(&S.rt[par][0][ty], rk), ub, bar);
-        st_async(mapa(&S.rt[par][1][ty], rk), vb0, bar);
-        st_async(mapa(&S.rt[par][2][ty], rk), vb1, bar);
-      }
-      if (tid == 0) mbar_expect_tx(&S.bd[par], dual_bytes);
-      __syncthreads();
-      // forward differences (rasters.py:144-155), zero where the edge leaves the mask
-      double ubx = shfl_dn(ub), vbx0 = shfl_dn(vb0), vbx1 = shfl_dn(vb1);
-      double uby = S.ub[tyd][lane], vby0 = S.vb0[tyd][lane], vby1 = S.vb1[tyd][lane];
-      if (has_r || (ty == kH - 1 && has_d)) {  // warp-uniform wait
-        mbar_wait(&S.bd[par], ph);
-        if (lane == kW - 1 && has_r) {
-          ubx = S.rt[par][0][ty]; vbx0 = S.rt[par][1][ty]; vbx1 = S.rt[par][2][ty];
-        }
-        if (ty == kH - 1 && has_d) {
-          uby = S.dn[par][0][lane]; vby0 = S.dn[par][1][lane]; vby1 = S.dn[par][2][lane];
-        }
-      }
-      const double gxx = ex ? ubx - ub : 0.0, gyy = ey ? uby - ub : 0.0;
-      const double g00 = ex ? vbx0 - vb0 : 0.0, g01 = ey ? vby0 - vb0 : 0.0;
-      const double g10 = ex ? vbx1 - vb1 : 0.0, g11 = ey ? vby1 - vb1 : 0.0;
-      dual_update_exact<double>(a, b, c, sp, sq, gxx, gyy, g00, g01, g10, g11, vb0, vb1, p0, p1,
-                                q0, q1, q2, q3, heps);
-      const double fx0 = ex ? a * p0 + b * p1 : 0.0;
-      const double fy0 = ey ? b * p0 + c * p1 : 0.0;
-      const double fx1 = ex ? q0 : 0.0, fy1 = ey ? q1 : 0.0;
-      const double fx2 = ex ? q2 : 0.0, fy2 = ey ? q3 : 0.0;
-      S.fy[0][ty][lane] = fy0;
-      S.fy[1][ty][lane] = fy1;
-      S.fy[2][ty][lane] = fy2;
-      if (ty == kH - 1 && has_d) {
-        const int rk = rank + CX;
-        const uint32_t bar = mapa(&S.bp[par], rk);
-        st_async(mapa(&S.up[par][0][lane], rk), fy0, bar);
-        st_async(mapa(&S.up[par][1][lane], rk), fy1, bar);
-        st_async(mapa(&S.up[par][2][lane], rk), fy2, bar);
-      }
-      if (lane == kW - 1 && has_r) {
-        const int rk = rank + 1;
-        const uint32_t bar = mapa(&S.bp[par], rk);
-        st_async(mapa(&S.lf[par][0][ty], rk), fx0, bar);
-        st_async(mapa(&S.lf[par][1][ty], rk), fx1, bar);
-        st_async(mapa(&S.lf[par][2][ty], rk), fx2, bar);
-      }
-      if (tid == 0) mbar_expect_tx(&S.bp[par], primal_bytes);
-      __syncthreads();
-      // backward divergence (rasters.py:158-172); no pixel left of / above the
-      // image: zero fluxes there
-      double lx0 = shfl_up(fx0), lx1 = shfl_up(fx1), lx2 = shfl_up(fx2);
-      if (lane == 0) lx0 = lx1 = lx2 = 0.0;
-      double uy0 = 0.0, uy1 = 0.0, uy2 = 0.0;
-      if (ty > 0) {
-        uy0 = S.fy[0][ty - 1][lane]; uy1 = S.fy[1][ty - 1][lane]; uy2 = S.fy[2][ty - 1][lane];
-      }
-      if (has_l || (ty == 0 && has_u)) {
-        mbar_wait(&S.bp[par], ph);
-        if (lane == 0 && has_l) {
-          lx0 = S.lf[par][0][ty]; lx1 = S.lf[par][1][ty]; lx2 = S.lf[par][2][ty];
-        }
-        if (ty == 0 && has_u) {
-          uy0 = S.up[par][0][lane]; uy1 = S.up[par][1][lane]; uy2 = S.up[par][2][lane];
-        }
-      }
-      const double dvv = ((fx0 - lx0) + fy0) - uy0;
-      const double dd0 = ((fx1 - lx1) + fy1) - uy1;
-      const double dd1 = ((fx2 - lx2) + fy2) - uy2;
-      primal_update_exact<double>(dvv, dd0, dd1, tu, tv, g, rh, uo, p0, p1, lam, alpha0, alpha1,
-                                  theta, u, v0, v1, ub, vb0, vb1);
-    }
+    const PdConst C{a, b, c, sp, tu, tv, g, rh, uo, ex, ey};
+    pd_cycles<kH>(S, E, C, Q, A.K, cyc, u, v0, v1, p0, p1, q0, q1, q2, q3);
     // ---- clip and accumulate (solver.py:356-360)
     if (in && m) {
       const double du = fmin(fmax(u - uo, -A.du_max), A.du_max);
