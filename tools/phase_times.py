@@ -17,5 +17,8 @@ for lvl in range(prm.pyramid_levels):
     eng.time_phases(lvl)
     t = eng.time_phases(lvl)
     nw = t["warps"]
+    if nw == 0:  # k64_level: the whole level is one launch
+        print(f"level {t['w']}x{t['h']}: one whole-level launch (k64_level)")
+        continue
     print(f"level {t['w']}x{t['h']}: prologue {t['sample_ms'] * 1e3 / nw:7.1f} us/warp, "
           f"PD {t['pd_ms'] * 1e3 / nw:7.1f} us/warp ({t['pd_launches_per_warp']} launches)")
