@@ -375,3 +375,30 @@ def test_randomized_configurations(seed):
     if sol.mask.any():
         e = np.abs(r32.u - sol.u)[sol.mask]
         assert np.median(e) <= 1e-3 and np.percentile(e, 99) <= 1e-2, (np.median(e), np.percentile(e, 99))
+
+
+def test_ragged_size_cluster_kernels_parity():
+    """A 614x452 unified pair (even width, not a multiple of 32; height not a
+    multiple of 8; >= 512^2 pixels): the finest level runs k64_ctile with
+    regions and CTA tiles hanging over the right and bottom edges, 307x226
+    (odd width) the k64_tile fallback, 77x57 the whole-level k64_level with a
+    partly filled cluster. Without diagnostics (the default kernels) and with
+    them (the DIAG variants, no k64_level), against the oracle."""
+    from paper_1909_07545_b200.camera import RelativePose, StereoRig, UnifiedCamera
+    from paper_1909_07545_b200.solver import SolverParams, solve_pyramid
+    cam0 = UnifiedCamera(width=614, height=452, fx=262.0, fy=263.0, cx=306.4, cy=225.6,
+                         fov=np.pi, xi=0.9)
+    cam1 = UnifiedCamera(width=614, height=452, fx=262.0, fy=263.0, cx=307.1, cy=225.1,
+                         fov=np.pi, xi=0.9)
+    rig = StereoRig(cam0, cam1, RelativePose.from_displacement((0.1, 0.01, 0.0),
+                                                               rotvec=(0.0, 0.02, 0.005)))
+    prm = SolverParams(warp_iters=3, pd_iters=10, pyramid_levels=4, min_width=40)
+    i0, i1 = _render_pair(rig)
+    sol = O.pyramid_solve(i0, i1, rig, prm)
+    for diag in (False, True):
+        res = solve_pyramid(i0, i1, rig, prm, collect_diagnostics=diag, precision="fp64")
+        np.testing.assert_array_equal(res.mask, sol.mask)
+        err = float(np.max(np.abs(res.u - sol.u)[sol.mask]))
+        werr = float(np.max(np.abs(res.w - sol.w)[sol.mask]))
+        print(f"diag={diag}: u max err {err:.3e}, w max err {werr:.3e}")
+        assert err <= 1e-8 and werr <= 1e-8
