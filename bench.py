@@ -239,19 +239,23 @@ class ClockSampler:
 
 
 def profiled_traffic(pattern: str):
-    """DRAM bytes per launch of a kernel from its committed ncu capture."""
+    """DRAM bytes per launch of a kernel from its committed ncu capture (the
+    first dram__bytes_read / _write lines of the newest matching summary)."""
     caps = sorted((ROOT / "profiles").glob(pattern))
     if not caps:
         return None, None
-    rd = wr = None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    vals = {}
     for line in caps[-1].read_text().splitlines():
-        if line.startswith("dram__bytes_read.sum"):
-            rd = float(line.split("=")[1])
-        if line.startswith("dram__bytes_write.sum"):
-            wr = float(line.split("=")[1])
-    if rd is None or wr is None:
+        line = line.strip()
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            if line.startswith(key + " ") and key not in vals:
+                unit = line[line.index("[") + 1:line.index("]")]
+                vals[key] = float(line.split("=")[1]) * scale.get(unit, float("nan"))
+    if len(vals) != 2:
         return None, None
-    return (rd + wr) * 1e6, f"ncu --set full, profiles/{caps[-1].name} (Mbyte read + write)"
+    return (sum(vals.values()),
+            f"ncu --set full, profiles/{caps[-1].name} (dram bytes read + write)")
 
 
 def measured_peak():
