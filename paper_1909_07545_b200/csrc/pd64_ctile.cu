@@ -90,29 +90,6 @@ constexpr size_t smem_bytes() { return sizeof(SmemC<kH>) + 128; }
 
 FSB_INLINE double shfl_dn(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 FSB_INLINE double shfl_up(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
-// Cluster barrier without a release fence: it only has to publish the
-// mbarrier initialisation, which fence.mbarrier_init.release.cluster orders
-// (a release arrive costs a MEMBAR.GPU).
-FSB_INLINE void cluster_arrive_relaxed() {
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-}
-FSB_INLINE void cluster_wait() {
-  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-}
-// the same shared-memory location in CTA `rank` of the cluster
-FSB_INLINE uint32_t mapa(const void* p, int rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-  return r;
-}
-// store into another CTA's shared memory, counted on its mbarrier (no fence:
-// the receiver's mbarrier wait orders it)
-FSB_INLINE void st_async(uint32_t raddr, double v, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(
-                   raddr),
-               "d"(v), "r"(rbar)
-               : "memory");
-}
 
 // kH rows per CTA: 16 (512 threads, 2 CTAs per SM), 8 (256 threads, 4 per SM) or 4
 template <int R, int CX, int CY, int kH, bool DIAG>

@@ -1,7 +1,7 @@
 // k64_level: the whole warp loop of a small float64 pyramid level in one
 // cluster launch.
 //
-// On the small levels (C3: 64^2, 128^2) every warp is four dependent launches
+// On the small levels (C3: 64^2) every warp is four dependent launches
 // (sampling, linearisation, two primal-dual launches) over a grid that fills a
 // fraction of the GPU, so a warp costs launch and memory latencies, not work.
 // Here one cluster of up to 16 CTAs holds the whole level: each CTA one
@@ -52,21 +52,6 @@ struct LvlSmem {
 
 FSB_INLINE double shfl_dn(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 FSB_INLINE double shfl_up(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
-FSB_INLINE void cluster_sync_rel_acq() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n"
-               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-FSB_INLINE uint32_t mapa(const void* p, int rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-  return r;
-}
-FSB_INLINE void st_async(uint32_t raddr, double v, uint32_t rbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(
-                   raddr),
-               "d"(v), "r"(rbar)
-               : "memory");
-}
 
 // A CTA's place in its cluster and the neighbours it exchanges with.
 struct Nbr {

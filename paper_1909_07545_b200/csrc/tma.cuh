@@ -71,4 +71,31 @@ FSB_INLINE void bulk_wait_read0() {
 // every committed store is complete
 FSB_INLINE void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// ---- cluster helpers (k64_ctile, k64_level)
+// release / acquire cluster barrier (a MEMBAR.GPU per use: not for inner loops)
+FSB_INLINE void cluster_sync_rel_acq() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// Cluster barrier without a release fence: enough to publish mbarrier
+// initialisation, which fence.mbarrier_init.release.cluster orders.
+FSB_INLINE void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+FSB_INLINE void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+// the same shared-memory location in CTA `rank` of the cluster
+FSB_INLINE uint32_t mapa(const void* p, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// store into another CTA's shared memory, counted on its mbarrier (no fence:
+// the receiver's mbarrier wait orders it)
+FSB_INLINE void st_async(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(
+                   raddr),
+               "d"(v), "r"(rbar)
+               : "memory");
+}
+
 }  // namespace fsb
