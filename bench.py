@@ -675,8 +675,9 @@ def run_b200(a) -> None:
                "api": "paper_1909_07545_b200.solve_pyramid (float64 host arrays in, "
                       "StereoResult of float64 / bool host arrays out; default precision)",
                "timer": "host wall clock around each API call: host copy into pinned "
-                        "staging, H2D of i0 / i1 (float64), graph replay, D2H of u, w, v, "
-                        "mask, i1_calibrated into pinned output buffers"}
+                        "staging, H2D of i0 / i1 (float64), graph replay, D2H of u, w, v "
+                        "after the frame and of mask, i1_calibrated during it (side stream "
+                        "behind the graph's early-output event) into pinned output buffers"}
     roof = pro = None
     if rank == 0:
         roof, pro = pd64_roofline(eng, prm)

@@ -387,6 +387,15 @@ int fsb_graph_create_f64(const fsb_rig* rig, const fsb_params* prm, const double
                          int64_t* n_kernels);
 int fsb_graph_launch(fsb_graph* graph, void* stream);
 int fsb_graph_destroy(fsb_graph* graph);
+/* float64 graphs: an event (cudaEvent_t, owned by the graph; NULL for float32
+ * graphs) that each replay records as soon as `mask` and `i1c` hold their final
+ * values (after the calibration, long before u / w / v), so the host can copy
+ * those two outputs out while the frame is still solving. No reference
+ * counterpart: an API-level latency optimisation of solve_pyramid's outputs
+ * (solver.py:451-452). */
+void* fsb_graph_early_event(fsb_graph* graph);
+/* cudaStreamWaitEvent(stream, event, 0) for callers without a CUDA binding. */
+int fsb_stream_wait_event(void* stream, void* event);
 
 /* ---------------------------------------------------------------- synthetic inputs */
 

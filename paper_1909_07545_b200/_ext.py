@@ -35,7 +35,7 @@ EXPORTED = (
     "fsb_upsample_state", "fsb_compute_tensor", "fsb_precondition_steps", "fsb_level_partials", "fsb_level_tiles", "fsb_level_setup", "fsb_warp_linearize",
     "fsb_pd_iterate", "fsb_thresholding_step", "fsb_warp_finish", "fsb_solve_level", "fsb_diag_counts",
     "fsb_solve_pyramid_workspace_bytes", "fsb_solve_pyramid",
-    "fsb_solve_pyramid_f64_workspace_bytes", "fsb_solve_pyramid_f64", "fsb_render", "fsb_graph_create", "fsb_graph_create_f64", "fsb_graph_launch", "fsb_graph_destroy",
+    "fsb_solve_pyramid_f64_workspace_bytes", "fsb_solve_pyramid_f64", "fsb_render", "fsb_graph_create", "fsb_graph_create_f64", "fsb_graph_launch", "fsb_graph_destroy", "fsb_graph_early_event", "fsb_stream_wait_event",
     "fsb_warp_linearize_f64_scratch_bytes", "fsb_warp_linearize_f64",
     "fsb_phase_timer_create", "fsb_phase_timer_read", "fsb_phase_timer_destroy",
     "fsb_solve_pyramid_f64_timed",
@@ -173,6 +173,8 @@ def lib() -> C.CDLL:
                                                       vp, vp, vp, vp, vp, vp, vp]),
             "fsb_graph_launch": (C.c_int, [vp, vp]),
             "fsb_graph_destroy": (C.c_int, [vp]),
+            "fsb_graph_early_event": (C.c_void_p, [vp]),
+            "fsb_stream_wait_event": (C.c_int, [vp, vp]),
             "fsb_version": (C.c_char_p, []),
         }
         for name, (res, args) in sig.items():

@@ -809,6 +809,12 @@ bool params_ok64(const fsb_params* p) {
 
 }  // namespace
 
+// Event recorded inside a float64 graph capture once mask / i1c are final
+// (fsb_graph_create_f64 sets it around the capture; thread-local like the
+// capture mode).
+thread_local cudaEvent_t g_early_event = nullptr;
+void set_early_output_event64(cudaEvent_t ev) { g_early_event = ev; }
+
 size_t solve_pyramid64_bytes(const fsb_rig* rig, const fsb_params* prm) {
   if (!rig || !params_ok64(prm)) return 0;
   Plan64 P;
@@ -875,6 +881,9 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
   rc = calibrate64_internal(rig, i1, P.mask1, i1c, P.i1c_ok, P.iters + 2, st);
   if (rc) return rc;
   k64_and_mask<<<(unsigned)((n0 + 255) / 256), 256, 0, st>>>(P.mask0, P.i1c_ok, n0, P.solve_mask);
+  // mask and i1c are final here: publish them early (graph capture only)
+  cudaMemcpyAsync(mask_out, P.solve_mask, n0, cudaMemcpyDeviceToDevice, st);
+  if (g_early_event) cudaEventRecordWithFlags(g_early_event, st, cudaEventRecordExternal);
   P.lvl_i0[0] = const_cast<double*>(i0);
   P.lvl_i1[0] = i1c;
   P.lvl_mask[0] = P.solve_mask;
@@ -952,7 +961,6 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
       cudaMemcpyAsync(u_out, u, n0 * sizeof(double), cudaMemcpyDeviceToDevice, st);
       cudaMemcpyAsync(w_out, wv, 2 * n0 * sizeof(double), cudaMemcpyDeviceToDevice, st);
       k64_interleave<<<(unsigned)((n0 + 255) / 256), 256, 0, st>>>(P.setA + n0, n0, v_out);
-      cudaMemcpyAsync(mask_out, P.solve_mask, n0, cudaMemcpyDeviceToDevice, st);
     }
     cur ^= 1;
   }

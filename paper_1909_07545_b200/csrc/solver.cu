@@ -17,6 +17,10 @@
 #include "pd_args.cuh"
 
 namespace fsb {
+void set_early_output_event64(cudaEvent_t ev);  // pd64.cu
+}  // namespace fsb
+
+namespace fsb {
 
 // defined in the other translation units
 int trajectory_field_internal(const fsb_camera* cam, const double t[3], double eps_scale,
@@ -739,6 +743,7 @@ int fsb_solve_pyramid(const fsb_rig* rig, const fsb_params* prm, const float* i0
 struct fsb_graph {
   cudaGraph_t graph;
   cudaGraphExec_t exec;
+  cudaEvent_t early;  // float64 graphs: recorded once mask / i1c are final
 };
 
 }  // extern "C"
@@ -770,7 +775,7 @@ int capture_graph(void* stream, fsb_graph** out, int64_t* n_kernels, Enqueue enq
   cudaGraphExec_t ex = nullptr;
   e = cudaGraphInstantiate(&ex, g, 0);
   if (e != cudaSuccess) { cudaGraphDestroy(g); return (int)e; }
-  fsb_graph* G = new fsb_graph{g, ex};
+  fsb_graph* G = new fsb_graph{g, ex, nullptr};
   *out = G;
   if (n_kernels) *n_kernels = k;
   return FSB_OK;
@@ -796,10 +801,21 @@ int fsb_graph_create_f64(const fsb_rig* rig, const fsb_params* prm, const double
                          double* u, double* w, double* v, uint8_t* mask, double* i1c,
                          const fsb_diag* diag, void* stream, fsb_graph** out,
                          int64_t* n_kernels) {
-  return capture_graph(stream, out, n_kernels, [&](cudaStream_t st) {
+  cudaEvent_t early = nullptr;
+  cudaError_t e = cudaEventCreateWithFlags(&early, cudaEventDisableTiming);
+  if (e != cudaSuccess) return (int)e;
+  fsb::set_early_output_event64(early);  // recorded inside the capture (pd64.cu)
+  const int rc = capture_graph(stream, out, n_kernels, [&](cudaStream_t st) {
     return fsb_solve_pyramid_f64(rig, prm, i0, i1, traj_dirs, traj_ok, workspace,
                                  workspace_bytes, u, w, v, mask, i1c, diag, st);
   });
+  fsb::set_early_output_event64(nullptr);
+  if (rc) {
+    cudaEventDestroy(early);
+    return rc;
+  }
+  (*out)->early = early;
+  return FSB_OK;
 }
 
 int fsb_graph_launch(fsb_graph* G, void* stream) {
@@ -812,8 +828,17 @@ int fsb_graph_destroy(fsb_graph* G) {
   if (!G) return FSB_OK;
   cudaGraphExecDestroy(G->exec);
   cudaGraphDestroy(G->graph);
+  if (G->early) cudaEventDestroy(G->early);
   delete G;
   return FSB_OK;
+}
+
+void* fsb_graph_early_event(fsb_graph* G) { return G ? (void*)G->early : nullptr; }
+
+int fsb_stream_wait_event(void* stream, void* event) {
+  if (!event) return FSB_EINVAL;
+  const cudaError_t e = cudaStreamWaitEvent(as_stream(stream), (cudaEvent_t)event, 0);
+  return e == cudaSuccess ? FSB_OK : (int)e;
 }
 
 const char* fsb_version(void) { return "fsb200 0.1 sm_100a"; }

@@ -475,6 +475,7 @@ class Solver:
         self._traj = None
         self._host = None
         self._out_pool: list = []  # pinned output sets (see _out_set)
+        self._early_stream = None   # D2H of mask / i1c during the frame (_solve)
         self.graph = None
         self.kernels_per_frame = None
 
@@ -646,15 +647,32 @@ class Solver:
             self.run()
         st = self._out_set()
         outs = {}
+        # float64 graphs record an event once mask and i1c are final: those two
+        # go out on a side stream while the frame is still solving
+        early = (_ext.lib().fsb_graph_early_event(self.graph)
+                 if self._traj is None and self.graph else None)
+        side = None
+        if early:
+            if self._early_stream is None:
+                self._early_stream = torch.cuda.Stream()
+            side = self._early_stream
+            _ext.check(_ext.lib().fsb_stream_wait_event(C.c_void_p(side.cuda_stream),
+                                                        C.c_void_p(early)), "stream_wait_event")
         for k, dt in self._OUT:
             src = getattr(self, k)
             # fp64 engines: every output is already float64 on the device and the
             # uint8 0/1 mask is viewed as bool, so no conversion kernel runs;
             # fp32 engines widen u / w / v / i1c on the device first.
             src = src.view(torch.bool) if dt == torch.bool else src.to(dt)
-            st[k][0].copy_(src, non_blocking=True)
+            if side is not None and k in ("mask", "i1c"):
+                with torch.cuda.stream(side):
+                    st[k][0].copy_(src, non_blocking=True)
+            else:
+                st[k][0].copy_(src, non_blocking=True)
             outs[k] = st[k][1].view()
         torch.cuda.current_stream().synchronize()
+        if side is not None:
+            side.synchronize()
         diag = None
         if self.diag is not None:
             diag = Diagnostics(du_max_limit=self.params.du_max)

@@ -11,7 +11,7 @@ ROOT = Path(__file__).resolve().parent.parent
 
 def header_symbols():
     text = (ROOT / "include" / "fsb200.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(fsb_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*|void\*)\s+(fsb_\w+)\(", text, re.M)))
 
 
 def test_header_matches_binding_list():
@@ -96,8 +96,8 @@ def test_binding_arity_matches_header():
     from paper_1909_07545_b200 import _ext
     L = _ext.lib()
     text = (ROOT / "include" / "fsb200.h").read_text()
-    decls = re.findall(r"^\s*(?:int|size_t|const char\*)\s+(fsb_\w+)\(([^;]*)\);", text,
-                       re.M | re.S)
+    decls = re.findall(r"^\s*(?:int|size_t|const char\*|void\*)\s+(fsb_\w+)\(([^;]*)\);",
+                       text, re.M | re.S)
     assert len(decls) == len(header_symbols())
     bad = []
     for name, args in decls:
