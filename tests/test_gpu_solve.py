@@ -110,10 +110,16 @@ def test_determinism_and_graph_replay(precision):
     eng.run()  # direct enqueue, no graph
     torch.cuda.synchronize()
     r3 = type(r1)(u=eng.u.cpu().numpy(), w=eng.w.cpu().numpy(), v=eng.v.cpu().numpy(),
-                  mask=eng.mask.cpu().numpy().astype(bool), i1_calibrated=None)
+                  mask=eng.mask.cpu().numpy().astype(bool),
+                  i1_calibrated=eng.i1c.double().cpu().numpy())
     for a, b in ((r1, r2), (r1, r3)):
         assert np.array_equal(a.u, b.u) and np.array_equal(a.w, b.w)
         assert np.array_equal(a.v, b.v) and np.array_equal(a.mask, b.mask)
+        # mask / i1_calibrated of the float64 graph leave early, on a side stream
+        assert np.array_equal(a.i1_calibrated, b.i1_calibrated)
+    from paper_1909_07545_b200 import _ext
+    early = _ext.lib().fsb_graph_early_event(eng.graph)
+    assert (early is not None) == (precision == "fp64")
 
 
 def test_api_errors():
