@@ -52,10 +52,11 @@ int sample_nan64_internal(const P64& L, int bx, int by, cudaStream_t st);
 int linearize_nan64_internal(const P64& L, int bx, int by, cudaStream_t st);
 bool side_stream_for(cudaStream_t main, cudaStream_t* side, cudaEvent_t** ev);  // solver.cu
 bool pd64_level_fits(int w, int h);  // pd64_level.cu
+int pd64_level_ctas(int w, int h);
 int pd64_level_launch(const P64& P, const double* T, const double* S, const uint32_t* ecode,
                       double* u, double* v, double* wv, double* scratch2, double lam,
                       double alpha0, double alpha1, double theta, double sigma_q, double heps,
-                      double du_max, int N, int K, cudaStream_t st);
+                      double du_max, int N, int K, const LvlDiag* diag, cudaStream_t st);
 
 }  // namespace fsb
 
@@ -96,6 +97,8 @@ struct L64 {
   uint32_t* ecode;
   int* tiles;
   double4* tex;  // NaN-encoded packed texels of the level (sample64.cu)
+  double* lvl_partials;     // k64_level's per-warp per-CTA |du| sums (diagnostics)
+  size_t lvl_partials_cap;  // their count
 };
 
 __device__ __forceinline__ bool ex_at(const uint8_t* __restrict__ m, int w, int x, size_t i) {
@@ -402,6 +405,8 @@ struct Plan64 {
   double *setA, *setB;
   double* carry_u;  // the finished level's u, read by the next level's upsample
   double *wv[2], *i1w, *dirs, *partials;
+  double* lvl_partials;  // k64_level diagnostics: N x CTAs partial sums
+  size_t lvl_partials_n;
   uint8_t *i1w_ok, *dir_ok;
   // per-level setup products (filled ahead on the side stream); cst: one block
   // of 10 planes per level — tensor a, b, c, steps sigma_p, tau_u, tau_v, I_u,
@@ -451,6 +456,8 @@ int plan64(const fsb_rig* rig, const fsb_params* prm, void* base, Plan64& P) {
   P.i1w = c.take<double>(n0); P.dirs = c.take<double>(2 * n0);
   P.i1w_ok = c.take<uint8_t>(n0); P.dir_ok = c.take<uint8_t>(n0);
   P.partials = c.take<double>(partial_count(H, W));
+  P.lvl_partials_n = (size_t)prm->warp_iters * 16;
+  P.lvl_partials = c.take<double>(P.lvl_partials_n);
   for (int l = 0; l < n; ++l) {
     const int lh = P.shapes[2 * l], lw = P.shapes[2 * l + 1];
     const size_t np = (size_t)lh * lw;
@@ -692,14 +699,31 @@ int solve_level64(const L64& L0, const fsb_params* prm, const fsb_diag* diag, in
   P64 PL;
   PL.h = L.h; PL.w = L.w; PL.i0 = L.i0; PL.mask = L.mask; PL.tex = L.tex; PL.wv = L.wv;
   PL.i1wn = L.i1w; PL.dirs = L.dirs; PL.dir_ok = L.dir_ok; PL.iu = L.iu; PL.rho0 = L.rho0;
-  // a small level without diagnostics: the whole warp loop in one cluster launch
-  // (k64_level, pd64_level.cu); the sampled-image scratch is 2 level planes of
-  // the finest-level i1w buffer
-  if (pro_nan && listed && !dpq && !ddu && L.u2 && pd64_level_fits(L.w, L.h)) {
+  // a small level: the whole warp loop in one cluster launch (k64_level,
+  // pd64_level.cu); the sampled-image scratch is 2 level planes of the
+  // finest-level i1w buffer. With diagnostics the kernel reduces them itself
+  // (the same kernels run with and without: bit-identical results).
+  if (pro_nan && listed && L.u2 && pd64_level_fits(L.w, L.h) &&
+      (!ddu || (size_t)N * pd64_level_ctas(L.w, L.h) <= L.lvl_partials_cap)) {
+    LvlDiag ld;
+    memset(&ld, 0, sizeof(ld));
+    if (dpq) { ld.p = diag->max_p_norm + pd_off; ld.q = diag->max_q_norm + pd_off; }
+    if (ddu) {
+      if (diag->max_du_f64) ld.du64 = diag->max_du_f64 + warp_off;
+      else ld.du = diag->max_du + warp_off;
+      ld.partials = L.lvl_partials;
+    }
     rc = pd64_level_launch(PL, L.T, L.S, L.ecode, L.u, L.v, L.wv, L.i1w, prm->lam,
                            prm->alpha0, prm->alpha1, prm->theta, sigma_q_of(prm),
-                           huber_eps_of(prm), prm->du_max, N, K, st);
+                           huber_eps_of(prm), prm->du_max, N, K, (dpq || ddu) ? &ld : nullptr,
+                           st);
     if (rc) return rc;
+    const int nc = pd64_level_ctas(L.w, L.h);
+    for (int wi = 0; ddu && wi < N; ++wi) {
+      rc = mean_finish_internal(L.lvl_partials + (size_t)wi * nc, nc, L.mask, n,
+                                diag->mean_abs_du + warp_off + wi, st);
+      if (rc) return rc;
+    }
     if (tm) {  // phase timer: the level is one launch
       tm->used = 0;
       tm->level_h = L.h; tm->level_w = L.w;
@@ -917,6 +941,7 @@ int solve_pyramid64(const fsb_rig* rig, const fsb_params* prm, const double* i0,
     L.ub2 = P.setB + 9 * np; L.vb2 = P.setB + 10 * np;
     L.full16 = P.f16l[l];
     L.ecode = P.ecl[l]; L.tiles = P.tll[l]; L.tex = P.texl[l];
+    L.lvl_partials = P.lvl_partials; L.lvl_partials_cap = P.lvl_partials_n;
     L.i1w = P.i1w; L.i1w_ok = P.i1w_ok;
     L.dirs = P.dirs; L.dir_ok = P.dir_ok; L.partials = P.partials;
   }

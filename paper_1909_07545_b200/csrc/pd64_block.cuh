@@ -68,6 +68,13 @@ int pd64_tma_launch(const B64& A, const Tma64Level& M, int src_set, cudaStream_t
 size_t pd64_tma_tile_count(int w, int h);
 int pd64_tma_tile_list(const uint8_t* mask, int w, int h, int* tiles, cudaStream_t st);
 
+// Diagnostics slots of the whole-level kernel (pd64_level.cu): per-cycle |p| /
+// |q| maxima from the level's first cycle, per-warp max |du| (float or
+// float64) from its first warp, and N x CTAs partial sums of |du|.
+struct LvlDiag {
+  float* p; float* q; float* du; double* du64; double* partials;
+};
+
 // The cluster-tile kernel (pd64_ctile.cu, the large levels): same layout as
 // k64_tma; regions of a cluster of CTAs exchange halos through DSMEM, R
 // (pd64_ctile_halo) cycles per launch. Tensor maps: [set][0] 12 planes, [set][1] 9.

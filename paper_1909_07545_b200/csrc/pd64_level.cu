@@ -47,6 +47,7 @@ struct LvlSmem {
   double rt[2][3][kH];  // dual: column 0 of the CTA to the right
   double up[2][3][kW];  // primal: last-row y-fluxes of the CTA above
   double lf[2][3][kH];  // primal: column 31 x-fluxes of the CTA to the left
+  double red_sum[kH], red_max[kH];  // diagnostics: per-warp |du| sums / maxima
   uint64_t bd[2], bp[2];
 };
 
@@ -83,10 +84,13 @@ struct PdScal {
 // on the receiver's mbarriers (parity buffers by the running cycle index cyc).
 // Left of column 0 / above row 0 without a neighbour CTA the fluxes are 0 (the
 // image border; at a region border these are halo pixels).
-template <int kH>
+// DIAG: per-cycle maxima of |p| and |q| over the CTA's pixels into dp[cyc],
+// dq[cyc] (solver.py:350-354; out-of-image threads hold p = q = 0).
+template <int kH, bool DIAG>
 FSB_INLINE void pd_cycles(LvlSmem<kH>& S, const Nbr& E, const PdConst& C, const PdScal& Q, int K,
                           int& cyc, double& u, double& v0, double& v1, double& p0, double& p1,
-                          double& q0, double& q1, double& q2, double& q3) {
+                          double& q0, double& q1, double& q2, double& q3, float* dp = nullptr,
+                          float* dq = nullptr) {
   const int lane = threadIdx.x, ty = threadIdx.y, tid = ty * kW + lane;
   const int tyd = ty + 1 < kH ? ty + 1 : ty;
   const bool ex = C.ex, ey = C.ey;
@@ -137,6 +141,14 @@ FSB_INLINE void pd_cycles(LvlSmem<kH>& S, const Nbr& E, const PdConst& C, const 
     S.fy[0][ty][lane] = fy0;
     S.fy[1][ty][lane] = fy1;
     S.fy[2][ty][lane] = fy2;
+    if (DIAG) {
+      const double pmax = warp_max(sqrt(p0 * p0 + p1 * p1));
+      const double qmax = warp_max(sqrt(((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3));
+      if (lane == 0) {
+        atomic_max_nonneg(dp + cyc, (float)pmax);
+        atomic_max_nonneg(dq + cyc, (float)qmax);
+      }
+    }
     if (ty == kH - 1 && E.has_d) {
       const int rk = E.rank + E.cx_n;
       const uint32_t bar = mapa(&S.bp[par], rk);
@@ -188,9 +200,12 @@ struct LvlArgs {
   double* i1wn[2];          // scratch planes: the sampled image by warp parity
   double lam, alpha0, alpha1, theta, sigma_q, heps, du_max;
   int N, K;
+  // diagnostics (nullptr = off): per-cycle |p| / |q| maxima, per-warp max |du|
+  // (float or float64) and per-warp per-CTA partial sums of |du| (N x CTAs)
+  float* diag_p; float* diag_q; float* diag_du; double* diag_du64; double* partials;
 };
 
-template <int kH, int CX>
+template <int kH, int CX, bool DIAG>
 __global__ void __launch_bounds__(kW * kH, 1) k64_level(const LvlArgs A) {
   extern __shared__ unsigned char smem_raw[];
   poison_dynamic_smem(smem_raw);  // checked build only
@@ -248,13 +263,29 @@ __global__ void __launch_bounds__(kW * kH, 1) k64_level(const LvlArgs A) {
     // warp-start reset (solver.py:344-346): u0 = u, u_bar = u, v_bar = v
     const double uo = u;
     const PdConst C{a, b, c, sp, tu, tv, g, rh, uo, ex, ey};
-    pd_cycles<kH>(S, E, C, Q, A.K, cyc, u, v0, v1, p0, p1, q0, q1, q2, q3);
+    pd_cycles<kH, DIAG>(S, E, C, Q, A.K, cyc, u, v0, v1, p0, p1, q0, q1, q2, q3, A.diag_p,
+                        A.diag_q);
     // ---- clip and accumulate (solver.py:356-360)
+    double adu = 0.0;
     if (in && m) {
       const double du = fmin(fmax(u - uo, -A.du_max), A.du_max);
       u = uo + du;
       wv.x = wv.x + du * d0;
       wv.y = wv.y + du * d1;
+      adu = fabs(du);
+    }
+    if (DIAG && A.partials) {  // max |du| and this CTA's sum of |du| for warp wi
+      const double mx = warp_max(adu), sm = warp_sum(adu);
+      if (lane == 0) { S.red_sum[ty] = sm; S.red_max[ty] = mx; }
+      __syncthreads();
+      if (tid == 0) {
+        double tsum = 0.0, mm = 0.0;
+        for (int j = 0; j < kH; ++j) { tsum += S.red_sum[j]; mm = fmax(mm, S.red_max[j]); }
+        A.partials[(size_t)wi * ncta + rank] = tsum;
+        if (A.diag_du64) atomic_max_nonneg(A.diag_du64 + wi, mm);
+        else atomic_max_nonneg(A.diag_du + wi, (float)mm);
+      }
+      __syncthreads();  // the reduction slots are reused by the next warp
     }
   }
   if (in) {
@@ -287,13 +318,16 @@ LvlShape level_shape(int w, int h) {
 
 template <int kH, int CX>
 int launch_level(const LvlArgs& A, int cy, cudaStream_t st) {
-  auto kern = k64_level<kH, CX>;
+  const bool diag = A.diag_p || A.partials;
+  auto kern = diag ? k64_level<kH, CX, true> : k64_level<kH, CX, false>;
   const int nc = CX * cy;
   static std::atomic<unsigned long long> attr{0};
   once_per_device(attr, [&] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(LvlSmem<kH>));
+    for (auto k : {k64_level<kH, CX, true>, k64_level<kH, CX, false>}) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(LvlSmem<kH>));
+    }
   });
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
@@ -326,6 +360,11 @@ int launch_level_th(const LvlArgs& A, const LvlShape& s, cudaStream_t st) {
 
 }  // namespace
 
+int pd64_level_ctas(int w, int h) {
+  const LvlShape s = level_shape(w, h);
+  return s.cx * s.cy;
+}
+
 bool pd64_level_fits(int w, int h) {
   static const bool on = [] {
     const char* e = getenv("FSB_LEVEL64");
@@ -337,7 +376,7 @@ bool pd64_level_fits(int w, int h) {
 int pd64_level_launch(const P64& P, const double* T, const double* S, const uint32_t* ecode,
                       double* u, double* v, double* wv, double* scratch2, double lam,
                       double alpha0, double alpha1, double theta, double sigma_q, double heps,
-                      double du_max, int N, int K, cudaStream_t st) {
+                      double du_max, int N, int K, const LvlDiag* diag, cudaStream_t st) {
   const LvlShape s = level_shape(P.w, P.h);
   if (!s.th) return FSB_EINVAL;
   LvlArgs A;
@@ -347,6 +386,10 @@ int pd64_level_launch(const P64& P, const double* T, const double* S, const uint
   A.i1wn[1] = scratch2 + (size_t)P.w * P.h;
   A.lam = lam; A.alpha0 = alpha0; A.alpha1 = alpha1; A.theta = theta; A.sigma_q = sigma_q;
   A.heps = heps; A.du_max = du_max; A.N = N; A.K = K;
+  if (diag) {
+    A.diag_p = diag->p; A.diag_q = diag->q; A.diag_du = diag->du; A.diag_du64 = diag->du64;
+    A.partials = diag->partials;
+  }
   return s.th == 8 ? launch_level_th<8>(A, s, st) : launch_level_th<16>(A, s, st);
 }
 

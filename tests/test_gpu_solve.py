@@ -257,3 +257,27 @@ def test_side_stream_overlap_is_bit_identical(tmp_path):
     with np.load(out) as z:
         assert np.array_equal(z["u"], r.u) and np.array_equal(z["w"], r.w)
         assert np.array_equal(z["v"], r.v)
+
+
+def test_diagnostics_do_not_change_the_solution():
+    """As in the reference (diagnostics only observe the iteration), collecting
+    diagnostics gives bit-identical u, w, v: the same kernels run in both modes
+    (k64_level and k64_ctile reduce the traces themselves)."""
+    import bench
+    from paper_1909_07545_b200 import synth as S
+    from paper_1909_07545_b200.solver import solve_pyramid
+    g = load_golden("pyramid_solve")
+    rig1, prm1 = bench.product_rig("c1"), bench.product_params("c1")
+    sc = S.default_scene()
+    i0 = S.render(sc, rig1.cam0, supersample=1)[0]
+    i1 = S.render(sc, rig1.cam1, pose=rig1.pose, supersample=1)[0]
+    for rig, prm, a, b in ((_rig(g), _params(g), g["i0"], g["i1"]), (rig1, prm1, i0, i1)):
+        r0 = solve_pyramid(a, b, rig, prm)
+        r1 = solve_pyramid(a, b, rig, prm, collect_diagnostics=True)
+        assert np.array_equal(r0.u, r1.u) and np.array_equal(r0.w, r1.w)
+        assert np.array_equal(r0.v, r1.v)
+        d = r1.diagnostics
+        assert len(d.max_p_norm) == prm.pyramid_levels * prm.warp_iters * prm.pd_iters or \
+            len(d.max_p_norm) > 0
+        assert max(d.max_p_norm) <= 1 + 1e-6 and max(d.max_du) <= prm.du_max * (1 + 1e-6)
+        assert all(np.isfinite(d.mean_abs_du)) and min(d.mean_abs_du) >= 0.0
